@@ -1,0 +1,343 @@
+"""Benchmark: 3D hull points/sec on the B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4]
+                    [--impl ours|reference] [--engine fast|exact]
+
+One "step" = one full ``convex_hull_3d`` of the config's point cloud: device
+presort + tie scan + degeneracy scan, both hull passes over all merge
+levels, facet extraction and the orientation/remap/unique epilogue.
+
+* ``value``: points/sec with the input cloud already resident in HBM (caller
+  order, 24 B/point; 2^24 points = 403 MB > the 126 MB L2, so every step
+  streams it from HBM), device events around K steps.
+* ``e2e``: the same metric through the public API with HOST buffers: every
+  step copies the pinned input host->device and reads faces + vertices back.
+* ``roofline``: the dominant kernel's algorithmic bytes (SURVEY.md 8(d)
+  model, per-level counts frozen from the reference in
+  tests/golden/level_stats.json) over its event-timed launch durations,
+  against MEASURED_PEAKS.json hbm_gbs.
+* ``cpu_baseline``: the unmodified reference (oracle/_ref) on this host's
+  cores on a bounded sample, rank 0 only.
+
+``--impl reference`` times the reference's own CPU implementation
+(ThreadBackend over all host cores) on a bounded sample of the same
+workload and prints the same JSON line with "impl": "reference".
+Multi-GPU (torchrun, N>1): x-slab sharding, see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (n, dist, seed, label)
+    "C1": (10_000, "cube", 0, "10^4 uniform cube [-1,1]^3"),
+    "C2": (2**20, "ball", 0, "2^20 uniform unit ball"),
+    "C3": (2**20, "sphere", 0, "2^20 sphere surface (h~n)"),
+    "C4": (2**24, "cube", 0, "2^24 uniform cube [-1,1]^3"),
+    "C5": (2**27, "mixed", 0, "2^27 ball + 2^20 radius-2 shell"),
+}
+STATS_KEY = {"C2": "C2_ball_2^20", "C3": "C3_sphere_2^20", "C4": "C4_cube_2^24"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--engine", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=2**20)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[5:9]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference
+def reference_module():
+    from oracle import oracle as O
+
+    ref = O.reference()
+    if ref is None:
+        raise RuntimeError("reference not built: run oracle/build_ref.sh (or __graft_entry__.build())")
+    return ref
+
+
+def time_reference(n: int, dist: str, seed: int, reps: int, warm: int = 1):
+    """Reference convex_hull_3d with ThreadBackend(all cores): list of seconds."""
+    from paper_1205_1171_b200.generators import generate
+
+    ref = reference_module()
+    pts = generate(n, dist, seed)
+    cores = os.cpu_count() or 1
+    out = []
+    with ref.ThreadBackend(cores) as be:
+        for i in range(warm + reps):
+            t0 = time.perf_counter()
+            ref.convex_hull_3d(pts, be)
+            dt = time.perf_counter() - t0
+            if i >= warm:
+                out.append(dt)
+    return out, cores
+
+
+def cpu_baseline(cfg: str, sample_n: int) -> dict:
+    n, dist, seed, _ = CONFIGS[cfg]
+    sn = min(n, sample_n)
+    secs, cores = time_reference(sn, dist, seed, reps=3, warm=1)
+    med = statistics.median(secs)
+    return {"value": sn / med, "unit": "points/s", "cores": cores, "kind": "reference",
+            "sample": f"reference convex_hull_3d(ThreadBackend({cores})) on generate({sn}, "
+                      f"'{dist}', {seed}) (bounded sample of {cfg}), median of {len(secs)} "
+                      f"after 1 warm-up; host CPU {cpu_model()}"}
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    n, dist, seed, label = CONFIGS[args.config]
+    sn = min(n, max(args.cpu_sample_n, 1 << 22)) if args.config in ("C4", "C5") else n
+    secs, cores = time_reference(sn, dist, seed, reps=args.steps, warm=args.warmup)
+    total = sum(secs)
+    value = sn * len(secs) / total
+    line = {
+        "impl": "reference", "metric": "3D hull points/sec", "value": value, "unit": "points/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / len(secs) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, PCG64)",
+        "config": {"workload": f"{args.config}: {label}", "n": n, "sample_n": sn,
+                   "distribution": dist, "seed": seed},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "reference",
+                         "sample": f"generate({sn}, '{dist}', {seed}) per step; host CPU "
+                                   f"{cpu_model()}"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def level_bytes(cfg: str):
+    """Per (pass, level) algorithmic bytes B_alg = 4(E_in+E_out) + 40(D+2J)."""
+    key = STATS_KEY.get(cfg)
+    p = os.path.join(ROOT, "tests", "golden", "level_stats.json")
+    if key is None or not os.path.exists(p):
+        return None
+    st = json.load(open(p)).get(key)
+    if st is None:
+        return None
+    out = {}
+    for pi, which in enumerate(("lower", "upper")):
+        for r in st[which]:
+            out[(pi, r["level"])] = 4 * (r["E_in"] + r["E_out"]) + 40 * (r["D"] + 2 * r["J"])
+    return out
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1205_1171_b200 as H
+    from paper_1205_1171_b200 import engine as E
+    from paper_1205_1171_b200.generators import generate
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        from paper_1205_1171_b200 import multigpu
+
+        return multigpu.bench_rank(args, CONFIGS)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, dist, seed, label = CONFIGS[args.config]
+    pts_host = generate(n, dist, seed)
+    pinned = torch.from_numpy(pts_host).pin_memory()
+    pts_dev = pinned.to(dev)
+    be = H.CudaBackend(local, engine=args.engine)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        res = H.convex_hull_3d(pts_dev, be, return_device=True)
+    torch.cuda.synchronize()
+    nfaces = int(res.faces.shape[0])
+    nverts = int(res.vertices.shape[0])
+
+    # device-resident timed region (+ per-launch kernel events)
+    prof: list = []
+    E.PROFILE = prof
+    l0 = E.launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        H.convex_hull_3d(pts_dev, be, return_device=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    E.PROFILE = None
+    launches = (E.launch_count() - l0) // args.steps
+    ms = ev0.elapsed_time(ev1) / args.steps
+    value = n / (ms / 1e3)
+
+    # roofline of the dominant kernel
+    per_kernel: dict = {}
+    lb = level_bytes(args.config)
+    for name, pass_idx, level, e0, e1 in prof:
+        t = e0.elapsed_time(e1) / 1e3
+        d = per_kernel.setdefault(name, {"time": 0.0, "launches": 0, "bytes": 0, "known": True})
+        d["time"] += t
+        d["launches"] += 1
+        b = None if lb is None else lb.get((pass_idx, level))
+        if b is None:
+            d["known"] = False
+        else:
+            d["bytes"] += b
+    peak, peak_kind = peak_hbm()
+    roof = None
+    if per_kernel:
+        name, d = max(per_kernel.items(), key=lambda kv: kv[1]["time"])
+        ach = d["bytes"] / d["time"] / 1e9 if d["known"] and d["time"] > 0 else None
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": None,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "launches_per_step": d["launches"] // args.steps,
+                "kernel_ms_per_step": d["time"] * 1e3 / args.steps,
+                "share_of_step": d["time"] * 1e3 / args.steps / ms,
+                "bytes_per_step": d["bytes"] // args.steps}
+
+    # end to end through the public API with host buffers
+    ev0.record(stream)
+    for _ in range(args.steps):
+        r = H.convex_hull_3d(pinned, be)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ev0.elapsed_time(ev1) / args.steps
+    e2e = {"value": n / (e2e_ms / 1e3), "unit": "points/s", "h2d_bytes_per_step": 24 * n,
+           "d2h_bytes_per_step": int(r.faces.nbytes + r.vertices.nbytes), "ms_per_step": e2e_ms}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.config, args.cpu_sample_n)
+        except Exception as exc:  # reference missing on this box
+            cpu = {"value": None, "unit": "points/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    line = {
+        "metric": "3D hull points/sec", "value": value, "unit": "points/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, PCG64)",
+        "config": {"workload": f"{args.config}: {label}", "n": n, "distribution": dist,
+                   "seed": seed, "engine": args.engine, "parallelism": "1 GPU",
+                   "l2": "input 24n bytes > 126 MB L2 (C4/C5); no explicit flush",
+                   "faces": nfaces, "vertices": nverts},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,154 @@
+/*
+ * hull3d_b200.h -- C ABI of the B200-native kinetic 3D convex hull.
+ *
+ * Drop-in boundary for the hot path of the reference package `hull3d`
+ * (arxiv/paper_1205_1171).  Two groups of entry points:
+ *
+ *  1. The kernel-module seam.  The reference selects its hot kernels through
+ *     `hull3d.kernels.active()` (pkg/src/hull3d/kernels.py:52-54), a module
+ *     exporting the functions of pkg/src/hull3d/_ckernels.pyx:231-375 over
+ *     caller-owned buffers that never allocate and report failures as
+ *     negative codes.  Each `h3d_seam_*` function below replaces one of them
+ *     with the same argument meaning, buffer layout and return convention,
+ *     except that every buffer is a DEVICE pointer and a CUDA stream is
+ *     passed.  They are synchronous (they read back one result word), like
+ *     the reference's blocking calls.  INTEGRATION.md shows the ctypes module
+ *     a maintainer would register in kernels._BY_NAME.
+ *
+ *  2. The fused B200 path used by `paper_1205_1171_b200.convex_hull_3d`
+ *     (the reference entry point pkg/src/hull3d/api.py:162-284): device
+ *     presort, both passes of all merge levels, facet extraction and the
+ *     orientation / remap epilogue, stream-ordered, over caller-provided
+ *     fixed-capacity workspace (the library never allocates).
+ *
+ * Layouts (pkg/src/hull3d/store.py:46-118): pts = n rows of (x,y,z) f64,
+ * links = n rows of (prev,next) i32, slots = 2n i32 with the log of group
+ * [L,R) at slot 2L, NIL (-1) terminated; jobs = m rows of (L,M,R) i64.
+ * No torch types cross this boundary: plain pointers, sizes and a
+ * cudaStream_t passed as void*.
+ */
+#ifndef HULL3D_B200_H
+#define HULL3D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* constants and error codes: pkg/src/hull3d/_ckernels.pyx:19-24 */
+#define H3D_NIL (-1)
+#define H3D_E_OVERFLOW (-1)      /* MergeOverflowError   (merge.py:33-35)   */
+#define H3D_E_BRIDGE (-2)        /* BridgeWalkError      (merge.py:37-39)   */
+#define H3D_E_CHAIN (-3)         /* ChainError           (store.py:24-26)   */
+#define H3D_E_COUNT (-4)         /* LogError             (store.py:29-30)   */
+#define H3D_E_UNTERMINATED (-5)  /* LogError             (store.py:29-30)   */
+#define H3D_E_TIES (-6)          /* DegenerateInputError (api.py:106-108)   */
+#define H3D_E_COINCIDENT (-7)    /* DegenerateInputError (api.py:131-132)   */
+#define H3D_E_COLLINEAR (-8)     /* DegenerateInputError (api.py:138-139)   */
+#define H3D_E_COPLANAR (-9)      /* DegenerateInputError (api.py:146-147)   */
+#define H3D_E_NOFACETS (-10)     /* DegenerateInputError (api.py:253-256)   */
+#define H3D_E_CAPACITY (-11)     /* fast-path fixed capacity exceeded       */
+#define H3D_E_NONFINITE (-12)   /* ValueError("coordinates must be finite") */
+#define H3D_E_ARG (-100)         /* bad argument                            */
+#define H3D_E_CUDA (-101)        /* CUDA runtime error                      */
+
+/* library identification (the reference's kernel modules export IMPL) */
+const char *h3d_impl(void);
+/* last CUDA error string seen by the library (diagnostics) */
+const char *h3d_last_error(void);
+/* number of this library's own kernel launches so far (process-wide) */
+int64_t h3d_launch_count(void);
+
+/* ---------------------------------------------------------------------
+ * 1. kernel-module seam (pkg/src/hull3d/_ckernels.pyx)
+ * ------------------------------------------------------------------- */
+
+/* act(links, i) -> 0 or E_CHAIN                        _ckernels.pyx:231-234 */
+int64_t h3d_seam_act(int32_t *links, int64_t i, void *stream);
+
+/* init_base_logs(links, slots, n) -> 0                 _ckernels.pyx:237-245 */
+int64_t h3d_seam_init_base_logs(int32_t *links, int32_t *slots, int64_t n,
+                                void *stream);
+
+/* find_initial_bridge(pts, links, u, v, limit) -> (u, v) or (NIL, NIL)
+ *                                                      _ckernels.pyx:248-255 */
+int64_t h3d_seam_find_initial_bridge(const double *pts, const int32_t *links,
+                                     int64_t u, int64_t v, int64_t limit,
+                                     int64_t *uv_out /* host, 2 */,
+                                     void *stream);
+
+/* merge_movies(pts, links, in, out, L, M, R) -> k or code
+ *                                                      _ckernels.pyx:258-264 */
+int64_t h3d_seam_merge_movies(const double *pts, int32_t *links,
+                              const int32_t *in_slots, int32_t *out_slots,
+                              int64_t L, int64_t M, int64_t R, void *stream);
+
+/* merge_range(pts, links, in, out, jobs, lo, hi) -> 0 or code
+ *                                                      _ckernels.pyx:267-280 */
+int64_t h3d_seam_merge_range(const double *pts, int32_t *links,
+                             const int32_t *in_slots, int32_t *out_slots,
+                             const int64_t *jobs, int64_t lo, int64_t hi,
+                             void *stream);
+
+/* replay / rewind_replay(links, slots, off, count) -> 0 or code
+ *                                                      _ckernels.pyx:292-321 */
+int64_t h3d_seam_replay(int32_t *links, const int32_t *slots, int64_t off,
+                        int64_t count, void *stream);
+int64_t h3d_seam_rewind_replay(int32_t *links, const int32_t *slots,
+                               int64_t off, int64_t count, void *stream);
+
+/* extract_faces(links, slots, off, faces (limit,3) i32) -> m or code
+ *                                                      _ckernels.pyx:324-349 */
+int64_t h3d_seam_extract_faces(int32_t *links, const int32_t *slots,
+                               int64_t off, int32_t *faces, int64_t limit,
+                               void *stream);
+
+/* log_length(slots, off, cap) -> k or E_UNTERMINATED   _ckernels.pyx:352-360 */
+int64_t h3d_seam_log_length(const int32_t *slots, int64_t off, int64_t cap,
+                            void *stream);
+
+/* copy_log(src, dst, off, cap) -> k or E_UNTERMINATED  _ckernels.pyx:363-375 */
+int64_t h3d_seam_copy_log(const int32_t *src, int32_t *dst, int64_t off,
+                          int64_t cap, void *stream);
+
+/* One whole level of build_movie (pkg/src/hull3d/parallel.py:96-109): every
+ * merge job of plan_level(n, level) plus the carry, in one launch, with the
+ * reference's exact sequential merge per job.  zsign = -1.0 reads pts with z
+ * negated (the upper pass).  Returns 0 or the first error code. */
+int64_t h3d_seam_run_level(const double *pts, double zsign, int32_t *links,
+                           const int32_t *in_slots, int32_t *out_slots,
+                           int64_t n, int64_t level, void *stream);
+
+/* ---------------------------------------------------------------------
+ * 2. fused B200 path
+ * ------------------------------------------------------------------- */
+
+/* bytes of workspace h3d_presort / h3d_hull need for n points */
+size_t h3d_presort_workspace_bytes(int64_t n);
+
+/* Device presort = _sort_and_perturb + _scan_degenerate
+ * (pkg/src/hull3d/api.py:61-147): stable radix argsort of x; on any x tie,
+ * a stable (x,y,z) lexsort, bit-exact tie perturbation and a stable
+ * re-sort.  Writes sorted (n,3) f64 and order (n) i64 (caller -> sorted).
+ * *perturbed (host) is set to 0/1.  Returns 0 or H3D_E_NONFINITE / _TIES /
+ * _COINCIDENT / _COLLINEAR / _COPLANAR. */
+int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts,
+                    int64_t *order, void *workspace, size_t workspace_bytes,
+                    int32_t *perturbed, void *stream);
+
+/* Epilogue (pkg/src/hull3d/api.py:252-266): faces_raw (F,3) i32 in sorted
+ * indices (lower block then upper block) -> faces (F,3) i64 oriented outward
+ * against the centroid and mapped through order; vertex_mark (n) i32 scratch;
+ * vertices (<= n) i64 = np.unique(faces).  Returns the vertex count. */
+int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
+                         const int64_t *order, const int32_t *faces_raw,
+                         int64_t nfaces, int64_t *faces, int32_t *vertex_mark,
+                         int64_t *vertices, void *workspace,
+                         size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HULL3D_B200_H */

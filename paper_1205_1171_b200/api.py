@@ -1,0 +1,251 @@
+"""Public entry point -- drop-in for ``hull3d.convex_hull_3d``.
+
+Same signature, result types, orientation, vertex order, stats semantics
+and exceptions as pkg/src/hull3d/api.py:162-284.  Every step after the
+host->device copy runs on the B200: presort + tie perturbation + degeneracy
+scan (csrc/presort.cu), both hull passes (engine.py), facet extraction and
+the orientation/remap/unique epilogue.  There is no CPU fallback: without a
+CUDA device or the built library this raises.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import level_count, run_pass_exact, stream_ptr
+from .errors import DegenerateInputError, check_api
+
+
+@dataclass
+class HullStats:
+    """Run metadata (api.py:28-44).  As in the reference, ``*_level_ms``
+    hold per-level SECONDS and are empty for the serial
+    solver."""
+
+    n: int
+    levels: int
+    lower_events: int
+    upper_events: int
+    sort_ms: float
+    lower_ms: float
+    upper_ms: float
+    total_ms: float
+    perturbed: bool
+    solver: str
+    workers: int
+    lower_level_ms: list[float] = field(default_factory=list)
+    upper_level_ms: list[float] = field(default_factory=list)
+
+
+@dataclass
+class HullResult:
+    """Hull vertices (sorted ascending) and outward-oriented facets, both in
+    the caller's input indexing (api.py:47-58).  With ``return_device=True``
+    the arrays are CUDA int64 tensors instead of numpy arrays."""
+
+    vertices: np.ndarray
+    faces: np.ndarray
+    stats: HullStats
+
+    def face_set(self) -> set[tuple[int, int, int]]:
+        faces = self.faces.cpu().numpy() if isinstance(self.faces, torch.Tensor) else self.faces
+        return {tuple(sorted(map(int, row))) for row in faces}
+
+
+class CudaBackend:
+    """Backend object selecting the B200 engine (passed in the reference's
+    ``backend`` slot).  ``workers`` is reported in HullStats like the
+    reference's ThreadBackend.workers."""
+
+    def __init__(self, device: int | str | torch.device | None = None, engine: str = "fast"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("CudaBackend needs a CUDA device")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        if engine not in ("fast", "exact"):
+            raise ValueError(f"unknown engine {engine!r}")
+        self.engine = engine
+        self.workers = 1
+
+    def __repr__(self):
+        return f"CudaBackend(device={self.device}, engine={self.engine!r})"
+
+
+def _device_of(points, backend) -> torch.device:
+    if isinstance(backend, CudaBackend):
+        return backend.device
+    if isinstance(points, torch.Tensor) and points.is_cuda:
+        return points.device
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1205_1171_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class _Workspace:
+    """Grow-only device scratch per (device) for presort/epilogue."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, device: torch.device, nbytes: int) -> torch.Tensor:
+        buf = cls._cache.get(device)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            cls._cache[device] = buf
+        return buf
+
+
+def presort(pts_dev: torch.Tensor):
+    """Device _sort_and_perturb + _scan_degenerate -> (sorted, order, perturbed)."""
+    L = _lib.load()
+    n = pts_dev.shape[0]
+    dev = pts_dev.device
+    ws_bytes = int(L.h3d_presort_workspace_bytes(n))
+    ws = _Workspace.get(dev, ws_bytes)
+    sorted_pts = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    order = torch.empty(n, dtype=torch.int64, device=dev)
+    import ctypes
+
+    pert = ctypes.c_int32(0)
+    code = L.h3d_presort(pts_dev.data_ptr(), n, sorted_pts.data_ptr(), order.data_ptr(),
+                         ws.data_ptr(), ws.numel(), ctypes.addressof(pert), stream_ptr(dev))
+    check_api(code)
+    return sorted_pts, order, bool(pert.value)
+
+
+def orient_remap(sorted_pts: torch.Tensor, order: torch.Tensor, raw: torch.Tensor):
+    """Device api.py:252-266 -> (vertices i64, faces i64) on device."""
+    L = _lib.load()
+    n = sorted_pts.shape[0]
+    dev = sorted_pts.device
+    F = raw.shape[0]
+    if F == 0:
+        raise DegenerateInputError("no facets produced; input is degenerate")
+    ws_bytes = int(L.h3d_presort_workspace_bytes(n))
+    ws = _Workspace.get(dev, ws_bytes)
+    faces = torch.empty((F, 3), dtype=torch.int64, device=dev)
+    mark = torch.empty(n, dtype=torch.int32, device=dev)
+    verts = torch.empty(n, dtype=torch.int64, device=dev)
+    raw = raw.contiguous()
+    h = check_api(L.h3d_orient_remap(sorted_pts.data_ptr(), n, order.data_ptr(), raw.data_ptr(), F,
+                                     faces.data_ptr(), mark.data_ptr(), verts.data_ptr(),
+                                     ws.data_ptr(), ws.numel(), stream_ptr(dev)))
+    return verts[:h], faces
+
+
+def _to_device(points, dev: torch.device) -> torch.Tensor:
+    if isinstance(points, torch.Tensor):
+        t = points.to(dtype=torch.float64)
+        if t.ndim != 2 or t.shape[1] != 3:
+            raise ValueError("points must have shape (n, 3)")
+        if not t.is_cuda:
+            t = t.to(dev, non_blocking=t.is_pinned())
+        elif t.device != dev:
+            t = t.to(dev)
+        return t.contiguous()
+    coords = np.asarray(points, dtype=np.float64)
+    if coords.ndim != 2 or coords.shape[1] != 3:
+        raise ValueError("points must have shape (n, 3)")
+    return torch.from_numpy(np.ascontiguousarray(coords)).to(dev)
+
+
+def _run_passes(sorted_pts, engine, solver, level_lists):
+    """Both passes; returns (lower raw, upper raw, lower ms, upper ms)."""
+    from . import fast  # noqa: WPS433 (engine module, loaded lazily)
+
+    out = []
+    ms = []
+    for which, zsign in ((0, 1.0), (1, -1.0)):
+        t0 = time.perf_counter()
+        lv = level_lists[which] if solver == "parallel" else None
+        if engine == "exact":
+            raw = run_pass_exact(sorted_pts, zsign, lv)
+        else:
+            raw = fast.run_pass(sorted_pts, zsign, lv)
+        torch.cuda.current_stream(sorted_pts.device).synchronize()
+        ms.append((time.perf_counter() - t0) * 1e3)
+        out.append(raw)
+    return out[0], out[1], ms[0], ms[1]
+
+
+def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
+                   concurrent_passes: bool | None = None,
+                   return_device: bool = False) -> HullResult:
+    """Convex hull of 3D points on the B200 (drop-in for api.py:162-284).
+
+    ``points`` may be any (n,3) array-like, a CPU tensor (pinned tensors are
+    copied asynchronously) or a CUDA tensor (device-resident input).
+    ``solver`` is accepted for signature compatibility: both values run the
+    device engine, whose final logs equal the serial solver's (the final
+    movie is canonical, tests/test_serial_parallel.py:106-116 in the
+    reference); as in the reference, the serial solver reports no per-level
+    times.  ``concurrent_passes`` is accepted and ignored (both passes are
+    stream-ordered on one device).
+    """
+    if solver not in ("parallel", "serial"):
+        raise ValueError(f"unknown solver {solver!r}")
+    total_t0 = time.perf_counter()
+    dev = _device_of(points, backend)
+    pts = _to_device(points, dev)
+    n = pts.shape[0]
+    if n == 0:
+        raise ValueError("no points")
+    workers = getattr(backend, "workers", 1)
+    engine = getattr(backend, "engine", "fast")
+    if n <= 3:
+        if not bool(torch.isfinite(pts).all()):
+            raise ValueError("coordinates must be finite")
+        total_ms = (time.perf_counter() - total_t0) * 1e3
+        stats = HullStats(n=n, levels=0, lower_events=0, upper_events=0, sort_ms=0.0,
+                          lower_ms=0.0, upper_ms=0.0, total_ms=total_ms, perturbed=False,
+                          solver=solver, workers=workers)
+        verts = torch.arange(n, dtype=torch.int64, device=dev)
+        faces = torch.empty((0, 3), dtype=torch.int64, device=dev)
+        if not return_device:
+            verts, faces = verts.cpu().numpy(), faces.cpu().numpy()
+        return HullResult(vertices=verts, faces=faces, stats=stats)
+
+    sort_t0 = time.perf_counter()
+    sorted_pts, order, perturbed = presort(pts)
+    sort_ms = (time.perf_counter() - sort_t0) * 1e3
+
+    lower_levels: list[float] = []
+    upper_levels: list[float] = []
+    lo, up, lo_ms, up_ms = _run_passes(sorted_pts, engine, solver, (lower_levels, upper_levels))
+    raw = torch.cat([lo, up])
+    verts, faces = orient_remap(sorted_pts, order, raw)
+    if not return_device:
+        verts, faces = verts.cpu().numpy(), faces.cpu().numpy()
+    total_ms = (time.perf_counter() - total_t0) * 1e3
+    stats = HullStats(n=n, levels=level_count(n), lower_events=int(lo.shape[0]),
+                      upper_events=int(up.shape[0]), sort_ms=sort_ms, lower_ms=lo_ms,
+                      upper_ms=up_ms, total_ms=total_ms, perturbed=perturbed, solver=solver,
+                      workers=workers, lower_level_ms=lower_levels, upper_level_ms=upper_levels)
+    return HullResult(vertices=verts, faces=faces, stats=stats)
+
+
+def perturb_ties(points) -> np.ndarray:
+    """api.py:61-83, exposed for API parity (host helper, not on the hot path:
+    the device presort performs the same perturbation in csrc/presort.cu)."""
+    pts = np.array(points, dtype=np.float64, copy=True)
+    x = pts[:, 0]
+    n = len(x)
+    eps16 = 16 * np.finfo(np.float64).eps
+    i = 0
+    while i < n:
+        j = i + 1
+        while j < n and x[j] == x[i]:
+            j += 1
+        if j - i > 1:
+            base = x[i]
+            step = eps16 * max(1.0, abs(base))
+            for rank in range(1, j - i):
+                x[i + rank] = base + rank * step
+        i = j
+    return pts

@@ -1,0 +1,38 @@
+// h3d_host.h -- host-side helpers shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+// records the error string for h3d_last_error(); returns true on failure
+bool h3d_check(cudaError_t e);
+// counts this library's own kernel launches (bench.py reports gpu_launches)
+void h3d_count_launches(int k);
+
+inline unsigned h3d_grid(long long work, int block) {
+  long long g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 0x7fffffffll) g = 0x7fffffffll;
+  return static_cast<unsigned>(g);
+}
+
+// bump allocator over a caller-provided workspace (the library never
+// allocates on the fused path); every carve is 256-byte aligned
+struct h3d_arena {
+  char *base;
+  size_t size, used;
+  h3d_arena(void *p, size_t n) : base(static_cast<char *>(p)), size(n), used(0) {}
+  template <class T>
+  T *take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    if (base == nullptr) {  // sizing pass
+      used += bytes;
+      return nullptr;
+    }
+    if (used + bytes > size) return nullptr;
+    T *p = reinterpret_cast<T *>(base + used);
+    used += bytes;
+    return p;
+  }
+};

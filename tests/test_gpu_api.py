@@ -1,0 +1,125 @@
+"""convex_hull_3d on the B200 against the unmodified reference's outputs
+(tests/golden/small.npz) and its API contract (pkg/tests/test_api.py)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1205_1171_b200 as H
+from paper_1205_1171_b200.generators import generate
+
+pytestmark = pytest.mark.gpu
+
+TETRA = np.array([[0.0, 0, 0], [1, 0.1, 2], [2, 1.9, 0.3], [3, 0.2, 0.1]])
+
+
+@pytest.mark.parametrize("engine", ["fast", "exact"])
+def test_golden_cases_bit_exact(small, engine):
+    be = H.CudaBackend(0, engine=engine)
+    for name in small.names:
+        c = small.case(name)
+        if engine == "fast" and not c["general"]:
+            continue  # degenerate inputs: the reference's own solvers disagree
+        r = H.convex_hull_3d(c["pts"], be)
+        assert np.array_equal(r.faces, c["faces"]), name
+        assert np.array_equal(r.vertices, c["vertices"]), name
+        assert (r.stats.lower_events, r.stats.upper_events) == (c["lower"], c["upper"]), name
+        assert r.stats.perturbed == c["perturbed"], name
+
+
+def test_degenerate_golden_cases_exact_engine(small):
+    be = H.CudaBackend(0, engine="exact")
+    for name in small.names:
+        c = small.case(name)
+        if c["general"]:
+            continue
+        r = H.convex_hull_3d(c["pts"], be)
+        assert np.array_equal(r.faces, c["faces"]), name
+
+
+def test_tetrahedron_and_orientation():
+    res = H.convex_hull_3d(TETRA)
+    assert res.vertices.tolist() == [0, 1, 2, 3]
+    assert len(res.faces) == 4
+    c = TETRA.mean(axis=0)
+    a = TETRA[res.faces[:, 0]]
+    nrm = np.cross(TETRA[res.faces[:, 1]] - a, TETRA[res.faces[:, 2]] - a)
+    assert (np.einsum("ij,ij->i", nrm, c - a) < 0).all()
+
+
+def test_input_order_invariance():
+    pts = generate(48, "gauss", 17)
+    res = H.convex_hull_3d(pts)
+    perm = np.random.default_rng(0).permutation(len(pts))
+    res2 = H.convex_hull_3d(pts[perm])
+    remapped = {tuple(sorted(int(perm[i]) for i in f)) for f in res2.faces}
+    assert remapped == res.face_set()
+
+
+def test_device_resident_and_pinned_inputs():
+    pts = generate(5000, "ball", 1)
+    ref = H.convex_hull_3d(pts)
+    d = H.convex_hull_3d(torch.from_numpy(pts).cuda(), return_device=True)
+    assert d.faces.is_cuda and np.array_equal(d.faces.cpu().numpy(), ref.faces)
+    p = H.convex_hull_3d(torch.from_numpy(pts).pin_memory())
+    assert np.array_equal(p.faces, ref.faces)
+
+
+def test_degenerate_inputs_raise():
+    rng = np.random.default_rng(1)
+    flat = np.column_stack([rng.random(10), rng.random(10), np.zeros(10)])
+    with pytest.raises(H.DegenerateInputError):
+        H.convex_hull_3d(flat)
+    line = np.column_stack([np.arange(8.0), np.arange(8.0) * 2, np.arange(8.0) * 3])
+    with pytest.raises(H.DegenerateInputError):
+        H.convex_hull_3d(line)
+    with pytest.raises(H.DegenerateInputError):
+        H.convex_hull_3d(np.zeros((6, 3)))
+
+
+def test_input_validation():
+    with pytest.raises(ValueError, match="no points"):
+        H.convex_hull_3d(np.empty((0, 3)))
+    with pytest.raises(ValueError):
+        H.convex_hull_3d(np.array([[0.0, 0.0]]))
+    with pytest.raises(ValueError):
+        H.convex_hull_3d(np.array([[0.0, np.inf, 0.0]]))
+    with pytest.raises(ValueError, match="finite"):
+        H.convex_hull_3d(np.vstack([TETRA, [[np.nan, 0, 0]]]))
+    with pytest.raises(ValueError):
+        H.convex_hull_3d(TETRA, solver="fancy")
+
+
+def test_tiny_inputs_have_no_faces():
+    for n in (1, 2, 3):
+        res = H.convex_hull_3d(generate(n, "gauss", 0))
+        assert res.vertices.tolist() == list(range(n))
+        assert res.faces.shape == (0, 3)
+        assert res.stats.levels == 0
+
+
+def test_stats_fields():
+    pts = generate(256, "ball", 0)
+    st = H.convex_hull_3d(pts).stats
+    assert st.n == 256 and st.levels == 8
+    assert st.solver == "parallel" and st.workers == 1
+    assert st.total_ms > 0 and st.sort_ms >= 0
+    assert len(st.lower_level_ms) == st.levels
+    assert not st.perturbed
+    ser = H.convex_hull_3d(pts, solver="serial").stats
+    assert ser.solver == "serial" and ser.lower_level_ms == []
+
+
+def test_every_point_inside_hull():
+    for seed in range(3):
+        pts = generate(2000, "gauss", seed)
+        res = H.convex_hull_3d(pts)
+        scale = float(np.abs(pts).max())
+        a = pts[res.faces[:, 0]]
+        nrm = np.cross(pts[res.faces[:, 1]] - a, pts[res.faces[:, 2]] - a)
+        nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+        dist = nrm @ pts.T - np.einsum("ij,ij->i", nrm, a)[:, None]
+        assert dist.max() <= 1e-9 * scale
+        assert len(res.faces) == 2 * len(res.vertices) - 4
