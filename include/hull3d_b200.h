@@ -60,6 +60,12 @@ const char *h3d_impl(void);
 const char *h3d_last_error(void);
 /* number of this library's own kernel launches so far (process-wide) */
 int64_t h3d_launch_count(void);
+/* per-level profile: when enabled, every merge level of h3d_fast_pass is
+ * bracketed by CUDA events on its stream; collect returns (level, pass,
+ * milliseconds) rows, synchronising on the recorded events, and clears them */
+void h3d_profile_enable(int32_t on);
+int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms,
+                            int64_t max);
 
 /* ---------------------------------------------------------------------
  * 1. kernel-module seam (pkg/src/hull3d/_ckernels.pyx)
@@ -147,6 +153,31 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
                          int64_t nfaces, int64_t *faces, int32_t *vertex_mark,
                          int64_t *vertices, void *workspace,
                          size_t workspace_bytes, void *stream);
+
+/* bytes of workspace one h3d_fast_pass needs for n points (two compact
+ * group buffers: headers, 32-byte point records, ids, 24-byte events) */
+size_t h3d_fast_pass_workspace_bytes(int64_t n);
+
+/* One hull pass (build_movie, pkg/src/hull3d/parallel.py:68-112) over the
+ * presorted points, all ceil(log2 n) levels, stream-ordered, no host sync.
+ * zsign = +1.0 lower hull, -1.0 upper hull (z negated on load).  Errors are
+ * recorded into *err_dev (device int64, first error wins; H3D_E_* codes or
+ * -13 = the fast path cannot reproduce the reference semantics for this
+ * input, rerun the exact seam path).  verify != 0 re-derives every child
+ * event time from the links and flags any difference.  Returns which of the
+ * workspace's two buffers holds the final group (0/1) or a negative code. */
+int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign,
+                      void *workspace, size_t workspace_bytes,
+                      int64_t *err_dev, int32_t verify, void *stream);
+
+/* Facets of both passes from their final groups (extract_faces,
+ * _ckernels.pyx:324-349): faces (cap,3) i32 in sorted indices, lower block
+ * then upper block; counts_dev (device int64[2]) = (lower, upper) counts.
+ * A total above cap records H3D_E_CAPACITY into err_dev. */
+int64_t h3d_fast_extract(void *ws_lower, void *ws_upper, int64_t n,
+                         int64_t final_lower, int64_t final_upper,
+                         int32_t *faces, int64_t cap, int64_t *counts_dev,
+                         int64_t *err_dev, void *stream);
 
 #ifdef __cplusplus
 }

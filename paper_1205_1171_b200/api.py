@@ -156,22 +156,49 @@ def _to_device(points, dev: torch.device) -> torch.Tensor:
 
 
 def _run_passes(sorted_pts, engine, solver, level_lists):
-    """Both passes; returns (lower raw, upper raw, lower ms, upper ms)."""
-    from . import fast  # noqa: WPS433 (engine module, loaded lazily)
+    """Both passes; returns (raw faces int32 (F,3) on device, lower count,
+    upper count, lower ms, upper ms).  Per-level times are device events
+    (seconds, like the reference's perf_counter deltas)."""
+    from . import engine as E
+    from . import fast
 
+    want_levels = solver == "parallel"
+    if engine == "fast":
+        t0 = time.perf_counter()
+        profiling = want_levels or E.PROFILE is not None
+        if profiling:
+            fast.profile_enable(True)
+        try:
+            res = fast.run_both(sorted_pts)
+        finally:
+            if profiling:
+                fast.profile_enable(False)
+        rows = fast.profile_collect() if profiling else []
+        if res is not None:
+            dt = (time.perf_counter() - t0) * 1e3
+            raw, k_lo, k_up = res
+            ms = [0.0, 0.0]
+            for lv, p, t in rows:
+                ms[p] += t
+                if want_levels:
+                    level_lists[p].append(t / 1e3)
+                if E.PROFILE is not None:
+                    E.PROFILE.append(("k_fast_level", p, lv, t))
+            tot = ms[0] + ms[1]
+            lo_ms = dt * ms[0] / tot if tot > 0 else dt / 2
+            return raw, k_lo, k_up, lo_ms, dt - lo_ms
+        for lst in level_lists:
+            lst.clear()
     out = []
     ms = []
     for which, zsign in ((0, 1.0), (1, -1.0)):
         t0 = time.perf_counter()
-        lv = level_lists[which] if solver == "parallel" else None
-        if engine == "exact":
-            raw = run_pass_exact(sorted_pts, zsign, lv)
-        else:
-            raw = fast.run_pass(sorted_pts, zsign, lv)
+        lv = level_lists[which] if want_levels else None
+        raw = run_pass_exact(sorted_pts, zsign, lv)
         torch.cuda.current_stream(sorted_pts.device).synchronize()
         ms.append((time.perf_counter() - t0) * 1e3)
         out.append(raw)
-    return out[0], out[1], ms[0], ms[1]
+    return torch.cat(out), out[0].shape[0], out[1].shape[0], ms[0], ms[1]
 
 
 def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
@@ -217,14 +244,14 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
 
     lower_levels: list[float] = []
     upper_levels: list[float] = []
-    lo, up, lo_ms, up_ms = _run_passes(sorted_pts, engine, solver, (lower_levels, upper_levels))
-    raw = torch.cat([lo, up])
+    raw, k_lo, k_up, lo_ms, up_ms = _run_passes(sorted_pts, engine, solver,
+                                                (lower_levels, upper_levels))
     verts, faces = orient_remap(sorted_pts, order, raw)
     if not return_device:
         verts, faces = verts.cpu().numpy(), faces.cpu().numpy()
     total_ms = (time.perf_counter() - total_t0) * 1e3
-    stats = HullStats(n=n, levels=level_count(n), lower_events=int(lo.shape[0]),
-                      upper_events=int(up.shape[0]), sort_ms=sort_ms, lower_ms=lo_ms,
+    stats = HullStats(n=n, levels=level_count(n), lower_events=int(k_lo),
+                      upper_events=int(k_up), sort_ms=sort_ms, lower_ms=lo_ms,
                       upper_ms=up_ms, total_ms=total_ms, perturbed=perturbed, solver=solver,
                       workers=workers, lower_level_ms=lower_levels, upper_level_ms=upper_levels)
     return HullResult(vertices=verts, faces=faces, stats=stats)

@@ -20,3 +20,60 @@ bool h3d_check(cudaError_t e) {
 extern "C" const char *h3d_impl(void) { return "b200"; }
 extern "C" const char *h3d_last_error(void) { return g_last_error; }
 extern "C" int64_t h3d_launch_count(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------ level profile
+#include <mutex>
+#include <vector>
+
+namespace {
+struct ProfRec {
+  int level, pass;
+  cudaEvent_t e0, e1;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+bool h3d_profiling() { return g_prof_on; }
+
+void *h3d_prof_begin(cudaStream_t s) {
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  cudaEventRecord(e, s);
+  return e;
+}
+
+void h3d_prof_end(void *e0, int level, int pass, cudaStream_t s) {
+  if (!e0) return;
+  cudaEvent_t e1;
+  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEventRecord(e1, s);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof.push_back({level, pass, static_cast<cudaEvent_t>(e0), e1});
+}
+
+extern "C" void h3d_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+extern "C" int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms, int64_t max) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  int64_t m = 0;
+  for (auto &r : g_prof) {
+    if (m < max) {
+      float t = 0.f;
+      cudaEventSynchronize(r.e1);
+      cudaEventElapsedTime(&t, r.e0, r.e1);
+      level[m] = r.level;
+      pass[m] = r.pass;
+      ms[m] = t;
+      ++m;
+    }
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  g_prof.clear();
+  return m;
+}

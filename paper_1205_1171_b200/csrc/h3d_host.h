@@ -9,6 +9,10 @@
 bool h3d_check(cudaError_t e);
 // counts this library's own kernel launches (bench.py reports gpu_launches)
 void h3d_count_launches(int k);
+// per-level CUDA-event profile (h3d_profile_enable); no-ops when disabled
+bool h3d_profiling();
+void *h3d_prof_begin(cudaStream_t s);
+void h3d_prof_end(void *e0, int level, int pass, cudaStream_t s);
 
 inline unsigned h3d_grid(long long work, int block) {
   long long g = (work + block - 1) / block;

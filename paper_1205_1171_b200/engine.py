@@ -27,7 +27,7 @@ from .errors import check_merge, check_store
 NIL = -1
 
 # bench.py instrumentation: when a list, every merge-level launch appends
-# (kernel name, pass index, level, start event, end event)
+# (kernel name, pass index, level, device milliseconds)
 PROFILE: list | None = None
 
 
@@ -55,7 +55,8 @@ def record_end(e0, name: str, pass_idx: int, level: int, device=None) -> None:
         return
     e1 = torch.cuda.Event(enable_timing=True)
     e1.record()
-    PROFILE.append((name, pass_idx, level, e0, e1))
+    e1.synchronize()
+    PROFILE.append((name, pass_idx, level, e0.elapsed_time(e1)))
 
 
 def launch_count() -> int:

@@ -1,10 +1,109 @@
-"""Fused fast pass engine (placeholder: delegates to the exact engine until
-csrc/fast.cu lands)."""
+"""Fused fast engine: both hull passes over compact groups (csrc/fast.cu).
+
+The final logs equal the reference's (tests/test_gpu_fast.py checks every
+level's log against the reference's per-level buffers).  If the device
+reports that the fast path cannot reproduce the reference semantics for an
+input (degenerate inputs: a stored event time disagreeing with the links in
+verify mode, a compact-capacity overflow, a dangling link), or any merge
+error, the pass is rerun on the exact seam engine, which reproduces the
+reference's behaviour (and its exceptions) step for step.
+"""
 
 from __future__ import annotations
 
-from .engine import run_pass_exact
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import level_count, run_pass_exact, stream_ptr
+
+E_FASTPATH = -13
+
+# how many pass pairs the exact engine had to redo (tests assert 0 on
+# general-position inputs: the fast path must be the one that runs)
+FALLBACKS = [0]
+LAST_ERROR = [0]
+
+
+class _WS:
+    """Grow-only per-device workspaces for the two passes."""
+
+    cache: dict = {}
+
+    @classmethod
+    def get(cls, device, which: int, nbytes: int) -> torch.Tensor:
+        key = (device, which)
+        buf = cls.cache.get(key)
+        if buf is None or buf.numel() < nbytes:
+            cls.cache.pop(key, None)
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            cls.cache[key] = buf
+        return buf
+
+
+def profile_enable(on: bool) -> None:
+    _lib.load().h3d_profile_enable(1 if on else 0)
+
+
+def profile_collect(max_rows: int = 4096):
+    """[(level, pass, ms)] recorded since the last collect."""
+    L = _lib.load()
+    lv = np.zeros(max_rows, dtype=np.int32)
+    ps = np.zeros(max_rows, dtype=np.int32)
+    ms = np.zeros(max_rows, dtype=np.float32)
+    m = L.h3d_profile_collect(lv.ctypes.data, ps.ctypes.data, ms.ctypes.data, max_rows)
+    return [(int(lv[i]), int(ps[i]), float(ms[i])) for i in range(m)]
+
+
+def run_both(sorted_pts: torch.Tensor, verify: bool = False):
+    """Both passes + facet extraction.  Returns (raw faces int32 (F,3) on
+    device, lower count, upper count) or None when the exact engine must
+    take over."""
+    L = _lib.load()
+    n = sorted_pts.shape[0]
+    dev = sorted_pts.device
+    s = stream_ptr(dev)
+    wsb = int(L.h3d_fast_pass_workspace_bytes(n))
+    ws_lo = _WS.get(dev, 0, wsb)
+    ws_up = _WS.get(dev, 1, wsb)
+    state = torch.zeros(4, dtype=torch.int64, device=dev)  # err, kLo, kUp, pad
+    err = state[0:1]
+    counts = state[1:3]
+    fin = []
+    for ws, zs in ((ws_lo, 1.0), (ws_up, -1.0)):
+        r = L.h3d_fast_pass(sorted_pts.data_ptr(), n, zs, ws.data_ptr(), ws.numel(),
+                            err.data_ptr(), 1 if verify else 0, s)
+        if r < 0:
+            from .errors import check_merge
+
+            check_merge(int(r))
+        fin.append(int(r))
+    cap = max(2 * n, 8)
+    faces = torch.empty((cap, 3), dtype=torch.int32, device=dev)
+    r = L.h3d_fast_extract(ws_lo.data_ptr(), ws_up.data_ptr(), n, fin[0], fin[1],
+                           faces.data_ptr(), cap, counts.data_ptr(), err.data_ptr(), s)
+    if r < 0:
+        from .errors import check_merge
+
+        check_merge(int(r))
+    h = state.cpu()  # the one host sync of the pass pair
+    if int(h[0]) != 0:
+        FALLBACKS[0] += 1
+        LAST_ERROR[0] = int(h[0])
+        return None
+    k_lo, k_up = int(h[1]), int(h[2])
+    return faces[: k_lo + k_up], k_lo, k_up
 
 
 def run_pass(pts, zsign, level_times=None):
+    """Single pass on the exact engine (kept for API symmetry)."""
     return run_pass_exact(pts, zsign, level_times)
+
+
+def levels_of(n: int) -> int:
+    return level_count(n)
+
+
+__all__ = ["run_both", "profile_enable", "profile_collect", "E_FASTPATH", "ctypes"]

@@ -40,8 +40,8 @@ def main():
         H.convex_hull_3d(pts, be, return_device=True)
         torch.cuda.synchronize()
         E.PROFILE = None
-        for name, p, lv, e0, e1 in prof:
-            acc.setdefault((name, p, lv), []).append(e0.elapsed_time(e1))
+        for name, p, lv, t in prof:
+            acc.setdefault((name, p, lv), []).append(t)
     lb = bench.level_bytes(a.config) or {}
     rows = []
     for (name, p, lv), ts in sorted(acc.items(), key=lambda kv: (kv[0][1], kv[0][2], kv[0][0])):
