@@ -209,19 +209,30 @@ def peak_hbm():
     return 6650.0, "fallback"
 
 
-def level_bytes(cfg: str):
-    """Per (pass, level) algorithmic bytes B_alg = 4(E_in+E_out) + 40(D+2J)."""
+def level_stats(cfg: str):
     key = STATS_KEY.get(cfg)
     p = os.path.join(ROOT, "tests", "golden", "level_stats.json")
     if key is None or not os.path.exists(p):
         return None
-    st = json.load(open(p)).get(key)
+    return json.load(open(p)).get(key)
+
+
+def level_bytes(cfg: str):
+    """Algorithmic bytes per (pass, level) row of the profile:
+    a per-level merge is credited B_alg = 4(E_in+E_out) + 40(D+2J); the fused
+    leaf kernel (profile level -b = levels 1..b in one launch) is credited
+    once: 4*E_in(1) + 4*E_out(b) + 40*(points in its groups) -- one 32-byte
+    record read + one 8-byte link write per point -- not the per-level sum."""
+    st = level_stats(cfg)
     if st is None:
         return None
+    n = CONFIGS[cfg][0]
     out = {}
     for pi, which in enumerate(("lower", "upper")):
-        for r in st[which]:
-            out[(pi, r["level"])] = 4 * (r["E_in"] + r["E_out"]) + 40 * (r["D"] + 2 * r["J"])
+        rows = {r["level"]: r for r in st[which]}
+        for lv, r in rows.items():
+            out[(pi, lv)] = 4 * (r["E_in"] + r["E_out"]) + 40 * (r["D"] + 2 * r["J"])
+            out[(pi, -lv)] = 4 * rows[1]["E_in"] + 4 * r["E_out"] + 40 * n
     return out
 
 

@@ -178,12 +178,19 @@ def _run_passes(sorted_pts, engine, solver, level_lists):
             dt = (time.perf_counter() - t0) * 1e3
             raw, k_lo, k_up = res
             ms = [0.0, 0.0]
+            nlev = level_count(sorted_pts.shape[0])
+            per = [[0.0] * nlev, [0.0] * nlev]
             for lv, p, t in rows:
                 ms[p] += t
-                if want_levels:
-                    level_lists[p].append(t / 1e3)
+                name, lv = fast.kernel_of(lv)
+                # a negative level is a fused kernel (levels 1..|lv|); its time
+                # is reported at its last level, 0.0 below it
+                per[p][abs(lv) - 1] += t / 1e3
                 if E.PROFILE is not None:
-                    E.PROFILE.append(("k_fast_level", p, lv, t))
+                    E.PROFILE.append((name, p, lv, t))
+            if want_levels:
+                level_lists[0].extend(per[0])
+                level_lists[1].extend(per[1])
             tot = ms[0] + ms[1]
             lo_ms = dt * ms[0] / tot if tot > 0 else dt / 2
             return raw, k_lo, k_up, lo_ms, dt - lo_ms

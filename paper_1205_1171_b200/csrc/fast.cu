@@ -1,17 +1,28 @@
 // fast.cu -- the fused fast path: all merge levels of a pass over compact groups.
 //
-// Level scheduler (parallel.py:68-112 on the device): one launch of
-// k_fast_level per level plus one k_fast_big launch that picks up the jobs
-// too big for the level kernel's shared-memory budget and the carry.  No
-// host synchronisation inside a pass; a device error word is read once per
-// hull.
+// Level scheduler (parallel.py:68-112 on the device), no host synchronisation
+// inside a pass; a device error word is read once per hull:
 //
-// k_fast_level: one thread per merge job, jobs packed into a CTA's dynamic
-// shared memory by a block-wide prefix scan of their footprints (jobs that do
-// not fit wait for the next round).  Each warp stages its jobs' contiguous
-// child runs (records, events) with coalesced loads, every thread then runs
-// its merge (merge_compact, fast.cuh) entirely in shared memory, and the warp
-// compacts (ballot/popc prefix scans) and streams each merged group back out.
+//  * k_fast_tpj    one launch per level while jobs are plentiful: one THREAD
+//                  per merge job (merge_tpj, the reference's sequential sweep
+//                  with cached candidate times), int16 links in a packed
+//                  shared-memory slice, coordinates and child events streamed
+//                  from HBM, merged events written straight back, and the
+//                  start-of-time links rebuilt from the merged -inf chain and
+//                  first events (no sequential rewind).
+//  * k_fast_warp   one launch per level above the leaf.  One WARP per merge
+//                  job (merge_warp): the kinetic sweep advances through the
+//                  time-merged child logs 32 events at a time -- every event
+//                  that neither touches the bridge feet nor comes after the
+//                  next bridge event is retired in parallel (survivor
+//                  emission by ballot prefix, link writes resolved
+//                  last-writer-wins with __match_any_sync) -- and only foot
+//                  events and bridge events are sequential.  The start-of-time
+//                  links of the merged group are rebuilt in parallel (merged
+//                  -inf chain + each point's first facet) instead of the
+//                  reference's sequential rewind.  Jobs are staged in a
+//                  shared-memory pool when they fit, else run in place in HBM.
+//  * k_fast_extract  facets of both passes straight from the final events.
 #include <cub/cub.cuh>
 
 #include "fast.cuh"
@@ -27,30 +38,12 @@ struct GroupBuf {
 };
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int FIRST_FLAG = 1 << 30;        // "on a child's -inf chain"
+constexpr int FIRST_NONE = FIRST_FLAG - 1; // no event yet
 
-__device__ __forceinline__ long long align8(long long b) { return (b + 7) & ~7ll; }
+__host__ __device__ __forceinline__ long long align8(long long b) { return (b + 7) & ~7ll; }
 
-// shared-memory footprint of one merge job
-__device__ __forceinline__ long long job_bytes(int nS, int kin) {
-  return align8(32ll * nS + 24ll * kin + 24ll * (2ll * nS) + 4ll * nS);
-}
-
-struct JobView {
-  Rec *rec;
-  Ev *evL, *evR, *out;
-  int *mark;
-};
-
-__device__ __forceinline__ JobView carve_job(unsigned char *base, int nS, int kL, int kR) {
-  JobView v;
-  v.rec = reinterpret_cast<Rec *>(base);
-  v.evL = reinterpret_cast<Ev *>(base + 32ll * nS);
-  v.evR = v.evL + kL;
-  v.out = v.evR + kR;
-  v.mark = reinterpret_cast<int *>(v.out + 2 * nS);
-  return v;
-}
-
+// --------------------------------------------------------- thread per job
 // level 0: every point is a one-point group with an empty log
 __global__ void k_fast_init(const double *__restrict__ pts, double zs, long long n, GroupBuf g) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -67,282 +60,733 @@ __global__ void k_fast_init(const double *__restrict__ pts, double zs, long long
   }
 }
 
-// Cooperative (group of `width` lanes, lane index `lane`) staging of one job.
-__device__ __forceinline__ void stage_job(const GroupBuf &in, JobView v, long long L, long long M,
-                                          int nSL, int nSR, int kL, int kR, int lane, int width) {
-  const int nS = nSL + nSR;
-  for (int p = lane; p < nS; p += width) {
-    Rec r;
-    if (p < nSL) {
-      r = in.rec[L + p];
-    } else {
-      r = in.rec[M + (p - nSL)];
-      if (r.prev != NIL) r.prev += nSL;
-      if (r.next != NIL) r.next += nSL;
-    }
-    v.rec[p] = r;
-    v.mark[p] = 0;
+constexpr unsigned short INFO_CHAIN = 0x8000;  // on its child's -inf chain
+constexpr unsigned short INFO_NONE = 0x7fff;   // no merged event yet
+
+// Thread-per-job merge state: the job's records (coordinates + int16 links
+// would not save a cycle on the dependency chain, so records stay 32 B) and
+// its info table live in this thread's shared-memory slice.
+struct TpjJob {
+  Rec *R;                 // nS records, left [0,nSL), right [nSL,nS)
+  unsigned short *info;   // nS: INFO_CHAIN | first merged event index
+  int nSL;
+};
+
+// The reference's kinetic sweep (_merge_one phase 1, _ckernels.pyx:86-183)
+// for one job on one thread, written branch-free so the 32 lanes of a warp
+// (32 different jobs) stay converged: every lane evaluates the quantities of
+// all six cases and selects; the four bridge candidates are recomputed every
+// step.  Child candidate times are the stored times (the time the facet got
+// when it was emitted one level down, same expression, same triple); events
+// go straight to HBM with their facet and kind; each point's first merged
+// event is recorded for the link rebuild that replaces the rewind.
+// Returns k or a negative code.
+__device__ long long merge_tpj(TpjJob &J, const Ev *__restrict__ evL, int kL,
+                               const Ev *__restrict__ evR, int kR, Ev *out, long long capRef,
+                               long long limitRef, int *pu0, int *pv0) {
+  Rec *R = J.R;
+  const int nSL = J.nSL;
+  int u = nSL - 1, v = nSL;
+  if (bridge_rec(R, &u, &v, limitRef) < 0) return H3D_E_BRIDGE;
+  *pu0 = u;
+  *pv0 = v;
+  int i = 0, j = 0, k = 0;
+  double tcur = -INF;
+  double c0 = INF, c1 = INF;
+  int bL = 0, bR = 0;
+  Ev nL, nR;  // prefetched next child events
+  nL.t = INF;
+  nR.t = INF;
+  if (kL > 0) {
+    c0 = evL[0].t;
+    bL = evL[0].b;
+    if (kL > 1) nL = evL[1];
   }
-  for (int e = lane; e < kL; e += width) v.evL[e] = in.ev[2 * L + e];
-  for (int e = lane; e < kR; e += width) v.evR[e] = in.ev[2 * M + e];
+  if (kR > 0) {
+    c1 = evR[0].t;
+    bR = evR[0].b + nSL;
+    if (kR > 1) nR = evR[1];
+  }
+  double c2 = evt_rec(R, u, R[u].next, v);
+  double c3 = evt_rec(R, R[u].prev, u, v);
+  double c4 = evt_rec(R, u, v, R[v].next);
+  double c5 = evt_rec(R, u, R[v].prev, v);
+  int err = 0;
+  for (;;) {
+    double best = INF;
+    int which = -1;
+    if (c0 > tcur && c0 < best) { best = c0; which = 0; }
+    if (c1 > tcur && c1 < best) { best = c1; which = 1; }
+    if (c2 > tcur && c2 < best) { best = c2; which = 2; }
+    if (c3 > tcur && c3 < best) { best = c3; which = 3; }
+    if (c4 > tcur && c4 < best) { best = c4; which = 4; }
+    if (c5 > tcur && c5 < best) { best = c5; which = 5; }
+    if (which < 0) break;
+    const bool left = which == 0, right = which == 1, child = which <= 1;
+    const int e = left ? bL : (right ? bR : u);
+    const int p = R[e].prev, q = R[e].next;
+    const int un = R[u].next, up = R[u].prev, vn = R[v].next, vp = R[v].prev;
+    const bool nilnb = (p == NIL) | (q == NIL);
+    const int ps = nilnb ? e : p;
+    const bool del = R[ps].next == e;
+    int ea = u, eb = un, ec = v, ek = EV_INS;  // case 2
+    if (child) { ea = p; eb = e; ec = q; ek = del ? EV_DEL : EV_INS; }
+    if (which == 3) { ea = up; eb = u; ek = EV_DEL; }
+    if (which == 4) { eb = v; ec = vn; ek = EV_DEL; }
+    if (which == 5) { eb = vp; }
+    const bool emit = child ? (left ? e < u : e > v) : true;
+    if (child && nilnb) {
+      err = H3D_E_CHAIN;
+      break;
+    }
+    if (emit) {
+      if (k >= capRef - 1) {
+        err = H3D_E_OVERFLOW;
+        break;
+      }
+      if (k >= 0x4000) {
+        err = static_cast<int>(E_FASTPATH);
+        break;
+      }
+      Ev o;
+      o.t = best;
+      o.a = ea;
+      o.b = eb;
+      o.c = ec;
+      o.kind = ek;
+      out[k] = o;
+      const unsigned short inf = J.info[eb];
+      if ((inf & INFO_NONE) == INFO_NONE)
+        J.info[eb] = static_cast<unsigned short>((inf & INFO_CHAIN) | k);
+      ++k;
+    }
+    if (child) {  // _act
+      R[p].next = del ? q : e;
+      R[q].prev = del ? p : e;
+    }
+    if (left) {
+      ++i;
+      c0 = nL.t;
+      bL = nL.b;
+      if (i + 1 < kL) nL = evL[i + 1]; else nL.t = INF;
+    }
+    if (right) {
+      ++j;
+      c1 = nR.t;
+      bR = nR.b + nSL;
+      if (j + 1 < kR) nR = evR[j + 1]; else nR.t = INF;
+    }
+    u = (which == 2) ? un : ((which == 3) ? up : u);
+    v = (which == 4) ? vn : ((which == 5) ? vp : v);
+    c2 = evt_rec(R, u, R[u].next, v);
+    c3 = evt_rec(R, R[u].prev, u, v);
+    c4 = evt_rec(R, u, v, R[v].next);
+    c5 = evt_rec(R, u, R[v].prev, v);
+    tcur = best;
+  }
+  return err ? err : k;
 }
 
-// Warp-cooperative compaction + write-out of one merged job (warp-wide call).
-// mark[p] != 0 keeps p; afterwards mark[p] holds its new id (or -1).
-__device__ void writeout_job_warp(const GroupBuf &in, const GroupBuf &out, JobView v, long long L,
-                                  long long M, int nSL, int nS, int k, long long gidx,
-                                  long long *err) {
-  const int lane = threadIdx.x & 31;
-  int base = 0;
-  for (int p0 = 0; p0 < nS; p0 += 32) {
-    const int p = p0 + lane;
-    const bool keep = p < nS && v.mark[p] != 0;
-    const unsigned bal = __ballot_sync(FULL, keep);
-    if (p < nS) v.mark[p] = keep ? base + __popc(bal & ((1u << lane) - 1)) : -1;
-    base += __popc(bal);
-  }
-  __syncwarp();
-  bool bad = false;
-  for (int p = lane; p < nS; p += 32) {
-    const int id = v.mark[p];
-    if (id < 0) continue;
-    Rec r = v.rec[p];
-    if (r.prev != NIL) {
-      r.prev = v.mark[r.prev];
-      bad |= r.prev < 0;
-    }
-    if (r.next != NIL) {
-      r.next = v.mark[r.next];
-      bad |= r.next < 0;
-    }
-    out.rec[L + id] = r;
-    out.gid[L + id] = in.gid[p < nSL ? L + p : M + (p - nSL)];
-  }
-  for (int e = lane; e < k; e += 32) {
-    Ev o = v.out[e];
-    o.a = v.mark[o.a];
-    o.b = v.mark[o.b];
-    o.c = v.mark[o.c];
-    bad |= (o.a < 0) | (o.b < 0) | (o.c < 0);
-    out.ev[2 * L + e] = o;
-  }
-  if (__any_sync(FULL, bad) && lane == 0) raise_err(err, E_FASTPATH);
-  if (lane == 0) out.hdr[gidx] = make_int2(base, k);
-}
+constexpr int TPJ_TPB = 128;
+constexpr int TPJ_REC_BYTES = 34;  // 32-byte record + 2-byte info per point
 
-template <int TPB>
-__global__ void __launch_bounds__(TPB) k_fast_level(GroupBuf in, GroupBuf out, long long n,
-                                                    int level, int *deferred, int *ndeferred,
-                                                    long long *err, int verify, int budget) {
+// One thread per merge job (levels with many jobs).  Each thread's slice of
+// the shared-memory pool holds its job's records and info table; slices are
+// packed by a block-wide prefix scan of the actual sizes (jobs that do not
+// fit wait for the next round).
+__global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(GroupBuf in, GroupBuf out, long long n,
+                                                     int level, long long *err, int pool) {
   extern __shared__ __align__(16) unsigned char smem[];
-  typedef cub::BlockScan<long long, TPB> Scan;
+  typedef cub::BlockScan<int, TPJ_TPB> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
-
   const long long size = 1ll << level, half = size >> 1;
   const long long jobs = (n + size - 1) >> level;
-  const long long j = blockIdx.x * (long long)TPB + threadIdx.x;
+  const long long j = blockIdx.x * (long long)TPJ_TPB + threadIdx.x;
   const long long L = j << level, M = L + half;
-  const long long R = (L + size < n) ? L + size : n;
+  const long long R_ = (L + size < n) ? L + size : n;
   const bool valid = j < jobs;
-  bool pending = valid && (R - L > half);
   int nSL = 0, kL = 0, nSR = 0, kR = 0;
-  long long f = 0;
+  bool pending = false;
   if (valid) {
     const int2 hl = in.hdr[2 * j];
     nSL = hl.x;
     kL = hl.y;
-    if (pending) {
+    if (R_ - L > half) {
       const int2 hr = in.hdr[2 * j + 1];
       nSR = hr.x;
       kR = hr.y;
-      f = job_bytes(nSL + nSR, kL + kR);
-    }
-    if (!pending || f > budget) {
-      // carries and oversize jobs go to k_fast_big
-      deferred[atomicAdd(ndeferred, 1)] = static_cast<int>(j);
-      pending = false;
-    }
-  }
-  const int lane = threadIdx.x & 31;
-  while (__syncthreads_or(pending)) {
-    long long off, total;
-    Scan(scan_tmp).ExclusiveSum(pending ? f : 0ll, off, total);
-    const bool active = pending && off + f <= budget;
-    unsigned char *mine = smem + (active ? off : 0);
-    // stage: the warp copies each active lane's child runs in turn
-    unsigned todo = __ballot_sync(FULL, active);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const long long sL = __shfl_sync(FULL, L, src), sM = __shfl_sync(FULL, M, src);
-      const int snSL = __shfl_sync(FULL, nSL, src), snSR = __shfl_sync(FULL, nSR, src);
-      const int skL = __shfl_sync(FULL, kL, src), skR = __shfl_sync(FULL, kR, src);
-      const long long soff = __shfl_sync(FULL, off, src);
-      stage_job(in, carve_job(smem + soff, snSL + snSR, skL, skR), sL, sM, snSL, snSR, skL, skR,
-                lane, 32);
-    }
-    __syncwarp();
-    long long k = 0;
-    if (active) {
-      JobView v = carve_job(mine, nSL + nSR, kL, kR);
-      k = merge_compact(v.rec, nSL, nSL + nSR, v.evL, kL, 0, v.evR, kR, nSL, v.out,
-                        2 * (nSL + nSR), v.mark, 2 * (R - L), R - L, verify != 0);
-      if (k < 0) raise_err(err, k);
-    }
-    __syncwarp();
-    // write-out: the warp compacts and stores each active lane's job in turn
-    todo = __ballot_sync(FULL, active && k >= 0);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const long long sL = __shfl_sync(FULL, L, src), sM = __shfl_sync(FULL, M, src);
-      const int snSL = __shfl_sync(FULL, nSL, src), snSR = __shfl_sync(FULL, nSR, src);
-      const int skL = __shfl_sync(FULL, kL, src), skR = __shfl_sync(FULL, kR, src);
-      const long long soff = __shfl_sync(FULL, off, src);
-      const int sk = static_cast<int>(__shfl_sync(FULL, k, src));
-      const long long sj = __shfl_sync(FULL, j, src);
-      writeout_job_warp(in, out, carve_job(smem + soff, snSL + snSR, skL, skR), sL, sM, snSL,
-                        snSL + snSR, sk, sj, err);
-    }
-    pending = pending && !active;
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------- big jobs
-// One CTA per deferred job: carries are copied; merges are staged in this
-// CTA's (large) shared memory when they fit, else run in place in global
-// memory using the output group's own slot range as scratch.
-template <int TPB>
-__global__ void __launch_bounds__(TPB) k_fast_big(GroupBuf in, GroupBuf out, long long n,
-                                                  int level, const int *deferred,
-                                                  const int *ndeferred, long long *err,
-                                                  int verify, int budget) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  typedef cub::BlockScan<int, TPB> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ long long s_k;
-  __shared__ int s_base;
-  const int count = *ndeferred;
-  const long long size = 1ll << level, half = size >> 1;
-  for (int w = blockIdx.x; w < count; w += gridDim.x) {
-    const long long j = deferred[w];
-    const long long L = j << level, M = L + half;
-    const long long R = (L + size < n) ? L + size : n;
-    const int2 hl = in.hdr[2 * j];
-    const int nSL = hl.x, kL = hl.y;
-    if (R - L <= half) {  // carry (copy_log, parallel.py:107-108)
-      for (int p = threadIdx.x; p < nSL; p += TPB) {
+      pending = true;
+    } else {  // carry (copy_log, parallel.py:107-108)
+      for (int p = 0; p < nSL; ++p) {
         out.rec[L + p] = in.rec[L + p];
         out.gid[L + p] = in.gid[L + p];
       }
-      for (int e = threadIdx.x; e < kL; e += TPB) out.ev[2 * L + e] = in.ev[2 * L + e];
-      if (threadIdx.x == 0) out.hdr[j] = hl;
-      __syncthreads();
+      for (int e = 0; e < kL; ++e) out.ev[2 * L + e] = in.ev[2 * L + e];
+      out.hdr[j] = hl;
+    }
+  }
+  const int nS = nSL + nSR;
+  const int need = static_cast<int>(align8((long long)TPJ_REC_BYTES * nS));
+  if (pending && (need > pool || nS >= 0x4000)) {
+    raise_err(err, E_FASTPATH);  // the host never routes such jobs here
+    pending = false;
+  }
+  while (__syncthreads_or(pending)) {
+    int off, total;
+    Scan(scan_tmp).ExclusiveSum(pending ? need : 0, off, total);
+    const bool run = pending && off + need <= pool;
+    if (run) {
+      TpjJob J;
+      J.R = reinterpret_cast<Rec *>(smem + off);
+      J.info = reinterpret_cast<unsigned short *>(J.R + nS);
+      J.nSL = nSL;
+      Rec *R = J.R;
+      {  // stage: independent loads first, then shared stores
+        const Rec *__restrict__ gl = in.rec + L;
+        const Rec *__restrict__ gr = in.rec + M;
+        int p = 0;
+        for (; p + 4 <= nS; p += 4) {
+          Rec r0 = p < nSL ? gl[p] : gr[p - nSL];
+          Rec r1 = p + 1 < nSL ? gl[p + 1] : gr[p + 1 - nSL];
+          Rec r2 = p + 2 < nSL ? gl[p + 2] : gr[p + 2 - nSL];
+          Rec r3 = p + 3 < nSL ? gl[p + 3] : gr[p + 3 - nSL];
+          R[p] = r0;
+          R[p + 1] = r1;
+          R[p + 2] = r2;
+          R[p + 3] = r3;
+        }
+        for (; p < nS; ++p) R[p] = p < nSL ? gl[p] : gr[p - nSL];
+        for (p = nSL; p < nS; ++p) {
+          if (R[p].prev != NIL) R[p].prev += nSL;
+          if (R[p].next != NIL) R[p].next += nSL;
+        }
+      }
+      for (int p = 0; p < nS; ++p) {
+        const int pr = R[p].prev;
+        const bool chain = p == 0 || p == nSL || (pr != NIL && R[pr].next == p);
+        J.info[p] = chain ? (INFO_CHAIN | INFO_NONE) : INFO_NONE;
+      }
+      int u0 = 0, v0 = 0;
+      Ev *evo = out.ev + 2 * L;
+      const long long k = merge_tpj(J, in.ev + 2 * L, kL, in.ev + 2 * M, kR, evo, 2 * (R_ - L),
+                                    R_ - L, &u0, &v0);
+      if (k < 0) {
+        raise_err(err, k);
+      } else {
+        // start-of-time links of the merged group (see rebuild_writeout)
+        int cnt = 0;
+        for (int p = 0; p < nS; ++p) {
+          const unsigned short inf = J.info[p];
+          const bool chain = (inf & INFO_CHAIN) && (p < nSL ? p <= u0 : p >= v0);
+          const int fe = inf & INFO_NONE;
+          const bool keep = chain || fe != INFO_NONE;
+          int prv = NIL, nxt = NIL;
+          if (chain) {
+            const Rec &r = p < nSL ? in.rec[L + p] : in.rec[M + (p - nSL)];
+            const int o = p < nSL ? 0 : nSL;
+            prv = r.prev == NIL ? NIL : r.prev + o;
+            nxt = r.next == NIL ? NIL : r.next + o;
+            if (p == u0) nxt = v0;
+            if (p == v0) prv = u0;
+          } else if (keep) {
+            prv = evo[fe].a;
+            nxt = evo[fe].c;
+          }
+          R[p].prev = prv;
+          R[p].next = nxt;
+          J.info[p] = keep ? static_cast<unsigned short>(cnt++) : 0xffff;
+        }
+        bool bad = false;
+        // events first (they read arbitrary new ids), in place in HBM
+        for (int e = 0; e < k; ++e) {
+          Ev o = evo[e];
+          const unsigned short na = J.info[o.a], nb = J.info[o.b], nc = J.info[o.c];
+          bad |= (na == 0xffff) | (nb == 0xffff) | (nc == 0xffff);
+          o.a = na;
+          o.b = nb;
+          o.c = nc;
+          evo[e] = o;
+        }
+        for (int p = 0; p < nS; ++p) {
+          const unsigned short id = J.info[p];
+          if (id == 0xffff) continue;
+          Rec r = R[p];
+          r.prev = r.prev == NIL ? NIL : J.info[r.prev];
+          r.next = r.next == NIL ? NIL : J.info[r.next];
+          bad |= (r.prev == 0xffff) | (r.next == 0xffff);
+          out.rec[L + id] = r;
+          out.gid[L + id] = in.gid[p < nSL ? L + p : M + (p - nSL)];
+        }
+        if (bad) raise_err(err, E_FASTPATH);
+        out.hdr[j] = make_int2(cnt, static_cast<int>(k));
+      }
+      pending = false;
+    }
+  }
+}
+
+// -------------------------------------------------------------- warp merge
+struct WarpScratch {
+  Ev ev[32];
+  int side[32];
+};
+
+__device__ __forceinline__ int count_less(double a, double key) {
+  // number of entries < key in the warp-sorted sequence a (one per lane)
+  int pos = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const double x = __shfl_sync(FULL, a, pos + step - 1);
+    if (x < key) pos += step;
+  }
+  const double x = __shfl_sync(FULL, a, pos);
+  if (x < key) ++pos;
+  return pos;
+}
+
+__device__ __forceinline__ int count_leq(double a, double key) {
+  int pos = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const double x = __shfl_sync(FULL, a, pos + step - 1);
+    if (x <= key) pos += step;
+  }
+  const double x = __shfl_sync(FULL, a, pos);
+  if (x <= key) ++pos;
+  return pos;
+}
+
+__device__ __forceinline__ void first_event(int *first, int b, int idx) {
+  const int cur = *reinterpret_cast<volatile int *>(&first[b]);
+  atomicMin(&first[b], (cur & FIRST_FLAG) | idx);
+}
+
+// The warp-cooperative merge.  All lanes call it; returns k (warp-uniform)
+// or a negative code.  R[0, nS): records at -inf (left [0,nSL), right
+// [nSL,nS)); evL/evR: child events in HBM with child-local ids (right ids get
+// +nSL); out: merged events (local ids); first[p]: FIRST_FLAG if p is on its
+// child's -inf chain, low bits = index of p's first merged event.
+__device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int kL,
+                                const Ev *__restrict__ evR, int kR, Ev *out, int capO,
+                                int *first, long long capRef, long long limitRef,
+                                WarpScratch *ws, int *pu0, int *pv0) {
+  const int lane = threadIdx.x & 31;
+  const unsigned ltmask = (1u << lane) - 1;
+  int u = nSL - 1, v = nSL, st = 0;
+  if (lane == 0) st = bridge_rec(R, &u, &v, limitRef);
+  st = __shfl_sync(FULL, st, 0);
+  if (st < 0) return H3D_E_BRIDGE;
+  u = __shfl_sync(FULL, u, 0);
+  v = __shfl_sync(FULL, v, 0);
+  *pu0 = u;
+  *pv0 = v;
+  double c2, c3, c4, c5;
+  auto cands = [&]() {
+    double c = INF;
+    if (lane == 0)
+      c = evt_rec(R, u, R[u].next, v);
+    else if (lane == 1)
+      c = evt_rec(R, R[u].prev, u, v);
+    else if (lane == 2)
+      c = evt_rec(R, u, v, R[v].next);
+    else if (lane == 3)
+      c = evt_rec(R, u, R[v].prev, v);
+    c2 = __shfl_sync(FULL, c, 0);
+    c3 = __shfl_sync(FULL, c, 1);
+    c4 = __shfl_sync(FULL, c, 2);
+    c5 = __shfl_sync(FULL, c, 3);
+  };
+  cands();
+  int i = 0, j = 0, k = 0, errc = 0;
+  double tcur = -INF;
+  for (;;) {
+    // next bridge event: earliest candidate strictly after tcur, lowest case on ties
+    double tb = INF;
+    int wb = -1;
+    if (c2 > tcur && c2 < tb) { tb = c2; wb = 2; }
+    if (c3 > tcur && c3 < tb) { tb = c3; wb = 3; }
+    if (c4 > tcur && c4 < tb) { tb = c4; wb = 4; }
+    if (c5 > tcur && c5 < tb) { tb = c5; wb = 5; }
+    const int remL = kL - i, remR = kR - j;
+    int f = 0, nb = 0;
+    bool child_next = false;
+    if (remL + remR > 0) {
+      // time-merge of the next 32 events of each child log (merge path)
+      double tl = INF, tr = INF;
+      Ev el, er;
+      if (lane < remL) {
+        el = evL[i + lane];
+        tl = el.t;
+      }
+      if (lane < remR) {
+        er = evR[j + lane];
+        er.a += nSL;
+        er.b += nSL;
+        er.c += nSL;
+        tr = er.t;
+      }
+      const int rl = lane + count_less(tr, tl);   // left first on equal times
+      const int rr = lane + count_leq(tl, tr);
+      if (lane < remL && rl < 32) {
+        ws->ev[rl] = el;
+        ws->side[rl] = 0;
+      }
+      if (lane < remR && rr < 32) {
+        ws->ev[rr] = er;
+        ws->side[rr] = 1;
+      }
+      __syncwarp();
+      nb = min(32, min(remL, 32) + min(remR, 32));
+      Ev my;
+      int side = 0;
+      if (lane < nb) {
+        my = ws->ev[lane];
+        side = ws->side[lane];
+      }
+      __syncwarp();
+      const double tprev = __shfl_up_sync(FULL, lane < nb ? my.t : INF, 1);
+      const bool valid = lane < nb;
+      // exact time ties are outside general position: the reference's strict
+      // `t > oldt` rule then skips events; leave those inputs to the exact path
+      if (valid && ((lane > 0 && my.t == tprev) || my.t == tb || my.t <= tcur)) errc = E_FASTPATH;
+      const bool touches = valid && (my.a == u || my.a == v || my.c == u || my.c == v);
+      const bool stop = !valid || touches || my.t > tb;
+      const unsigned sb = __ballot_sync(FULL, stop);
+      f = sb ? __ffs(sb) - 1 : 32;
+      // retire [0, f) in parallel
+      const bool pre = lane < f;
+      const bool surv = pre && (side == 0 ? my.b < u : my.b > v);
+      const unsigned vs = __ballot_sync(FULL, surv);
+      if (surv) {
+        const int pos = k + __popc(vs & ltmask);
+        if (pos >= capRef - 1) {
+          errc = H3D_E_OVERFLOW;
+        } else if (pos >= capO) {
+          errc = E_FASTPATH;
+        } else {
+          out[pos] = my;
+          first_event(first, my.b, pos);
+        }
+      }
+      k += __popc(vs);
+      const int key1 = pre ? my.a : (int)(0x80000000u + lane);
+      const int key2 = pre ? my.c : (int)(0x80000000u + lane);
+      const unsigned m1 = __match_any_sync(FULL, key1);
+      const unsigned m2 = __match_any_sync(FULL, key2);
+      if (pre && (31 - __clz(m1)) == lane) R[my.a].next = (my.kind == EV_INS) ? my.b : my.c;
+      if (pre && (31 - __clz(m2)) == lane) R[my.c].prev = (my.kind == EV_INS) ? my.b : my.a;
+      if (f > 0) tcur = __shfl_sync(FULL, my.t, f - 1);
+      const int nl = __popc(__ballot_sync(FULL, pre && side == 0));
+      i += nl;
+      j += f - nl;
+      // what comes next: a foot-touching child event before the bridge event?
+      if (f < nb) {
+        const double tf = __shfl_sync(FULL, my.t, f);
+        child_next = tf < tb;
+        if (child_next) {
+          const int a = __shfl_sync(FULL, my.a, f), b = __shfl_sync(FULL, my.b, f);
+          const int c = __shfl_sync(FULL, my.c, f), kd = __shfl_sync(FULL, my.kind, f);
+          const int sd = __shfl_sync(FULL, side, f);
+          __syncwarp();
+          if (lane == 0) {
+            const int p = R[b].prev, q = R[b].next;
+            if (p != a || q != c || p == NIL || q == NIL) {
+              errc = E_FASTPATH;
+            } else {
+              const int kind = (R[p].next == b) ? EV_DEL : EV_INS;
+              if (kind != kd) errc = E_FASTPATH;
+              if (sd == 0 ? b < u : b > v) {
+                if (k >= capRef - 1) {
+                  errc = H3D_E_OVERFLOW;
+                } else if (k >= capO) {
+                  errc = E_FASTPATH;
+                } else {
+                  Ev o;
+                  o.t = tf;
+                  o.a = a;
+                  o.b = b;
+                  o.c = c;
+                  o.kind = kind;
+                  out[k] = o;
+                  first_event(first, b, k);
+                }
+              }
+              act_rec(R, b);
+            }
+          }
+          if (sd == 0 ? b < u : b > v) ++k;
+          if (sd == 0)
+            ++i;
+          else
+            ++j;
+          tcur = tf;
+          __syncwarp();
+          cands();
+        }
+      }
+    }
+    errc = __reduce_min_sync(FULL, errc);
+    if (errc < 0) return errc;
+    if (child_next || f == nb && nb > 0 && (remL + remR > nb || tb == INF)) continue;
+    if (f == nb && remL + remR > nb) continue;
+    // the bridge event comes next (or nothing is left)
+    if (wb < 0) {
+      if (remL + remR - f == 0) break;
       continue;
     }
-    const int2 hr = in.hdr[2 * j + 1];
-    const int nSR = hr.x, kR = hr.y, nS = nSL + nSR;
-    const bool in_smem = job_bytes(nS, kL + kR) <= budget;
-    JobView v;
-    const Ev *evL, *evR;
-    if (in_smem) {
-      v = carve_job(smem, nS, kL, kR);
-      stage_job(in, v, L, M, nSL, nSR, kL, kR, threadIdx.x, TPB);
-      evL = v.evL;
-      evR = v.evR;
+    if (lane == 0) {
+      int a, b, c, kind;
+      if (wb == 2) {
+        a = u; b = R[u].next; c = v; kind = EV_INS; u = b;
+      } else if (wb == 3) {
+        a = R[u].prev; b = u; c = v; kind = EV_DEL; u = a;
+      } else if (wb == 4) {
+        a = u; b = v; c = R[v].next; kind = EV_DEL; v = c;
+      } else {
+        a = u; b = R[v].prev; c = v; kind = EV_INS; v = b;
+      }
+      if (k >= capRef - 1) {
+        errc = H3D_E_OVERFLOW;
+      } else if (k >= capO) {
+        errc = E_FASTPATH;
+      } else {
+        Ev o;
+        o.t = tb;
+        o.a = a;
+        o.b = b;
+        o.c = c;
+        o.kind = kind;
+        out[k] = o;
+        first_event(first, b, k);
+      }
+    }
+    errc = __shfl_sync(FULL, errc, 0);
+    if (errc < 0) return errc;
+    u = __shfl_sync(FULL, u, 0);
+    v = __shfl_sync(FULL, v, 0);
+    ++k;
+    tcur = tb;
+    __syncwarp();
+    cands();
+  }
+  return k;
+}
+
+// Parallel rebuild of the merged group's start-of-time links, compaction and
+// write-out (warp-wide).  Kept = merged -inf chain (left chain up to u0, right
+// chain from v0) U every point of the merged log.  Links: chain points keep
+// their -inf links (u0 -> v0 stitched), the others get the neighbours of
+// their first event (an insertion: a point off the -inf chain enters the
+// hull once).  These are exactly the links the reference's rewind leaves on
+// every kept point.
+__device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R, Ev *evo,
+                                 int *first, long long L, long long M, int nSL, int nS, int k,
+                                 int u0, int v0, long long gidx, bool in_place, long long *err) {
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  // A: final links (local ids) into R, keep flag into first
+  for (int p = lane; p < nS; p += 32) {
+    const int fp = first[p];
+    const bool chain = (fp & FIRST_FLAG) && (p < nSL ? p <= u0 : p >= v0);
+    const int fe = fp & FIRST_NONE;
+    const bool hasev = fe != FIRST_NONE;
+    int prv = NIL, nxt = NIL;
+    if (chain) {
+      const Rec o = (p < nSL) ? in.rec[L + p] : in.rec[M + (p - nSL)];
+      const int off = (p < nSL) ? 0 : nSL;
+      prv = (o.prev == NIL) ? NIL : o.prev + off;
+      nxt = (o.next == NIL) ? NIL : o.next + off;
+      if (p == u0) nxt = v0;
+      if (p == v0) prv = u0;
+    } else if (hasev) {
+      prv = evo[fe].a;
+      nxt = evo[fe].c;
+    }
+    R[p].prev = prv;
+    R[p].next = nxt;
+    first[p] = (chain || hasev) ? 1 : 0;
+  }
+  __syncwarp();
+  // B: new ids
+  int cnt = 0;
+  for (int p0 = 0; p0 < nS; p0 += 32) {
+    const int p = p0 + lane;
+    const bool keep = p < nS && first[p] != 0;
+    const unsigned bal = __ballot_sync(FULL, keep);
+    if (p < nS) first[p] = keep ? cnt + __popc(bal & ((1u << lane) - 1)) : -1;
+    cnt += __popc(bal);
+  }
+  __syncwarp();
+  // C: events (in place when evo aliases out.ev)
+  for (int e = lane; e < k; e += 32) {
+    Ev o = evo[e];
+    o.a = first[o.a];
+    o.b = first[o.b];
+    o.c = first[o.c];
+    bad |= (o.a < 0) | (o.b < 0) | (o.c < 0);
+    out.ev[2 * L + e] = o;
+  }
+  // D: links remapped in place
+  for (int p = lane; p < nS; p += 32) {
+    if (first[p] < 0) continue;
+    Rec &r = R[p];
+    if (r.prev != NIL) {
+      r.prev = first[r.prev];
+      bad |= r.prev < 0;
+    }
+    if (r.next != NIL) {
+      r.next = first[r.next];
+      bad |= r.next < 0;
+    }
+  }
+  __syncwarp();
+  // E: move records and gids (chunked read-all / write; ids only move left,
+  // and a gid write only lands on ids already consumed)
+  for (int p0 = 0; p0 < nS; p0 += 32) {
+    const int p = p0 + lane;
+    int id = -1, g = 0;
+    Rec r;
+    if (p < nS) {
+      id = first[p];
+      if (id >= 0) {
+        r = R[p];
+        g = in.gid[p < nSL ? L + p : M + (p - nSL)];
+      }
+    }
+    __syncwarp();
+    if (id >= 0) {
+      out.rec[L + id] = r;
+      out.gid[L + id] = g;
+    }
+    __syncwarp();
+  }
+  (void)in_place;
+  if (__any_sync(FULL, bad) && lane == 0) raise_err(err, E_FASTPATH);
+  if (lane == 0) out.hdr[gidx] = make_int2(cnt, k);
+}
+
+__device__ __forceinline__ long long warp_job_bytes(int nS) {
+  return align8(32ll * nS + 24ll * 2 * nS + 4ll * nS);
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_fast_warp(GroupBuf in, GroupBuf out, long long n,
+                                                          int level, long long *err, int pool) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ WarpScratch scratch[WARPS];
+  __shared__ long long s_need[WARPS];
+  __shared__ int s_done[WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long size = 1ll << level, half = size >> 1;
+  const long long jobs = (n + size - 1) >> level;
+  const long long j = blockIdx.x * (long long)WARPS + warp;
+  const long long L = j << level, M = L + half;
+  const long long R_ = (L + size < n) ? L + size : n;
+  const bool valid = j < jobs;
+  int nSL = 0, kL = 0, nSR = 0, kR = 0;
+  bool merge = false;
+  if (valid) {
+    const int2 hl = in.hdr[2 * j];
+    nSL = hl.x;
+    kL = hl.y;
+    merge = R_ - L > half;
+    if (merge) {
+      const int2 hr = in.hdr[2 * j + 1];
+      nSR = hr.x;
+      kR = hr.y;
+    } else {  // carry (copy_log, parallel.py:107-108)
+      for (int p = lane; p < nSL; p += 32) {
+        out.rec[L + p] = in.rec[L + p];
+        out.gid[L + p] = in.gid[L + p];
+      }
+      for (int e = lane; e < kL; e += 32) out.ev[2 * L + e] = in.ev[2 * L + e];
+      if (lane == 0) out.hdr[j] = hl;
+    }
+  }
+  const int nS = nSL + nSR;
+  const long long need = merge ? warp_job_bytes(nS) : 0;
+  const bool global_mode = merge && need > pool;
+  bool pending = merge && !global_mode;
+  if (lane == 0) s_done[warp] = 0;
+  if (global_mode) {
+    // in place in HBM: records at out.rec[L..L+nS), merged events at
+    // out.ev[2L..2L+2nS), first-event table in out.gid[L..L+nS)
+    Rec *Rr = out.rec + L;
+    Ev *evo = out.ev + 2 * L;
+    int *first = out.gid + L;
+    for (int p = lane; p < nS; p += 32) {
+      Rec r = (p < nSL) ? in.rec[L + p] : in.rec[M + (p - nSL)];
+      if (p >= nSL) {
+        if (r.prev != NIL) r.prev += nSL;
+        if (r.next != NIL) r.next += nSL;
+      }
+      Rr[p] = r;
+    }
+    __syncwarp();
+    for (int p = lane; p < nS; p += 32) {
+      const int pr = Rr[p].prev;
+      const bool chain = (p == 0 || p == nSL) || (pr != NIL && Rr[pr].next == p);
+      first[p] = (chain ? FIRST_FLAG : 0) | FIRST_NONE;
+    }
+    __syncwarp();
+    int u0, v0;
+    const long long k = merge_warp(Rr, nSL, in.ev + 2 * L, kL, in.ev + 2 * M, kR, evo, 2 * nS,
+                                   first, 2 * (R_ - L), R_ - L, &scratch[warp], &u0, &v0);
+    if (k < 0) {
+      if (lane == 0) raise_err(err, k);
     } else {
-      // global scratch inside the output group's slots: records at [L, L+nS)
-      // (nS <= R-L), marks in the gid slots, merged events at [2L, 2L+2nS)
-      v.rec = out.rec + L;
-      v.mark = out.gid + L;
-      v.out = out.ev + 2 * L;
-      for (int p = threadIdx.x; p < nS; p += TPB) {
-        Rec r;
-        if (p < nSL) {
-          r = in.rec[L + p];
-        } else {
-          r = in.rec[M + (p - nSL)];
+      rebuild_writeout(in, out, Rr, evo, first, L, M, nSL, nS, static_cast<int>(k), u0, v0, j,
+                       true, err);
+    }
+  }
+  // shared-memory pool: warps whose jobs fit run together, the rest wait
+  for (;;) {
+    if (lane == 0) s_need[warp] = pending ? need : 0;
+    __syncthreads();
+    long long off = 0, total = 0;
+    bool any = false;
+    for (int w = 0; w < WARPS; ++w) {
+      const long long nw = s_need[w];
+      if (nw > 0) any = true;
+      if (w < warp) off += nw;
+      total += nw;
+    }
+    (void)total;
+    __syncthreads();
+    if (!any) break;
+    // a warp runs this round if its prefix fits (the first pending one always does)
+    const bool run = pending && off + need <= pool;
+    if (run) {
+      unsigned char *mine = smem + off;
+      Rec *Rr = reinterpret_cast<Rec *>(mine);
+      Ev *evo = reinterpret_cast<Ev *>(mine + 32ll * nS);
+      int *first = reinterpret_cast<int *>(evo + 2 * nS);
+      for (int p = lane; p < nS; p += 32) {
+        Rec r = (p < nSL) ? in.rec[L + p] : in.rec[M + (p - nSL)];
+        if (p >= nSL) {
           if (r.prev != NIL) r.prev += nSL;
           if (r.next != NIL) r.next += nSL;
         }
-        v.rec[p] = r;
-        v.mark[p] = 0;
+        Rr[p] = r;
       }
-      evL = in.ev + 2 * L;
-      evR = in.ev + 2 * M;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      s_k = merge_compact(v.rec, nSL, nS, evL, kL, 0, evR, kR, nSL, v.out, 2 * nS, v.mark,
-                          2 * (R - L), R - L, verify != 0);
-      if (s_k < 0) raise_err(err, s_k);
-    }
-    __syncthreads();
-    const long long k = s_k;
-    if (k < 0) continue;
-    // new ids by a chunked block scan (in order, so in-place is safe)
-    if (threadIdx.x == 0) s_base = 0;
-    __syncthreads();
-    for (int p0 = 0; p0 < nS; p0 += TPB) {
-      const int p = p0 + threadIdx.x;
-      const int keep = (p < nS && v.mark[p] != 0) ? 1 : 0;
-      int pre, tot;
-      Scan(scan_tmp).ExclusiveSum(keep, pre, tot);
-      const int base = s_base;
-      __syncthreads();
-      if (p < nS) v.mark[p] = keep ? base + pre : -1;
-      if (threadIdx.x == 0) s_base = base + tot;
-      __syncthreads();
-    }
-    const int nKeep = s_base;
-    int bad = 0;
-    // events first (they read arbitrary marks), in place
-    for (long long e = threadIdx.x; e < k; e += TPB) {
-      Ev o = v.out[e];
-      o.a = v.mark[o.a];
-      o.b = v.mark[o.b];
-      o.c = v.mark[o.c];
-      bad |= (o.a < 0) | (o.b < 0) | (o.c < 0);
-      out.ev[2 * L + e] = o;
-    }
-    // links next (they read arbitrary marks), in place
-    for (int p = threadIdx.x; p < nS; p += TPB) {
-      if (v.mark[p] < 0) continue;
-      Rec &r = v.rec[p];
-      if (r.prev != NIL) {
-        r.prev = v.mark[r.prev];
-        bad |= r.prev < 0;
+      __syncwarp();
+      for (int p = lane; p < nS; p += 32) {
+        const int pr = Rr[p].prev;
+        const bool chain = (p == 0 || p == nSL) || (pr != NIL && Rr[pr].next == p);
+        first[p] = (chain ? FIRST_FLAG : 0) | FIRST_NONE;
       }
-      if (r.next != NIL) {
-        r.next = v.mark[r.next];
-        bad |= r.next < 0;
+      __syncwarp();
+      int u0, v0;
+      const long long k = merge_warp(Rr, nSL, in.ev + 2 * L, kL, in.ev + 2 * M, kR, evo, 2 * nS,
+                                     first, 2 * (R_ - L), R_ - L, &scratch[warp], &u0, &v0);
+      if (k < 0) {
+        if (lane == 0) raise_err(err, k);
+      } else {
+        rebuild_writeout(in, out, Rr, evo, first, L, M, nSL, nS, static_cast<int>(k), u0, v0,
+                         j, false, err);
       }
+      pending = false;
     }
-    __syncthreads();
-    // records + gids: chunked read-all / sync / write (destinations <= sources,
-    // and a gid write only lands on marks already consumed)
-    for (int p0 = 0; p0 < nS; p0 += TPB) {
-      const int p = p0 + threadIdx.x;
-      int id = -1;
-      Rec r;
-      int g = 0;
-      if (p < nS) {
-        id = v.mark[p];
-        if (id >= 0) {
-          r = v.rec[p];
-          g = in.gid[p < nSL ? L + p : M + (p - nSL)];
-        }
-      }
-      __syncthreads();
-      if (id >= 0) {
-        out.rec[L + id] = r;
-        out.gid[L + id] = g;
-      }
-      __syncthreads();
-    }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) raise_err(err, E_FASTPATH);
-    if (threadIdx.x == 0) out.hdr[j] = make_int2(nKeep, static_cast<int>(k));
     __syncthreads();
   }
 }
@@ -374,16 +818,14 @@ using namespace h3d;
 
 namespace {
 
-constexpr int kLevelTPB = 128;
-constexpr int kBigTPB = 256;
-constexpr int kLevelBudget = 96 * 1024;
-constexpr int kBigBudget = 200 * 1024;
-constexpr int kBigGrid = 296;
+constexpr int kWarps = 8;
+constexpr int kPool = 64 * 1024;
+constexpr int kTpjPool = 96 * 1024;
+constexpr int kTpjMaxLevel = 9;
+constexpr long long kTpjMinJobs = 16384;
 
 struct PassWS {
   GroupBuf A, B;
-  int *deferred;
-  int *ndeferred;  // one counter per level (64)
 };
 
 bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
@@ -393,9 +835,7 @@ bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
     g->gid = ar.take<int>(n);
     g->ev = ar.take<Ev>(2 * n);
   }
-  w.deferred = ar.take<int>(n);
-  w.ndeferred = ar.take<int>(64);
-  return ar.base == nullptr || w.ndeferred != nullptr;
+  return ar.base == nullptr || w.B.ev != nullptr;
 }
 
 bool g_attr_done = false;
@@ -420,37 +860,46 @@ int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign, void *w
   PassWS w;
   if (!carve_pass(ar, n, w)) return H3D_E_ARG;
   if (!g_attr_done) {
-    if (h3d_check(cudaFuncSetAttribute(k_fast_level<kLevelTPB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kLevelBudget)) ||
-        h3d_check(cudaFuncSetAttribute(k_fast_big<kBigTPB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kBigBudget)))
+    if (h3d_check(cudaFuncSetAttribute(k_fast_warp<kWarps>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kPool)) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kTpjPool)))
       return H3D_E_CUDA;
     g_attr_done = true;
   }
   long long *err = reinterpret_cast<long long *>(err_dev);
-  cudaMemsetAsync(w.ndeferred, 0, sizeof(int) * 64, s);
+  int levels = 0;
+  while ((1ll << levels) < n) ++levels;
   h3d_count_launches(1);
   k_fast_init<<<h3d_grid(n, 256) > 8192 ? 8192 : h3d_grid(n, 256), 256, 0, s>>>(sorted_pts, zsign,
                                                                                 n, w.A);
   GroupBuf src = w.A, dst = w.B;
-  int levels = 0;
-  while ((1ll << levels) < n) ++levels;
+  int which = 0;
   for (int lv = 1; lv <= levels; ++lv) {
     const long long jobs = (n + (1ll << lv) - 1) >> lv;
-    void *ev = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
-    h3d_count_launches(2);
-    k_fast_level<kLevelTPB><<<h3d_grid(jobs, kLevelTPB), kLevelTPB, kLevelBudget, s>>>(
-        src, dst, n, lv, w.deferred + 0, w.ndeferred + lv, err, verify, kLevelBudget);
-    k_fast_big<kBigTPB><<<kBigGrid, kBigTPB, kBigBudget, s>>>(
-        src, dst, n, lv, w.deferred, w.ndeferred + lv, err, verify, kBigBudget);
-    h3d_prof_end(ev, lv, zsign > 0 ? 0 : 1, s);
+    void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
+    h3d_count_launches(1);
+    // thread per job while jobs are plentiful and small, warp per job above
+    if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel) {
+      // pool sized for the level's worst case (nS <= 2^lv), capped
+      long long pool = (long long)TPJ_TPB * align8((long long)TPJ_REC_BYTES << lv);
+      if (pool > kTpjPool) pool = kTpjPool;
+      if (pool < 4096) pool = 4096;
+      k_fast_tpj<<<h3d_grid(jobs, TPJ_TPB), TPJ_TPB, pool, s>>>(src, dst, n, lv, err,
+                                                                static_cast<int>(pool));
+      h3d_prof_end(e0, lv + 1000, zsign > 0 ? 0 : 1, s);
+    } else {
+      k_fast_warp<kWarps><<<h3d_grid(jobs, kWarps), kWarps * 32, kPool, s>>>(src, dst, n, lv,
+                                                                             err, kPool);
+      h3d_prof_end(e0, lv, zsign > 0 ? 0 : 1, s);
+    }
     GroupBuf t = src;
     src = dst;
     dst = t;
+    which ^= 1;
   }
   if (h3d_check(cudaGetLastError())) return H3D_E_CUDA;
-  // the final group lives in `src`; report which buffer (0 = A, 1 = B)
-  return (levels & 1) ? 1 : 0;
+  return which;
 }
 
 int64_t h3d_fast_extract(void *ws_lower, void *ws_upper, int64_t n, int64_t final_lower,

@@ -1,16 +1,18 @@
-// fast.cuh -- data layout and the compact-group merge of the fused fast path.
+// fast.cuh -- data layout and merge routines of the fused fast path.
 //
 // Layout in HBM (per pass, double-buffered A/B):
 //   hdr[g]              int2 (nS, k) of group g at the current level
 //   rec[L .. L+nS)      Rec: x, y, z (f64, z negated on the upper pass) and the
-//                       chain links prev/next as GROUP-LOCAL ids (NIL = -1)
+//                       chain links prev/next as GROUP-LOCAL ids (NIL = -1),
+//                       at the group's start-of-time (t = -inf) state
 //   gid[L .. L+nS)      global sorted index of each record
-//   ev[2L .. 2L+k)      Ev: event time t (f64) and the facet (a, b, c) of the
-//                       event, group-local ids; b is the reference's log entry
+//   ev[2L .. 2L+k)      Ev: event time t (f64), the facet (a, b, c) of the
+//                       event in group-local ids, and its kind (insertion /
+//                       deletion); b is the reference's log entry
 // A group [L, R) keeps only the points that matter above it: its chain at
-// t = -inf plus every point its log mentions (S = -inf chain U log).  Local
-// ids preserve x order, so the reference's x comparisons become integer
-// comparisons (x is strictly increasing, store.py:70-71).
+// t = -inf plus every point its log mentions.  Local ids preserve x order, so
+// the reference's x comparisons become integer comparisons (x is strictly
+// increasing, store.py:70-71).
 #pragma once
 #include "h3d_device.cuh"
 
@@ -23,11 +25,14 @@ struct __align__(8) Rec {
 
 struct __align__(8) Ev {
   double t;
-  int a, b, c, pad;
+  int a, b, c, kind;  // kind: 0 = b inserted between a and c, 1 = b deleted
 };
 
 static_assert(sizeof(Rec) == 32, "Rec must be one 32-byte sector");
 static_assert(sizeof(Ev) == 24, "Ev is 24 bytes");
+
+constexpr int EV_INS = 0;
+constexpr int EV_DEL = 1;
 
 // fast path could not reproduce the reference semantics: rerun exact
 constexpr long long E_FASTPATH = -13;
@@ -38,20 +43,19 @@ __device__ __forceinline__ double evt_rec(const Rec *R, int a, int b, int c) {
   return evtime_xyz(A.x, A.y, A.z, B.x, B.y, B.z, C.x, C.y, C.z);
 }
 
-// _act (_ckernels.pyx:49-60) on local links; returns -1 on a NIL neighbour
-__device__ __forceinline__ int act_rec(Rec *R, int e, int *p_out, int *q_out) {
+// _act (_ckernels.pyx:49-60) on local links; returns the kind or -1 on a
+// NIL neighbour
+__device__ __forceinline__ int act_rec(Rec *R, int e) {
   const int p = R[e].prev, q = R[e].next;
-  *p_out = p;
-  *q_out = q;
   if (p == NIL || q == NIL) return -1;
   if (R[p].next == e) {
     R[p].next = q;
     R[q].prev = p;
-  } else {
-    R[p].next = e;
-    R[q].prev = e;
+    return EV_DEL;
   }
-  return 0;
+  R[p].next = e;
+  R[q].prev = e;
+  return EV_INS;
 }
 
 // _find_bridge (_ckernels.pyx:63-83) on local ids
@@ -80,22 +84,19 @@ __device__ __forceinline__ int bridge_rec(const Rec *R, int *pu, int *pv, long l
   }
 }
 
-// One pairwise merge on a compact group pair: records R[0, nS) with the left
-// group at [0, nSL) and the right at [nSL, nS) (links already in this id
-// space); child logs evL[0,kL) and evR[0,kR) whose ids get +offL/+offR.
-// Semantics are _merge_one's (_ckernels.pyx:86-208) with three changes that
-// do not alter any decision: (1) a child event's candidate time is its
-// stored time (the time its facet got when it was emitted one level down,
-// computed by the same expression on the same triple); (2) the four bridge
-// candidates are recomputed only when a foot or a foot's neighbour changed;
-// (3) every emitted event records its facet (a, b, c) and time.  The rewind
-// is the reference's.  mark[p] |= 1 for every emitted point.
-// Returns k >= 0, or a negative code.
-__device__ long long merge_compact(Rec *R, int nSL, int nS, const Ev *evL, int kL, int offL,
-                                   const Ev *evR, int kR, int offR, Ev *out, int capO,
-                                   int *mark, long long capRef, long long limitRef,
-                                   bool verify) {
-  int u = nSL - 1, v = nSL;
+// Sequential merge (one thread) of ids [lo, mid) and [mid, hi) of R.  The
+// semantics are _merge_one's (_ckernels.pyx:86-208) with changes that do not
+// alter any decision: a child event's candidate time is its stored time (the
+// time its facet got when it was emitted one level down, by the same
+// expression on the same triple); the four bridge candidates are recomputed
+// only when a foot or a foot's neighbour changed; every emitted event records
+// its facet, kind and time.  The rewind is the reference's, so the links end
+// exactly as the reference leaves them.  mark[p] = 1 for every emitted p.
+// Returns k >= 0 or a negative code.
+__device__ long long merge_seq(Rec *R, int lo, int mid, const Ev *evL, int kL, const Ev *evR,
+                               int kR, Ev *out, int capO, int *mark, long long capRef,
+                               long long limitRef, bool verify) {
+  int u = mid - 1, v = mid;
   if (bridge_rec(R, &u, &v, limitRef) < 0) return H3D_E_BRIDGE;
   int i = 0, j = 0, k = 0;
   double tcur = -INF;
@@ -109,7 +110,7 @@ __device__ long long merge_compact(Rec *R, int nSL, int nS, const Ev *evL, int k
     c4 = evt_rec(R, u, v, R[v].next);           \
     c5 = evt_rec(R, u, R[v].prev, v);           \
   } while (0)
-#define H3D_EMIT(A_, B_, C_, T_)                        \
+#define H3D_EMIT(A_, B_, C_, T_, K_)                    \
   do {                                                  \
     if (k >= capRef - 1) return H3D_E_OVERFLOW;         \
     if (k >= capO) return E_FASTPATH;                   \
@@ -118,7 +119,8 @@ __device__ long long merge_compact(Rec *R, int nSL, int nS, const Ev *evL, int k
     o_.a = (A_);                                        \
     o_.b = (B_);                                        \
     o_.c = (C_);                                        \
-    mark[B_] |= 1;                                      \
+    o_.kind = (K_);                                     \
+    mark[B_] = 1;                                       \
     ++k;                                                \
   } while (0)
   H3D_BRIDGE_CANDS();
@@ -133,17 +135,13 @@ __device__ long long merge_compact(Rec *R, int nSL, int nS, const Ev *evL, int k
     if (c5 > tcur && c5 < best) { best = c5; which = 5; }
     if (which < 0) break;
     if (which <= 1) {
-      const Ev &ce = (which == 0) ? evL[i] : evR[j];
-      const int e = ce.b + (which == 0 ? offL : offR);
-      if (verify) {
-        // the stored time must be what the reference computes from the links
-        const double tl = evt_rec(R, R[e].prev, e, R[e].next);
-        if (!(tl == best)) return E_FASTPATH;
-      }
-      const bool outside = (which == 0) ? (e < u) : (e > v);
-      if (outside) H3D_EMIT(R[e].prev, e, R[e].next, best);
-      int p, q;
-      if (act_rec(R, e, &p, &q) < 0) return H3D_E_CHAIN;
+      const int e = (which == 0) ? evL[i].b : evR[j].b;
+      const int p = R[e].prev, q = R[e].next;
+      if (verify && !(evt_rec(R, p, e, q) == best)) return E_FASTPATH;
+      if (p == NIL || q == NIL) return H3D_E_CHAIN;
+      const int kind = (R[p].next == e) ? EV_DEL : EV_INS;
+      if ((which == 0) ? (e < u) : (e > v)) H3D_EMIT(p, e, q, best, kind);
+      act_rec(R, e);
       if (which == 0) {
         ++i;
         c0 = (i < kL) ? evL[i].t : INF;
@@ -154,23 +152,23 @@ __device__ long long merge_compact(Rec *R, int nSL, int nS, const Ev *evL, int k
       if (p == u || q == u || p == v || q == v) H3D_BRIDGE_CANDS();
     } else {
       switch (which) {
-        case 2: {
+        case 2: {  // u advances: the new foot enters the merged chain
           const int un = R[u].next;
-          H3D_EMIT(u, un, v, best);
+          H3D_EMIT(u, un, v, best, EV_INS);
           u = un;
           break;
         }
-        case 3:
-          H3D_EMIT(R[u].prev, u, v, best);
+        case 3:  // u leaves the merged chain
+          H3D_EMIT(R[u].prev, u, v, best, EV_DEL);
           u = R[u].prev;
           break;
-        case 4:
-          H3D_EMIT(u, v, R[v].next, best);
+        case 4:  // v leaves the merged chain
+          H3D_EMIT(u, v, R[v].next, best, EV_DEL);
           v = R[v].next;
           break;
-        default: {
+        default: {  // v retreats: the new foot enters the merged chain
           const int vp = R[v].prev;
-          H3D_EMIT(u, vp, v, best);
+          H3D_EMIT(u, vp, v, best, EV_INS);
           v = vp;
           break;
         }
@@ -187,8 +185,7 @@ __device__ long long merge_compact(Rec *R, int nSL, int nS, const Ev *evL, int k
   for (int idx = k - 1; idx >= 0; --idx) {
     const int e = out[idx].b;
     if (e <= u || e >= v) {
-      int p, q;
-      if (act_rec(R, e, &p, &q) < 0) return H3D_E_CHAIN;
+      if (act_rec(R, e) < 0) return H3D_E_CHAIN;
       if (e == u)
         u = R[u].prev;
       else if (e == v)
@@ -198,19 +195,12 @@ __device__ long long merge_compact(Rec *R, int nSL, int nS, const Ev *evL, int k
       R[e].prev = u;
       R[v].prev = e;
       R[e].next = v;
-      if (e < nSL)
+      if (e < mid)
         u = e;
       else
         v = e;
     }
   }
-  // the merged -inf chain (always kept): walk from the leftmost point
-  int steps = 0;
-  for (int p = 0; p != NIL; p = R[p].next) {
-    mark[p] |= 2;
-    if (++steps > nS) return E_FASTPATH;
-  }
-  (void)nS;
   return k;
 }
 

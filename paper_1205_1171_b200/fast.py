@@ -47,6 +47,15 @@ def profile_enable(on: bool) -> None:
     _lib.load().h3d_profile_enable(1 if on else 0)
 
 
+def kernel_of(tag: int):
+    """Decode a profile row's level tag -> (kernel name, level)."""
+    if tag >= 1000:
+        return "k_fast_tpj", tag - 1000
+    if tag < 0:
+        return "k_fast_leaf", tag
+    return "k_fast_warp", tag
+
+
 def profile_collect(max_rows: int = 4096):
     """[(level, pass, ms)] recorded since the last collect."""
     L = _lib.load()
