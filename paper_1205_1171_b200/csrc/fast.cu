@@ -23,6 +23,8 @@
 //                  reference's sequential rewind.  Jobs are staged in a
 //                  shared-memory pool when they fit, else run in place in HBM.
 //  * k_fast_extract  facets of both passes straight from the final events.
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "fast.cuh"
@@ -83,11 +85,13 @@ struct TpjJob {
 // Returns k or a negative code.
 __device__ long long merge_tpj(TpjJob &J, const Ev *__restrict__ evL, int kL,
                                const Ev *__restrict__ evR, int kR, Ev *out, long long capRef,
-                               long long limitRef, int *pu0, int *pv0) {
+                               long long limitRef, int *pu0, int *pv0, unsigned mask) {
   Rec *R = J.R;
   const int nSL = J.nSL;
   int u = nSL - 1, v = nSL;
-  if (bridge_rec(R, &u, &v, limitRef) < 0) return H3D_E_BRIDGE;
+  const int bst = bridge_rec(R, &u, &v, limitRef);
+  __syncwarp(mask);
+  if (bst < 0) return H3D_E_BRIDGE;
   *pu0 = u;
   *pv0 = v;
   int i = 0, j = 0, k = 0;
@@ -187,13 +191,13 @@ __device__ long long merge_tpj(TpjJob &J, const Ev *__restrict__ evL, int kL,
   return err ? err : k;
 }
 
-constexpr int TPJ_TPB = 128;
 constexpr int TPJ_REC_BYTES = 34;  // 32-byte record + 2-byte info per point
 
 // One thread per merge job (levels with many jobs).  Each thread's slice of
 // the shared-memory pool holds its job's records and info table; slices are
 // packed by a block-wide prefix scan of the actual sizes (jobs that do not
 // fit wait for the next round).
+template <int TPJ_TPB>
 __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(GroupBuf in, GroupBuf out, long long n,
                                                      int level, long long *err, int pool) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -235,6 +239,10 @@ __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(GroupBuf in, GroupBuf out,
     int off, total;
     Scan(scan_tmp).ExclusiveSum(pending ? need : 0, off, total);
     const bool run = pending && off + need <= pool;
+    // the lanes that run this round re-converge at every phase boundary
+    // (independent thread scheduling would otherwise let the variable-length
+    // staging loops split the warp and run the sweep once per split)
+    const unsigned rmask = __ballot_sync(0xffffffffu, run);
     if (run) {
       TpjJob J;
       J.R = reinterpret_cast<Rec *>(smem + off);
@@ -266,10 +274,12 @@ __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(GroupBuf in, GroupBuf out,
         const bool chain = p == 0 || p == nSL || (pr != NIL && R[pr].next == p);
         J.info[p] = chain ? (INFO_CHAIN | INFO_NONE) : INFO_NONE;
       }
+      __syncwarp(rmask);
       int u0 = 0, v0 = 0;
       Ev *evo = out.ev + 2 * L;
       const long long k = merge_tpj(J, in.ev + 2 * L, kL, in.ev + 2 * M, kR, evo, 2 * (R_ - L),
-                                    R_ - L, &u0, &v0);
+                                    R_ - L, &u0, &v0, rmask);
+      __syncwarp(rmask);
       if (k < 0) {
         raise_err(err, k);
       } else {
@@ -839,6 +849,10 @@ bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
 }
 
 bool g_attr_done = false;
+// thread-per-job tuning (H3D_TPJ_TPB, H3D_TPJ_FILL, H3D_TPJ_POOL_KB override)
+int g_tpj_tpb = 32;
+double g_tpj_fill = 0.5;
+long long g_tpj_pool = 24 * 1024;
 
 }  // namespace
 
@@ -862,9 +876,18 @@ int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign, void *w
   if (!g_attr_done) {
     if (h3d_check(cudaFuncSetAttribute(k_fast_warp<kWarps>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kPool)) ||
-        h3d_check(cudaFuncSetAttribute(k_fast_tpj, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kTpjPool)) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kTpjPool)) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kTpjPool)))
       return H3D_E_CUDA;
+    if (const char *e = getenv("H3D_TPJ_TPB")) g_tpj_tpb = atoi(e);
+    if (const char *e = getenv("H3D_TPJ_FILL")) g_tpj_fill = atof(e);
+    if (const char *e = getenv("H3D_TPJ_POOL_KB")) g_tpj_pool = atoll(e) * 1024;
+    if (g_tpj_tpb != 32 && g_tpj_tpb != 64) g_tpj_tpb = 128;
+    if (g_tpj_pool > kTpjPool) g_tpj_pool = kTpjPool;
     g_attr_done = true;
   }
   long long *err = reinterpret_cast<long long *>(err_dev);
@@ -881,12 +904,20 @@ int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign, void *w
     h3d_count_launches(1);
     // thread per job while jobs are plentiful and small, warp per job above
     if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel) {
-      // pool sized for the level's worst case (nS <= 2^lv), capped
-      long long pool = (long long)TPJ_TPB * align8((long long)TPJ_REC_BYTES << lv);
-      if (pool > kTpjPool) pool = kTpjPool;
-      if (pool < 4096) pool = 4096;
-      k_fast_tpj<<<h3d_grid(jobs, TPJ_TPB), TPJ_TPB, pool, s>>>(src, dst, n, lv, err,
-                                                                static_cast<int>(pool));
+      // threads per CTA and shared pool per level: the pool holds the CTA's
+      // jobs at an assumed fill of nS <= 2^lv * fill (rounds absorb overflow)
+      const int tpb = g_tpj_tpb;
+      long long pool = (long long)tpb * align8((long long)(TPJ_REC_BYTES * g_tpj_fill * (1ll << lv)));
+      if (pool > g_tpj_pool) pool = g_tpj_pool;
+      if (pool < (long long)TPJ_REC_BYTES << lv) pool = align8((long long)TPJ_REC_BYTES << lv);
+      if (pool < 2048) pool = 2048;
+      const unsigned grid = h3d_grid(jobs, tpb);
+      if (tpb == 32)
+        k_fast_tpj<32><<<grid, 32, pool, s>>>(src, dst, n, lv, err, static_cast<int>(pool));
+      else if (tpb == 64)
+        k_fast_tpj<64><<<grid, 64, pool, s>>>(src, dst, n, lv, err, static_cast<int>(pool));
+      else
+        k_fast_tpj<128><<<grid, 128, pool, s>>>(src, dst, n, lv, err, static_cast<int>(pool));
       h3d_prof_end(e0, lv + 1000, zsign > 0 ? 0 : 1, s);
     } else {
       k_fast_warp<kWarps><<<h3d_grid(jobs, kWarps), kWarps * 32, kPool, s>>>(src, dst, n, lv,
