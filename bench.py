@@ -233,6 +233,10 @@ def level_bytes(cfg: str):
         for lv, r in rows.items():
             out[(pi, lv)] = 4 * (r["E_in"] + r["E_out"]) + 40 * (r["D"] + 2 * r["J"])
             out[(pi, -lv)] = 4 * rows[1]["E_in"] + 4 * r["E_out"] + 40 * n
+    # pass index 2: one launch covering both passes of a level
+    for (pi, lv), b in list(out.items()):
+        if pi == 0 and (1, lv) in out:
+            out[(2, lv)] = b + out[(1, lv)]
     return out
 
 

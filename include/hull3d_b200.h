@@ -158,17 +158,18 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
  * group buffers: headers, 32-byte point records, ids, 24-byte events) */
 size_t h3d_fast_pass_workspace_bytes(int64_t n);
 
-/* One hull pass (build_movie, pkg/src/hull3d/parallel.py:68-112) over the
- * presorted points, all ceil(log2 n) levels, stream-ordered, no host sync.
- * zsign = +1.0 lower hull, -1.0 upper hull (z negated on load).  Errors are
- * recorded into *err_dev (device int64, first error wins; H3D_E_* codes or
- * -13 = the fast path cannot reproduce the reference semantics for this
- * input, rerun the exact seam path).  verify != 0 re-derives every child
- * event time from the links and flags any difference.  Returns which of the
- * workspace's two buffers holds the final group (0/1) or a negative code. */
-int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign,
-                      void *workspace, size_t workspace_bytes,
-                      int64_t *err_dev, int32_t verify, void *stream);
+/* Both hull passes (build_movie, pkg/src/hull3d/parallel.py:68-112) over the
+ * presorted points, all ceil(log2 n) levels, stream-ordered, no host sync:
+ * every level is ONE launch covering the lower (z as is) and the upper pass
+ * (z negated on load, api.py:215-216).  ws_lower / ws_upper are two
+ * workspaces of h3d_fast_pass_workspace_bytes(n) each.  Errors are recorded
+ * into *err_dev (device int64, first error wins; H3D_E_* codes or -13 = the
+ * fast path cannot reproduce the reference semantics for this input, rerun
+ * the exact seam path).  final_out (host int64[2]) receives which buffer of
+ * each workspace holds the final group.  Returns 0 or a negative code. */
+int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower,
+                        void *ws_upper, size_t workspace_bytes, int64_t *err_dev,
+                        int32_t verify, int64_t *final_out, void *stream);
 
 /* Facets of both passes from their final groups (extract_faces,
  * _ckernels.pyx:324-349): faces (cap,3) i32 in sorted indices, lower block

@@ -181,11 +181,14 @@ def _run_passes(sorted_pts, engine, solver, level_lists):
             nlev = level_count(sorted_pts.shape[0])
             per = [[0.0] * nlev, [0.0] * nlev]
             for lv, p, t in rows:
-                ms[p] += t
                 name, lv = fast.kernel_of(lv)
-                # a negative level is a fused kernel (levels 1..|lv|); its time
-                # is reported at its last level, 0.0 below it
-                per[p][abs(lv) - 1] += t / 1e3
+                # pass 2 = one launch covering both passes: split evenly
+                shares = ((0, t / 2), (1, t / 2)) if p == 2 else ((p, t),)
+                for pp, tt in shares:
+                    ms[pp] += tt
+                    # a negative level is a fused kernel (levels 1..|lv|); its
+                    # time is reported at its last level, 0.0 below it
+                    per[pp][abs(lv) - 1] += tt / 1e3
                 if E.PROFILE is not None:
                     E.PROFILE.append((name, p, lv, t))
             if want_levels:

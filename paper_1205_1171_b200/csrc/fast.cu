@@ -39,6 +39,11 @@ struct GroupBuf {
   Ev *ev;
 };
 
+// both passes of a level in one launch: blockIdx.y = 0 lower, 1 upper
+struct Pass2 {
+  GroupBuf in0, in1, out0, out1;
+};
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int FIRST_FLAG = 1 << 30;        // "on a child's -inf chain"
 constexpr int FIRST_NONE = FIRST_FLAG - 1; // no event yet
@@ -47,7 +52,9 @@ __host__ __device__ __forceinline__ long long align8(long long b) { return (b + 
 
 // --------------------------------------------------------- thread per job
 // level 0: every point is a one-point group with an empty log
-__global__ void k_fast_init(const double *__restrict__ pts, double zs, long long n, GroupBuf g) {
+__global__ void k_fast_init(const double *__restrict__ pts, long long n, Pass2 P) {
+  const GroupBuf g = blockIdx.y ? P.in1 : P.in0;
+  const double zs = blockIdx.y ? -1.0 : 1.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     Rec r;
@@ -198,8 +205,10 @@ constexpr int TPJ_REC_BYTES = 34;  // 32-byte record + 2-byte info per point
 // packed by a block-wide prefix scan of the actual sizes (jobs that do not
 // fit wait for the next round).
 template <int TPJ_TPB>
-__global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(GroupBuf in, GroupBuf out, long long n,
-                                                     int level, long long *err, int pool) {
+__global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(Pass2 P, long long n, int level,
+                                                     long long *err, int pool) {
+  const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
+  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   extern __shared__ __align__(16) unsigned char smem[];
   typedef cub::BlockScan<int, TPJ_TPB> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -680,8 +689,10 @@ __device__ __forceinline__ long long warp_job_bytes(int nS) {
 }
 
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_fast_warp(GroupBuf in, GroupBuf out, long long n,
-                                                          int level, long long *err, int pool) {
+__global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, int level,
+                                                          long long *err, int pool) {
+  const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
+  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ WarpScratch scratch[WARPS];
   __shared__ long long s_need[WARPS];
@@ -858,7 +869,7 @@ long long g_tpj_pool = 24 * 1024;
 
 extern "C" {
 
-size_t h3d_fast_pass_workspace_bytes(int64_t n) {
+size_t h3d_fast_pass_workspace_bytes(int64_t n) {  // per pass
   if (n < 1) n = 1;
   h3d_arena ar(nullptr, 0);
   PassWS w;
@@ -866,13 +877,15 @@ size_t h3d_fast_pass_workspace_bytes(int64_t n) {
   return ar.used + 4096;
 }
 
-int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign, void *workspace,
-                      size_t workspace_bytes, int64_t *err_dev, int32_t verify, void *stream) {
+int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower, void *ws_upper,
+                        size_t workspace_bytes, int64_t *err_dev, int32_t verify,
+                        int64_t *final_out, void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  (void)verify;
   if (n < 2 || n > (1ll << 30)) return H3D_E_ARG;
-  h3d_arena ar(workspace, workspace_bytes);
-  PassWS w;
-  if (!carve_pass(ar, n, w)) return H3D_E_ARG;
+  h3d_arena a0(ws_lower, workspace_bytes), a1(ws_upper, workspace_bytes);
+  PassWS w0, w1;
+  if (!carve_pass(a0, n, w0) || !carve_pass(a1, n, w1)) return H3D_E_ARG;
   if (!g_attr_done) {
     if (h3d_check(cudaFuncSetAttribute(k_fast_warp<kWarps>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kPool)) ||
@@ -893,10 +906,10 @@ int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign, void *w
   long long *err = reinterpret_cast<long long *>(err_dev);
   int levels = 0;
   while ((1ll << levels) < n) ++levels;
+  Pass2 P{w0.A, w1.A, w0.B, w1.B};
   h3d_count_launches(1);
-  k_fast_init<<<h3d_grid(n, 256) > 8192 ? 8192 : h3d_grid(n, 256), 256, 0, s>>>(sorted_pts, zsign,
-                                                                                n, w.A);
-  GroupBuf src = w.A, dst = w.B;
+  const unsigned gi = h3d_grid(n, 256) > 4096 ? 4096 : h3d_grid(n, 256);
+  k_fast_init<<<dim3(gi, 2), 256, 0, s>>>(sorted_pts, n, P);
   int which = 0;
   for (int lv = 1; lv <= levels; ++lv) {
     const long long jobs = (n + (1ll << lv) - 1) >> lv;
@@ -911,26 +924,26 @@ int64_t h3d_fast_pass(const double *sorted_pts, int64_t n, double zsign, void *w
       if (pool > g_tpj_pool) pool = g_tpj_pool;
       if (pool < (long long)TPJ_REC_BYTES << lv) pool = align8((long long)TPJ_REC_BYTES << lv);
       if (pool < 2048) pool = 2048;
-      const unsigned grid = h3d_grid(jobs, tpb);
+      const dim3 grid(h3d_grid(jobs, tpb), 2);
       if (tpb == 32)
-        k_fast_tpj<32><<<grid, 32, pool, s>>>(src, dst, n, lv, err, static_cast<int>(pool));
+        k_fast_tpj<32><<<grid, 32, pool, s>>>(P, n, lv, err, static_cast<int>(pool));
       else if (tpb == 64)
-        k_fast_tpj<64><<<grid, 64, pool, s>>>(src, dst, n, lv, err, static_cast<int>(pool));
+        k_fast_tpj<64><<<grid, 64, pool, s>>>(P, n, lv, err, static_cast<int>(pool));
       else
-        k_fast_tpj<128><<<grid, 128, pool, s>>>(src, dst, n, lv, err, static_cast<int>(pool));
-      h3d_prof_end(e0, lv + 1000, zsign > 0 ? 0 : 1, s);
+        k_fast_tpj<128><<<grid, 128, pool, s>>>(P, n, lv, err, static_cast<int>(pool));
+      h3d_prof_end(e0, lv + 1000, 2, s);
     } else {
-      k_fast_warp<kWarps><<<h3d_grid(jobs, kWarps), kWarps * 32, kPool, s>>>(src, dst, n, lv,
-                                                                             err, kPool);
-      h3d_prof_end(e0, lv, zsign > 0 ? 0 : 1, s);
+      k_fast_warp<kWarps><<<dim3(h3d_grid(jobs, kWarps), 2), kWarps * 32, kPool, s>>>(P, n, lv,
+                                                                                   err, kPool);
+      h3d_prof_end(e0, lv, 2, s);
     }
-    GroupBuf t = src;
-    src = dst;
-    dst = t;
+    P = Pass2{P.out0, P.out1, P.in0, P.in1};
     which ^= 1;
   }
   if (h3d_check(cudaGetLastError())) return H3D_E_CUDA;
-  return which;
+  final_out[0] = which;
+  final_out[1] = which;
+  return 0;
 }
 
 int64_t h3d_fast_extract(void *ws_lower, void *ws_upper, int64_t n, int64_t final_lower,

@@ -80,15 +80,14 @@ def run_both(sorted_pts: torch.Tensor, verify: bool = False):
     state = torch.zeros(4, dtype=torch.int64, device=dev)  # err, kLo, kUp, pad
     err = state[0:1]
     counts = state[1:3]
-    fin = []
-    for ws, zs in ((ws_lo, 1.0), (ws_up, -1.0)):
-        r = L.h3d_fast_pass(sorted_pts.data_ptr(), n, zs, ws.data_ptr(), ws.numel(),
-                            err.data_ptr(), 1 if verify else 0, s)
-        if r < 0:
-            from .errors import check_merge
+    fin = (ctypes.c_int64 * 2)()
+    r = L.h3d_fast_passes(sorted_pts.data_ptr(), n, ws_lo.data_ptr(), ws_up.data_ptr(), wsb,
+                          err.data_ptr(), 1 if verify else 0, ctypes.addressof(fin), s)
+    if r < 0:
+        from .errors import check_merge
 
-            check_merge(int(r))
-        fin.append(int(r))
+        check_merge(int(r))
+    fin = [int(fin[0]), int(fin[1])]
     cap = max(2 * n, 8)
     faces = torch.empty((cap, 3), dtype=torch.int32, device=dev)
     r = L.h3d_fast_extract(ws_lo.data_ptr(), ws_up.data_ptr(), n, fin[0], fin[1],
