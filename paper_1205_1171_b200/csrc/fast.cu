@@ -345,50 +345,66 @@ __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(Pass2 P, long long n, int 
 }
 
 // -------------------------------------------------------------- warp merge
-struct WarpScratch {
-  Ev ev[32];
-  int side[32];
-};
-
-__device__ __forceinline__ int count_less(double a, double key) {
-  // number of entries < key in the warp-sorted sequence a (one per lane)
-  int pos = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    const double x = __shfl_sync(FULL, a, pos + step - 1);
-    if (x < key) pos += step;
-  }
-  const double x = __shfl_sync(FULL, a, pos);
-  if (x < key) ++pos;
-  return pos;
-}
-
-__device__ __forceinline__ int count_leq(double a, double key) {
-  int pos = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    const double x = __shfl_sync(FULL, a, pos + step - 1);
-    if (x <= key) pos += step;
-  }
-  const double x = __shfl_sync(FULL, a, pos);
-  if (x <= key) ++pos;
-  return pos;
-}
-
 __device__ __forceinline__ void first_event(int *first, int b, int idx) {
   const int cur = *reinterpret_cast<volatile int *>(&first[b]);
   atomicMin(&first[b], (cur & FIRST_FLAG) | idx);
 }
 
-// The warp-cooperative merge.  All lanes call it; returns k (warp-uniform)
-// or a negative code.  R[0, nS): records at -inf (left [0,nSL), right
-// [nSL,nS)); evL/evR: child events in HBM with child-local ids (right ids get
-// +nSL); out: merged events (local ids); first[p]: FIRST_FLAG if p is on its
+// Warp-wide merge path: the child logs evL[0,kL) and evR[0,kR) (each sorted
+// by time) merged into seq[0, kL+kR) by time, left first on equal times; the
+// right child's ids get +nSL and the side is kept in bit 1 of `kind`.  Each
+// lane finds its diagonal split by one binary search, then merges its
+// contiguous slice of the output sequentially.
+__device__ void merge_logs_warp(const Ev *__restrict__ evL, int kL, const Ev *__restrict__ evR,
+                                int kR, int nSL, Ev *seq) {
+  const int lane = threadIdx.x & 31;
+  const int K = kL + kR;
+  const int chunk = (K + 31) / 32;
+  const int d0 = min(K, lane * chunk), d1 = min(K, d0 + chunk);
+  int lo = max(0, d0 - kR), hi = min(d0, kL);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (evL[mid].t <= evR[d0 - mid - 1].t) lo = mid + 1; else hi = mid;
+  }
+  int i = lo, j = d0 - lo;
+  for (int d = d0; d < d1; ++d) {
+    const bool takeL = i < kL && (j >= kR || evL[i].t <= evR[j].t);
+    Ev o;
+    if (takeL) {
+      o = evL[i++];
+    } else {
+      o = evR[j++];
+      o.a += nSL;
+      o.b += nSL;
+      o.c += nSL;
+      o.kind |= 2;
+    }
+    seq[d] = o;
+  }
+  __syncwarp();
+}
+
+// The warp-cooperative merge (levels with few, large jobs).  All lanes call
+// it; returns k (warp-uniform) or a negative code.
+//
+// The sweep walks the time-merged child events 32 at a time.  Every event
+// before the first one that touches a bridge foot (its facet has u or v as a
+// neighbour) and before the next bridge event is retired in parallel:
+// survivors (left: b < u, right: b > v -- the reference's emission rule) get
+// output slots by a ballot prefix sum, and the link writes of the retired
+// events are resolved last-writer-wins with __match_any_sync (an event's
+// facet and kind say exactly what act() writes).  A foot-touching event or
+// a bridge event is then processed alone, with the four bridge candidates
+// recomputed on four lanes.  Decisions are the reference's, step for step,
+// as long as no two events share a time (exact ties are outside general
+// position and send the job to the exact path).
+//
+// R[0,nS): records at -inf (left [0,nSL), right [nSL,nS)); seq: merged child
+// events; out: merged events (HBM); first[p]: FIRST_FLAG if p is on its
 // child's -inf chain, low bits = index of p's first merged event.
-__device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int kL,
-                                const Ev *__restrict__ evR, int kR, Ev *out, int capO,
-                                int *first, long long capRef, long long limitRef,
-                                WarpScratch *ws, int *pu0, int *pv0) {
+__device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, Ev *out,
+                                int *first, long long capRef, long long limitRef, int *pu0,
+                                int *pv0) {
   const int lane = threadIdx.x & 31;
   const unsigned ltmask = (1u << lane) - 1;
   int u = nSL - 1, v = nSL, st = 0;
@@ -416,7 +432,7 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int
     c5 = __shfl_sync(FULL, c, 3);
   };
   cands();
-  int i = 0, j = 0, k = 0, errc = 0;
+  int ptr = 0, k = 0, errc = 0;
   double tcur = -INF;
   for (;;) {
     // next bridge event: earliest candidate strictly after tcur, lowest case on ties
@@ -426,64 +442,33 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int
     if (c3 > tcur && c3 < tb) { tb = c3; wb = 3; }
     if (c4 > tcur && c4 < tb) { tb = c4; wb = 4; }
     if (c5 > tcur && c5 < tb) { tb = c5; wb = 5; }
-    const int remL = kL - i, remR = kR - j;
-    int f = 0, nb = 0;
+    const int rem = kin - ptr;
     bool child_next = false;
-    if (remL + remR > 0) {
-      // time-merge of the next 32 events of each child log (merge path)
-      double tl = INF, tr = INF;
-      Ev el, er;
-      if (lane < remL) {
-        el = evL[i + lane];
-        tl = el.t;
-      }
-      if (lane < remR) {
-        er = evR[j + lane];
-        er.a += nSL;
-        er.b += nSL;
-        er.c += nSL;
-        tr = er.t;
-      }
-      const int rl = lane + count_less(tr, tl);   // left first on equal times
-      const int rr = lane + count_leq(tl, tr);
-      if (lane < remL && rl < 32) {
-        ws->ev[rl] = el;
-        ws->side[rl] = 0;
-      }
-      if (lane < remR && rr < 32) {
-        ws->ev[rr] = er;
-        ws->side[rr] = 1;
-      }
-      __syncwarp();
-      nb = min(32, min(remL, 32) + min(remR, 32));
+    if (rem > 0) {
+      const bool valid = lane < rem;
       Ev my;
-      int side = 0;
-      if (lane < nb) {
-        my = ws->ev[lane];
-        side = ws->side[lane];
-      }
-      __syncwarp();
-      const double tprev = __shfl_up_sync(FULL, lane < nb ? my.t : INF, 1);
-      const bool valid = lane < nb;
-      // exact time ties are outside general position: the reference's strict
-      // `t > oldt` rule then skips events; leave those inputs to the exact path
+      my.t = INF;
+      if (valid) my = seq[ptr + lane];
+      const double tprev = __shfl_up_sync(FULL, my.t, 1);
+      // exact ties break the reference's strict `t > oldt` rule: exact path
       if (valid && ((lane > 0 && my.t == tprev) || my.t == tb || my.t <= tcur)) errc = E_FASTPATH;
       const bool touches = valid && (my.a == u || my.a == v || my.c == u || my.c == v);
       const bool stop = !valid || touches || my.t > tb;
       const unsigned sb = __ballot_sync(FULL, stop);
-      f = sb ? __ffs(sb) - 1 : 32;
-      // retire [0, f) in parallel
+      const int f = sb ? __ffs(sb) - 1 : 32;
       const bool pre = lane < f;
-      const bool surv = pre && (side == 0 ? my.b < u : my.b > v);
+      const bool isL = (my.kind & 2) == 0;
+      const int kind = my.kind & 1;
+      const bool surv = pre && (isL ? my.b < u : my.b > v);
       const unsigned vs = __ballot_sync(FULL, surv);
       if (surv) {
         const int pos = k + __popc(vs & ltmask);
         if (pos >= capRef - 1) {
           errc = H3D_E_OVERFLOW;
-        } else if (pos >= capO) {
-          errc = E_FASTPATH;
         } else {
-          out[pos] = my;
+          Ev o = my;
+          o.kind = kind;
+          out[pos] = o;
           first_event(first, my.b, pos);
         }
       }
@@ -492,40 +477,36 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int
       const int key2 = pre ? my.c : (int)(0x80000000u + lane);
       const unsigned m1 = __match_any_sync(FULL, key1);
       const unsigned m2 = __match_any_sync(FULL, key2);
-      if (pre && (31 - __clz(m1)) == lane) R[my.a].next = (my.kind == EV_INS) ? my.b : my.c;
-      if (pre && (31 - __clz(m2)) == lane) R[my.c].prev = (my.kind == EV_INS) ? my.b : my.a;
+      if (pre && (31 - __clz(m1)) == lane) R[my.a].next = (kind == EV_INS) ? my.b : my.c;
+      if (pre && (31 - __clz(m2)) == lane) R[my.c].prev = (kind == EV_INS) ? my.b : my.a;
       if (f > 0) tcur = __shfl_sync(FULL, my.t, f - 1);
-      const int nl = __popc(__ballot_sync(FULL, pre && side == 0));
-      i += nl;
-      j += f - nl;
-      // what comes next: a foot-touching child event before the bridge event?
-      if (f < nb) {
+      ptr += f;
+      if (f < 32 && f < rem) {
         const double tf = __shfl_sync(FULL, my.t, f);
         child_next = tf < tb;
-        if (child_next) {
+        if (child_next) {  // a foot-touching child event: process it alone
           const int a = __shfl_sync(FULL, my.a, f), b = __shfl_sync(FULL, my.b, f);
           const int c = __shfl_sync(FULL, my.c, f), kd = __shfl_sync(FULL, my.kind, f);
-          const int sd = __shfl_sync(FULL, side, f);
+          const bool sL = (kd & 2) == 0;
+          const bool sv = sL ? b < u : b > v;
           __syncwarp();
           if (lane == 0) {
             const int p = R[b].prev, q = R[b].next;
             if (p != a || q != c || p == NIL || q == NIL) {
               errc = E_FASTPATH;
             } else {
-              const int kind = (R[p].next == b) ? EV_DEL : EV_INS;
-              if (kind != kd) errc = E_FASTPATH;
-              if (sd == 0 ? b < u : b > v) {
+              const int kind1 = (R[p].next == b) ? EV_DEL : EV_INS;
+              if (kind1 != (kd & 1)) errc = E_FASTPATH;
+              if (sv) {
                 if (k >= capRef - 1) {
                   errc = H3D_E_OVERFLOW;
-                } else if (k >= capO) {
-                  errc = E_FASTPATH;
                 } else {
                   Ev o;
                   o.t = tf;
                   o.a = a;
                   o.b = b;
                   o.c = c;
-                  o.kind = kind;
+                  o.kind = kind1;
                   out[k] = o;
                   first_event(first, b, k);
                 }
@@ -533,26 +514,22 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int
               act_rec(R, b);
             }
           }
-          if (sd == 0 ? b < u : b > v) ++k;
-          if (sd == 0)
-            ++i;
-          else
-            ++j;
+          if (sv) ++k;
+          ++ptr;
           tcur = tf;
           __syncwarp();
           cands();
         }
       }
+      errc = __reduce_min_sync(FULL, errc);
+      if (errc < 0) return errc;
+      if (child_next) continue;
+      if (f == 32 && ptr < kin) continue;  // a full window retired: keep going
+      if (wb < 0) continue;                // no bridge event left: drain the logs
+    } else if (wb < 0) {
+      break;  // nothing left
     }
-    errc = __reduce_min_sync(FULL, errc);
-    if (errc < 0) return errc;
-    if (child_next || f == nb && nb > 0 && (remL + remR > nb || tb == INF)) continue;
-    if (f == nb && remL + remR > nb) continue;
-    // the bridge event comes next (or nothing is left)
-    if (wb < 0) {
-      if (remL + remR - f == 0) break;
-      continue;
-    }
+    // the bridge event comes next
     if (lane == 0) {
       int a, b, c, kind;
       if (wb == 2) {
@@ -566,8 +543,6 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int
       }
       if (k >= capRef - 1) {
         errc = H3D_E_OVERFLOW;
-      } else if (k >= capO) {
-        errc = E_FASTPATH;
       } else {
         Ev o;
         o.t = tb;
@@ -597,10 +572,10 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *__restrict__ evL, int
 // their -inf links (u0 -> v0 stitched), the others get the neighbours of
 // their first event (an insertion: a point off the -inf chain enters the
 // hull once).  These are exactly the links the reference's rewind leaves on
-// every kept point.
+// every kept point.  evo (the merged events, local ids) is out.ev + 2L.
 __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R, Ev *evo,
                                  int *first, long long L, long long M, int nSL, int nS, int k,
-                                 int u0, int v0, long long gidx, bool in_place, long long *err) {
+                                 int u0, int v0, long long gidx, long long *err) {
   const int lane = threadIdx.x & 31;
   bool bad = false;
   // A: final links (local ids) into R, keep flag into first
@@ -636,14 +611,14 @@ __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R
     cnt += __popc(bal);
   }
   __syncwarp();
-  // C: events (in place when evo aliases out.ev)
+  // C: events, in place
   for (int e = lane; e < k; e += 32) {
     Ev o = evo[e];
     o.a = first[o.a];
     o.b = first[o.b];
     o.c = first[o.c];
     bad |= (o.a < 0) | (o.b < 0) | (o.c < 0);
-    out.ev[2 * L + e] = o;
+    evo[e] = o;
   }
   // D: links remapped in place
   for (int p = lane; p < nS; p += 32) {
@@ -679,24 +654,30 @@ __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R
     }
     __syncwarp();
   }
-  (void)in_place;
   if (__any_sync(FULL, bad) && lane == 0) raise_err(err, E_FASTPATH);
   if (lane == 0) out.hdr[gidx] = make_int2(cnt, k);
 }
 
-__device__ __forceinline__ long long warp_job_bytes(int nS) {
-  return align8(32ll * nS + 24ll * 2 * nS + 4ll * nS);
+// shared bytes of one warp job: records, first table, merged child events
+__device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
+  return align8(32ll * nS + 4ll * nS) + 24ll * kin;
 }
 
+// One warp per merge job (levels with few, large jobs).  A job's records,
+// first table and time-merged child events are staged in the CTA's shared
+// pool when they fit (warps whose jobs do not fit wait a round), else they
+// live in HBM scratch inside the job's own output slots (records at
+// out.rec[L..], first table in out.gid[L..]) with the merged child events
+// in the pass's HBM scratch (PassWS::seq).
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, int level,
-                                                          long long *err, int pool) {
+                                                          long long *err, int pool,
+                                                          Ev *gseq0, Ev *gseq1) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
+  Ev *gseq = blockIdx.y ? gseq1 : gseq0;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ WarpScratch scratch[WARPS];
   __shared__ long long s_need[WARPS];
-  __shared__ int s_done[WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long size = 1ll << level, half = size >> 1;
   const long long jobs = (n + size - 1) >> level;
@@ -724,17 +705,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, 
       if (lane == 0) out.hdr[j] = hl;
     }
   }
-  const int nS = nSL + nSR;
-  const long long need = merge ? warp_job_bytes(nS) : 0;
+  const int nS = nSL + nSR, kin = kL + kR;
+  const long long need = merge ? warp_job_bytes(nS, kin) : 0;
   const bool global_mode = merge && need > pool;
   bool pending = merge && !global_mode;
-  if (lane == 0) s_done[warp] = 0;
-  if (global_mode) {
-    // in place in HBM: records at out.rec[L..L+nS), merged events at
-    // out.ev[2L..2L+2nS), first-event table in out.gid[L..L+nS)
-    Rec *Rr = out.rec + L;
-    Ev *evo = out.ev + 2 * L;
-    int *first = out.gid + L;
+  auto run_job = [&](Rec *Rr, int *first, Ev *seq) {
     for (int p = lane; p < nS; p += 32) {
       Rec r = (p < nSL) ? in.rec[L + p] : in.rec[M + (p - nSL)];
       if (p >= nSL) {
@@ -743,7 +718,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, 
       }
       Rr[p] = r;
     }
-    __syncwarp();
+    merge_logs_warp(in.ev + 2 * L, kL, in.ev + 2 * M, kR, nSL, seq);
     for (int p = lane; p < nS; p += 32) {
       const int pr = Rr[p].prev;
       const bool chain = (p == 0 || p == nSL) || (pr != NIL && Rr[pr].next == p);
@@ -751,61 +726,41 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, 
     }
     __syncwarp();
     int u0, v0;
-    const long long k = merge_warp(Rr, nSL, in.ev + 2 * L, kL, in.ev + 2 * M, kR, evo, 2 * nS,
-                                   first, 2 * (R_ - L), R_ - L, &scratch[warp], &u0, &v0);
+    Ev *evo = out.ev + 2 * L;
+    const long long k = merge_warp(Rr, nSL, seq, kin, evo, first, 2 * (R_ - L), R_ - L, &u0, &v0);
+    __syncwarp();
     if (k < 0) {
       if (lane == 0) raise_err(err, k);
     } else {
       rebuild_writeout(in, out, Rr, evo, first, L, M, nSL, nS, static_cast<int>(k), u0, v0, j,
-                       true, err);
+                       err);
     }
+  };
+  if (global_mode) {
+    // in HBM: records at out.rec[L..L+nS) (nS <= R-L), first table in
+    // out.gid[L..), merged child events in the level scratch at gseq[2L..)
+    run_job(out.rec + L, out.gid + L, gseq + 2 * L);
   }
   // shared-memory pool: warps whose jobs fit run together, the rest wait
   for (;;) {
     if (lane == 0) s_need[warp] = pending ? need : 0;
     __syncthreads();
-    long long off = 0, total = 0;
+    long long off = 0;
     bool any = false;
     for (int w = 0; w < WARPS; ++w) {
       const long long nw = s_need[w];
       if (nw > 0) any = true;
       if (w < warp) off += nw;
-      total += nw;
     }
-    (void)total;
     __syncthreads();
     if (!any) break;
     // a warp runs this round if its prefix fits (the first pending one always does)
-    const bool run = pending && off + need <= pool;
-    if (run) {
+    if (pending && off + need <= pool) {
       unsigned char *mine = smem + off;
       Rec *Rr = reinterpret_cast<Rec *>(mine);
-      Ev *evo = reinterpret_cast<Ev *>(mine + 32ll * nS);
-      int *first = reinterpret_cast<int *>(evo + 2 * nS);
-      for (int p = lane; p < nS; p += 32) {
-        Rec r = (p < nSL) ? in.rec[L + p] : in.rec[M + (p - nSL)];
-        if (p >= nSL) {
-          if (r.prev != NIL) r.prev += nSL;
-          if (r.next != NIL) r.next += nSL;
-        }
-        Rr[p] = r;
-      }
-      __syncwarp();
-      for (int p = lane; p < nS; p += 32) {
-        const int pr = Rr[p].prev;
-        const bool chain = (p == 0 || p == nSL) || (pr != NIL && Rr[pr].next == p);
-        first[p] = (chain ? FIRST_FLAG : 0) | FIRST_NONE;
-      }
-      __syncwarp();
-      int u0, v0;
-      const long long k = merge_warp(Rr, nSL, in.ev + 2 * L, kL, in.ev + 2 * M, kR, evo, 2 * nS,
-                                     first, 2 * (R_ - L), R_ - L, &scratch[warp], &u0, &v0);
-      if (k < 0) {
-        if (lane == 0) raise_err(err, k);
-      } else {
-        rebuild_writeout(in, out, Rr, evo, first, L, M, nSL, nS, static_cast<int>(k), u0, v0,
-                         j, false, err);
-      }
+      int *first = reinterpret_cast<int *>(Rr + nS);
+      Ev *seq = reinterpret_cast<Ev *>(mine + align8(36ll * nS));
+      run_job(Rr, first, seq);
       pending = false;
     }
     __syncthreads();
@@ -847,6 +802,7 @@ constexpr long long kTpjMinJobs = 16384;
 
 struct PassWS {
   GroupBuf A, B;
+  Ev *seq;  // merged child events of HBM-resident warp jobs (2n)
 };
 
 bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
@@ -856,7 +812,8 @@ bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
     g->gid = ar.take<int>(n);
     g->ev = ar.take<Ev>(2 * n);
   }
-  return ar.base == nullptr || w.B.ev != nullptr;
+  w.seq = ar.take<Ev>(2 * n);
+  return ar.base == nullptr || w.seq != nullptr;
 }
 
 bool g_attr_done = false;
@@ -933,8 +890,8 @@ int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower, voi
         k_fast_tpj<128><<<grid, 128, pool, s>>>(P, n, lv, err, static_cast<int>(pool));
       h3d_prof_end(e0, lv + 1000, 2, s);
     } else {
-      k_fast_warp<kWarps><<<dim3(h3d_grid(jobs, kWarps), 2), kWarps * 32, kPool, s>>>(P, n, lv,
-                                                                                   err, kPool);
+      k_fast_warp<kWarps><<<dim3(h3d_grid(jobs, kWarps), 2), kWarps * 32, kPool, s>>>(
+          P, n, lv, err, kPool, w0.seq, w1.seq);
       h3d_prof_end(e0, lv, 2, s);
     }
     P = Pass2{P.out0, P.out1, P.in0, P.in1};
