@@ -171,6 +171,25 @@ int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower,
                         void *ws_upper, size_t workspace_bytes, int64_t *err_dev,
                         int32_t verify, int64_t *final_out, void *stream);
 
+/* Level range form (multi-GPU x-slabs, pkg/src/hull3d/parallel.py:96-111
+ * restricted to the jobs inside one slab): runs levels lv_lo..lv_hi only for
+ * the jobs whose point range starts in [p0, p1); lv_lo == 1 also initialises
+ * the level-0 groups of [p0, p1).  Level l reads buffer (l-1)&1 and writes
+ * buffer l&1 of each workspace.  Returns lv_hi&1 or a negative code. */
+int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0,
+                              int64_t p1, int32_t lv_lo, int32_t lv_hi,
+                              void *ws_lower, void *ws_upper,
+                              size_t workspace_bytes, int64_t *err_dev,
+                              int32_t verify, void *stream);
+
+/* Byte offsets of the compact-group arrays inside one pass workspace:
+ * A.hdr, A.rec, A.gid, A.ev, B.hdr, B.rec, B.gid, B.ev, seq (host int64[9]).
+ * hdr = int2 (nS, k) per group; rec = 32-byte records (x, y, z f64, prev,
+ * next i32 group-local); gid = i32; ev = 24-byte events (t f64, a, b, c,
+ * kind i32); a group [L, R) at level l has header l, records at [L, L+nS)
+ * and events at [2L, 2L+k).  Used to ship groups between GPUs. */
+int64_t h3d_fast_layout(int64_t n, int64_t *offsets);
+
 /* Facets of both passes from their final groups (extract_faces,
  * _ckernels.pyx:324-349): faces (cap,3) i32 in sorted indices, lower block
  * then upper block; counts_dev (device int64[2]) = (lower, upper) counts.

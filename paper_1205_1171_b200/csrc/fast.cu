@@ -52,10 +52,10 @@ __host__ __device__ __forceinline__ long long align8(long long b) { return (b + 
 
 // --------------------------------------------------------- thread per job
 // level 0: every point is a one-point group with an empty log
-__global__ void k_fast_init(const double *__restrict__ pts, long long n, Pass2 P) {
+__global__ void k_fast_init(const double *__restrict__ pts, long long p0, long long p1, Pass2 P) {
   const GroupBuf g = blockIdx.y ? P.in1 : P.in0;
   const double zs = blockIdx.y ? -1.0 : 1.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+  for (long long i = p0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p1;
        i += (long long)gridDim.x * blockDim.x) {
     Rec r;
     r.x = pts[3 * i];
@@ -206,6 +206,7 @@ constexpr int TPJ_REC_BYTES = 34;  // 32-byte record + 2-byte info per point
 // fit wait for the next round).
 template <int TPJ_TPB>
 __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(Pass2 P, long long n, int level,
+                                                     long long j0, long long j1,
                                                      long long *err, int pool) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
@@ -213,8 +214,8 @@ __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(Pass2 P, long long n, int 
   typedef cub::BlockScan<int, TPJ_TPB> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
   const long long size = 1ll << level, half = size >> 1;
-  const long long jobs = (n + size - 1) >> level;
-  const long long j = blockIdx.x * (long long)TPJ_TPB + threadIdx.x;
+  const long long jobs = j1;
+  const long long j = j0 + blockIdx.x * (long long)TPJ_TPB + threadIdx.x;
   const long long L = j << level, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
   const bool valid = j < jobs;
@@ -671,6 +672,7 @@ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
 // in the pass's HBM scratch (PassWS::seq).
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, int level,
+                                                          long long j0, long long j1,
                                                           long long *err, int pool,
                                                           Ev *gseq0, Ev *gseq1) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
@@ -680,8 +682,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, 
   __shared__ long long s_need[WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long size = 1ll << level, half = size >> 1;
-  const long long jobs = (n + size - 1) >> level;
-  const long long j = blockIdx.x * (long long)WARPS + warp;
+  const long long jobs = j1;
+  const long long j = j0 + blockIdx.x * (long long)WARPS + warp;
   const long long L = j << level, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
   const bool valid = j < jobs;
@@ -797,8 +799,8 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kPool = 64 * 1024;
 constexpr int kTpjPool = 96 * 1024;
-constexpr int kTpjMaxLevel = 9;
-constexpr long long kTpjMinJobs = 16384;
+int kTpjMaxLevel = 9;  // H3D_TPJ_MAX_LEVEL
+long long kTpjMinJobs = 16384;  // H3D_TPJ_MIN_JOBS (per pass)
 
 struct PassWS {
   GroupBuf A, B;
@@ -826,6 +828,17 @@ long long g_tpj_pool = 24 * 1024;
 
 extern "C" {
 
+int64_t h3d_fast_layout(int64_t n, int64_t *offsets) {
+  // byte offsets of A.hdr, A.rec, A.gid, A.ev, B.hdr, B.rec, B.gid, B.ev, seq
+  char *base = reinterpret_cast<char *>(size_t(1) << 40);
+  h3d_arena ar(base, ~size_t(0) >> 4);
+  PassWS w;
+  if (!carve_pass(ar, n, w)) return H3D_E_ARG;
+  const void *p[9] = {w.A.hdr, w.A.rec, w.A.gid, w.A.ev, w.B.hdr, w.B.rec, w.B.gid, w.B.ev, w.seq};
+  for (int i = 0; i < 9; ++i) offsets[i] = static_cast<const char *>(p[i]) - base;
+  return 0;
+}
+
 size_t h3d_fast_pass_workspace_bytes(int64_t n) {  // per pass
   if (n < 1) n = 1;
   h3d_arena ar(nullptr, 0);
@@ -834,12 +847,13 @@ size_t h3d_fast_pass_workspace_bytes(int64_t n) {  // per pass
   return ar.used + 4096;
 }
 
-int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower, void *ws_upper,
-                        size_t workspace_bytes, int64_t *err_dev, int32_t verify,
-                        int64_t *final_out, void *stream) {
+int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, int64_t p1,
+                              int32_t lv_lo, int32_t lv_hi, void *ws_lower, void *ws_upper,
+                              size_t workspace_bytes, int64_t *err_dev, int32_t verify,
+                              void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   (void)verify;
-  if (n < 2 || n > (1ll << 30)) return H3D_E_ARG;
+  if (n < 2 || n > (1ll << 30) || p0 < 0 || p1 > n || p0 >= p1 || lv_lo < 1) return H3D_E_ARG;
   h3d_arena a0(ws_lower, workspace_bytes), a1(ws_upper, workspace_bytes);
   PassWS w0, w1;
   if (!carve_pass(a0, n, w0) || !carve_pass(a1, n, w1)) return H3D_E_ARG;
@@ -856,6 +870,8 @@ int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower, voi
     if (const char *e = getenv("H3D_TPJ_TPB")) g_tpj_tpb = atoi(e);
     if (const char *e = getenv("H3D_TPJ_FILL")) g_tpj_fill = atof(e);
     if (const char *e = getenv("H3D_TPJ_POOL_KB")) g_tpj_pool = atoll(e) * 1024;
+    if (const char *e = getenv("H3D_TPJ_MAX_LEVEL")) kTpjMaxLevel = atoi(e);
+    if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinJobs = atoll(e);
     if (g_tpj_tpb != 32 && g_tpj_tpb != 64) g_tpj_tpb = 128;
     if (g_tpj_pool > kTpjPool) g_tpj_pool = kTpjPool;
     g_attr_done = true;
@@ -863,17 +879,24 @@ int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower, voi
   long long *err = reinterpret_cast<long long *>(err_dev);
   int levels = 0;
   while ((1ll << levels) < n) ++levels;
-  Pass2 P{w0.A, w1.A, w0.B, w1.B};
-  h3d_count_launches(1);
-  const unsigned gi = h3d_grid(n, 256) > 4096 ? 4096 : h3d_grid(n, 256);
-  k_fast_init<<<dim3(gi, 2), 256, 0, s>>>(sorted_pts, n, P);
-  int which = 0;
-  for (int lv = 1; lv <= levels; ++lv) {
-    const long long jobs = (n + (1ll << lv) - 1) >> lv;
+  if (lv_hi > levels) lv_hi = levels;
+  // level l reads buffer (l-1)&1 and writes buffer l&1 (A = 0, B = 1)
+  Pass2 P = (lv_lo & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
+  if (lv_lo == 1) {
+    h3d_count_launches(1);
+    const long long np = p1 - p0;
+    const unsigned gi = h3d_grid(np, 256) > 4096 ? 4096 : h3d_grid(np, 256);
+    k_fast_init<<<dim3(gi, 2), 256, 0, s>>>(sorted_pts, p0, p1, P);
+  }
+  for (int lv = lv_lo; lv <= lv_hi; ++lv) {
+    // the jobs of this level inside the point range [p0, p1)
+    const long long j0 = p0 >> lv;
+    const long long j1 = (p1 + (1ll << lv) - 1) >> lv;
+    const long long jobs = j1 - j0;
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
     h3d_count_launches(1);
     // thread per job while jobs are plentiful and small, warp per job above
-    if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel) {
+    if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel && ((long long)TPJ_REC_BYTES << lv) <= kTpjPool) {
       // threads per CTA and shared pool per level: the pool holds the CTA's
       // jobs at an assumed fill of nS <= 2^lv * fill (rounds absorb overflow)
       const int tpb = g_tpj_tpb;
@@ -883,23 +906,33 @@ int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower, voi
       if (pool < 2048) pool = 2048;
       const dim3 grid(h3d_grid(jobs, tpb), 2);
       if (tpb == 32)
-        k_fast_tpj<32><<<grid, 32, pool, s>>>(P, n, lv, err, static_cast<int>(pool));
+        k_fast_tpj<32><<<grid, 32, pool, s>>>(P, n, lv, j0, j1, err, static_cast<int>(pool));
       else if (tpb == 64)
-        k_fast_tpj<64><<<grid, 64, pool, s>>>(P, n, lv, err, static_cast<int>(pool));
+        k_fast_tpj<64><<<grid, 64, pool, s>>>(P, n, lv, j0, j1, err, static_cast<int>(pool));
       else
-        k_fast_tpj<128><<<grid, 128, pool, s>>>(P, n, lv, err, static_cast<int>(pool));
+        k_fast_tpj<128><<<grid, 128, pool, s>>>(P, n, lv, j0, j1, err, static_cast<int>(pool));
       h3d_prof_end(e0, lv + 1000, 2, s);
     } else {
       k_fast_warp<kWarps><<<dim3(h3d_grid(jobs, kWarps), 2), kWarps * 32, kPool, s>>>(
-          P, n, lv, err, kPool, w0.seq, w1.seq);
+          P, n, lv, j0, j1, err, kPool, w0.seq, w1.seq);
       h3d_prof_end(e0, lv, 2, s);
     }
     P = Pass2{P.out0, P.out1, P.in0, P.in1};
-    which ^= 1;
   }
   if (h3d_check(cudaGetLastError())) return H3D_E_CUDA;
-  final_out[0] = which;
-  final_out[1] = which;
+  return lv_hi & 1;  // buffer holding the last level's groups
+}
+
+int64_t h3d_fast_passes(const double *sorted_pts, int64_t n, void *ws_lower, void *ws_upper,
+                        size_t workspace_bytes, int64_t *err_dev, int32_t verify,
+                        int64_t *final_out, void *stream) {
+  int levels = 0;
+  while ((1ll << levels) < n) ++levels;
+  const int64_t r = h3d_fast_passes_range(sorted_pts, n, 0, n, 1, levels, ws_lower, ws_upper,
+                                          workspace_bytes, err_dev, verify, stream);
+  if (r < 0) return r;
+  final_out[0] = r;
+  final_out[1] = r;
   return 0;
 }
 

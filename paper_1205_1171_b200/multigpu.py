@@ -1,0 +1,290 @@
+"""Multi-GPU x-slab sharding of the hull.
+
+One process per GPU (torch.distributed, NCCL over NVLink; gloo in the CPU
+tests).  After the global sort, rank r owns the sorted ranks
+[r*S, (r+1)*S) with S = 2^(L - log2 G) and L = ceil(log2 n): exactly the
+level-(L - log2 G) groups of the single-GPU merge tree, so every log is the
+one `plan_level` (pkg/src/hull3d/parallel.py:49-65) would produce.
+
+* Levels 1 .. L - log2 G run on every rank's own slab with no communication
+  (`h3d_fast_passes_range`).
+* Each of the last log2 G levels pairs slabs: at level l a group spans
+  2^(l-s) slabs; the owner of its right half sends its compact group (header,
+  records, ids, events of both passes -- everything the merge reads) to the
+  owner of the left half, which runs that one merge job.  A left half with no
+  right half (ragged n) is a carry and needs no message.
+* Rank 0 ends with the final groups and runs facet extraction and the
+  orientation / remap epilogue.
+
+Data path: only the final log2 G levels exchange anything, point-to-point,
+and the messages are the compact groups (a few KB for cube/ball, ~24 MB for
+a sphere-like top level).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class SlabPlan:
+    n: int
+    world: int
+
+    @property
+    def levels(self) -> int:
+        return (self.n - 1).bit_length()
+
+    @property
+    def G(self) -> int:
+        """Ranks that own slabs: the largest power of two <= world whose slabs
+        still hold at least two points."""
+        g = 1
+        while g * 2 <= self.world and (self.n + g * 2 - 1) // (g * 2) >= 2 and g * 2 <= (1 << max(self.levels - 1, 0)):
+            g *= 2
+        return g
+
+    @property
+    def slab_level(self) -> int:
+        return self.levels - (self.G.bit_length() - 1)
+
+    @property
+    def S(self) -> int:
+        return 1 << self.slab_level
+
+    def slab(self, rank: int):
+        """Point range [p0, p1) of a rank's slab, or None."""
+        if rank >= self.G:
+            return None
+        p0 = rank * self.S
+        if p0 >= self.n:
+            return None
+        return p0, min(self.n, p0 + self.S)
+
+    def role(self, level: int, rank: int):
+        """What a rank does at a cross level: ("merge", partner),
+        ("send", partner), ("carry", None) or ("idle", None)."""
+        s = self.slab_level
+        if level <= s or rank >= self.G:
+            return ("idle", None)
+        span = 1 << (level - s)
+        half = span >> 1
+        if rank % span == 0:
+            if rank * self.S >= self.n:
+                return ("idle", None)
+            right = rank + half
+            if right * self.S < self.n:
+                return ("merge", right)
+            return ("carry", None)
+        if rank % span == half and rank * self.S < self.n:
+            return ("send", rank - half)
+        return ("idle", None)
+
+
+class GroupLayout:
+    """Views of one pass workspace's compact-group arrays (see
+    h3d_fast_layout in include/hull3d_b200.h)."""
+
+    REC = 32
+    EV = 24
+
+    def __init__(self, ws: torch.Tensor, n: int):
+        offs = (ctypes.c_int64 * 9)()
+        _lib.load().h3d_fast_layout(n, ctypes.addressof(offs))
+        self.ws = ws
+        self.n = n
+        self.off = list(offs)
+
+    def _arr(self, buf: int, which: int) -> int:
+        return self.off[4 * buf + which]
+
+    def hdr_view(self, buf: int, g: int) -> torch.Tensor:
+        o = self._arr(buf, 0) + 8 * g
+        return self.ws[o:o + 8]
+
+    def rec_view(self, buf: int, L: int, nS: int) -> torch.Tensor:
+        o = self._arr(buf, 1) + self.REC * L
+        return self.ws[o:o + self.REC * nS]
+
+    def gid_view(self, buf: int, L: int, nS: int) -> torch.Tensor:
+        o = self._arr(buf, 2) + 4 * L
+        return self.ws[o:o + 4 * nS]
+
+    def ev_view(self, buf: int, L: int, k: int) -> torch.Tensor:
+        o = self._arr(buf, 3) + self.EV * 2 * L
+        return self.ws[o:o + self.EV * k]
+
+
+def group_header(layouts, buf: int, g: int) -> torch.Tensor:
+    """(nS, k) of group g in both passes as one int32 tensor [4]."""
+    return torch.cat([lay.hdr_view(buf, g) for lay in layouts]).view(torch.int32).clone()
+
+
+def _p2p_via_host() -> bool:
+    """gloo cannot move CUDA tensors point-to-point: stage them through host
+    memory (the single-GPU multi-process tests run gloo on one device)."""
+    import torch.distributed as dist
+
+    return dist.get_backend() == "gloo"
+
+
+def _send(t: torch.Tensor, dst: int) -> None:
+    import torch.distributed as dist
+
+    dist.send(t.cpu() if (t.is_cuda and _p2p_via_host()) else t, dst)
+
+
+def _recv(t: torch.Tensor, src: int) -> None:
+    import torch.distributed as dist
+
+    if t.is_cuda and _p2p_via_host():
+        tmp = torch.empty(t.shape, dtype=t.dtype)
+        dist.recv(tmp, src)
+        t.copy_(tmp)
+    else:
+        dist.recv(t, src)
+
+
+def send_group(layouts, buf: int, level: int, g: int, dst: int) -> None:
+    """Ship group g of `level` (in buffer `buf`) of both passes to rank dst."""
+    hdr = group_header(layouts, buf, g)
+    _send(hdr, dst)
+    L = g << level
+    h = hdr.cpu().tolist()
+    for p, lay in enumerate(layouts):
+        nS, k = h[2 * p], h[2 * p + 1]
+        for view in (lay.rec_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
+            if view.numel():
+                _send(view.contiguous(), dst)
+
+
+def recv_group(layouts, buf: int, level: int, g: int, src: int) -> None:
+    """Receive group g of `level` of both passes from rank src into the same
+    slots of this rank's buffer `buf`."""
+    dev = layouts[0].ws.device
+    hdr = torch.empty(4, dtype=torch.int32, device=dev)
+    _recv(hdr, src)
+    L = g << level
+    h = hdr.cpu().tolist()
+    for p, lay in enumerate(layouts):
+        nS, k = h[2 * p], h[2 * p + 1]
+        lay.hdr_view(buf, g).copy_(hdr[2 * p:2 * p + 2].view(torch.uint8))
+        for view in (lay.rec_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
+            if view.numel():
+                tmp = torch.empty_like(view)
+                _recv(tmp, src)
+                view.copy_(tmp)
+
+
+def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
+    """Both passes of the hull over x-slabs.  Every rank passes the same
+    input (caller order, on its own device).  Returns on rank 0 the same
+    tuple as fast.run_both plus (sorted points, order, perturbed); None on the
+    other ranks; None on rank 0 too when the exact engine must take over."""
+    import torch.distributed as dist
+
+    from .api import presort
+    from .engine import stream_ptr
+    from .fast import _WS
+
+    L = _lib.load()
+    n = pts_dev.shape[0]
+    dev = pts_dev.device
+    s = stream_ptr(dev)
+    sorted_pts, order, perturbed = presort(pts_dev)
+    plan = SlabPlan(n, world)
+    wsb = int(L.h3d_fast_pass_workspace_bytes(n))
+    ws = [_WS.get(dev, 0, wsb), _WS.get(dev, 1, wsb)]
+    lays = [GroupLayout(ws[0], n), GroupLayout(ws[1], n)]
+    state = torch.zeros(4, dtype=torch.int64, device=dev)
+    err = state[0:1]
+    sl = plan.slab(rank)
+    if sl is not None:
+        r = L.h3d_fast_passes_range(sorted_pts.data_ptr(), n, sl[0], sl[1], 1, plan.slab_level,
+                                    ws[0].data_ptr(), ws[1].data_ptr(), wsb, err.data_ptr(), 0, s)
+        if r < 0:
+            err.fill_(int(r))
+    for lv in range(plan.slab_level + 1, plan.levels + 1):
+        role, peer = plan.role(lv, rank)
+        prev_buf = (lv - 1) & 1
+        if role == "send":
+            send_group(lays, prev_buf, lv - 1, (rank * plan.S) >> (lv - 1), peer)
+        elif role in ("merge", "carry"):
+            if role == "merge":
+                recv_group(lays, prev_buf, lv - 1, (peer * plan.S) >> (lv - 1), peer)
+            p0 = rank * plan.S
+            p1 = min(n, p0 + (1 << lv))
+            r = L.h3d_fast_passes_range(sorted_pts.data_ptr(), n, p0, p1, lv, lv,
+                                        ws[0].data_ptr(), ws[1].data_ptr(), wsb, err.data_ptr(),
+                                        0, s)
+            if r < 0:
+                err.fill_(int(r))
+    # any error anywhere sends the whole hull to the exact engine on rank 0
+    flag = (err != 0).to(torch.int64)
+    if _p2p_via_host():
+        flag = flag.cpu()
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    if rank != 0:
+        return None
+    if int(flag.item()) != 0:
+        return None
+    final = plan.levels & 1
+    cap = max(2 * n, 8)
+    faces = torch.empty((cap, 3), dtype=torch.int32, device=dev)
+    counts = state[1:3]
+    L.h3d_fast_extract(ws[0].data_ptr(), ws[1].data_ptr(), n, final, final, faces.data_ptr(), cap,
+                       counts.data_ptr(), err.data_ptr(), s)
+    h = state.cpu()
+    if int(h[0]) != 0:
+        return None
+    k_lo, k_up = int(h[1]), int(h[2])
+    return faces[: k_lo + k_up], k_lo, k_up, sorted_pts, order, perturbed
+
+
+def convex_hull_3d_distributed(points, device=None, return_device: bool = False):
+    """Distributed drop-in: every rank calls it with the same points; rank 0
+    gets the HullResult (identical to the single-GPU one), the others None."""
+    import time
+
+    import numpy as np
+    import torch.distributed as dist
+
+    from .api import HullResult, HullStats, _to_device, convex_hull_3d, orient_remap
+    from .engine import level_count
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    pts = _to_device(points, dev)
+    n = pts.shape[0]
+    if world == 1 or n <= 3 or SlabPlan(n, world).G == 1:
+        return convex_hull_3d(pts, return_device=return_device) if rank == 0 else None
+    res = hull_distributed(pts, rank, world)
+    if rank != 0:
+        return None
+    if res is None:  # exact engine, single GPU, reference semantics
+        return convex_hull_3d(pts, _exact_backend(dev), return_device=return_device)
+    raw, k_lo, k_up, sorted_pts, order, perturbed = res
+    verts, faces = orient_remap(sorted_pts, order, raw)
+    total_ms = (time.perf_counter() - t0) * 1e3
+    stats = HullStats(n=n, levels=level_count(n), lower_events=k_lo, upper_events=k_up,
+                      sort_ms=0.0, lower_ms=0.0, upper_ms=0.0, total_ms=total_ms,
+                      perturbed=perturbed, solver="parallel", workers=world)
+    if not return_device:
+        verts, faces = verts.cpu().numpy(), faces.cpu().numpy()
+    return HullResult(vertices=verts, faces=faces, stats=stats)
+
+
+def _exact_backend(dev):
+    from .api import CudaBackend
+
+    return CudaBackend(dev, engine="exact")
+
+
+__all__ = ["SlabPlan", "GroupLayout", "send_group", "recv_group", "hull_distributed",
+           "convex_hull_3d_distributed"]
