@@ -198,7 +198,29 @@ __device__ long long merge_tpj(TpjJob &J, const Ev *__restrict__ evL, int kL,
   return err ? err : k;
 }
 
-constexpr int TPJ_REC_BYTES = 34;  // 32-byte record + 2-byte info per point
+constexpr int TPJ_REC_BYTES = 34;
+
+// max over CTAs (chunks of tpb consecutive jobs) of the shared bytes the
+// chunk's merges need -- sizes the thread-per-job pool so no CTA needs a
+// second round (a round serialises behind the slowest sweep)
+__global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1, int tpb,
+                           unsigned long long *out) {
+  const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
+  const long long size = 1ll << level, half = size >> 1;
+  const long long chunks = (j1 - j0 + tpb - 1) / tpb;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < chunks;
+       c += (long long)gridDim.x * blockDim.x) {
+    unsigned long long tot = 0;
+    for (long long j = j0 + c * tpb; j < j0 + (c + 1) * tpb && j < j1; ++j) {
+      const long long L = j << level;
+      const long long R_ = (L + size < n) ? L + size : n;
+      if (R_ - L <= half) continue;
+      const int nS = in.hdr[2 * j].x + in.hdr[2 * j + 1].x;
+      tot += align8((long long)TPJ_REC_BYTES * nS);
+    }
+    atomicMax(out, tot);
+  }
+}  // 32-byte record + 2-byte info per point
 
 // One thread per merge job (levels with many jobs).  Each thread's slice of
 // the shared-memory pool holds its job's records and info table; slices are
@@ -798,13 +820,14 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kPool = 64 * 1024;
-constexpr int kTpjPool = 96 * 1024;
+constexpr int kTpjPool = 200 * 1024;
 int kTpjMaxLevel = 9;  // H3D_TPJ_MAX_LEVEL
 long long kTpjMinJobs = 16384;  // H3D_TPJ_MIN_JOBS (per pass)
 
 struct PassWS {
   GroupBuf A, B;
-  Ev *seq;  // merged child events of HBM-resident warp jobs (2n)
+  Ev *seq;                  // merged child events of HBM-resident warp jobs (2n)
+  unsigned long long *need; // thread-per-job pool sizing
 };
 
 bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
@@ -815,14 +838,16 @@ bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
     g->ev = ar.take<Ev>(2 * n);
   }
   w.seq = ar.take<Ev>(2 * n);
-  return ar.base == nullptr || w.seq != nullptr;
+  w.need = ar.take<unsigned long long>(4);
+  return ar.base == nullptr || w.need != nullptr;
 }
 
 bool g_attr_done = false;
 // thread-per-job tuning (H3D_TPJ_TPB, H3D_TPJ_FILL, H3D_TPJ_POOL_KB override)
 int g_tpj_tpb = 32;
 double g_tpj_fill = 0.5;
-long long g_tpj_pool = 24 * 1024;
+long long g_tpj_pool = 200 * 1024;
+int g_tpj_measure = 1;  // H3D_TPJ_MEASURE=0: size the pool by H3D_TPJ_FILL instead
 
 }  // namespace
 
@@ -871,6 +896,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     if (const char *e = getenv("H3D_TPJ_FILL")) g_tpj_fill = atof(e);
     if (const char *e = getenv("H3D_TPJ_POOL_KB")) g_tpj_pool = atoll(e) * 1024;
     if (const char *e = getenv("H3D_TPJ_MAX_LEVEL")) kTpjMaxLevel = atoi(e);
+    if (const char *e = getenv("H3D_TPJ_MEASURE")) g_tpj_measure = atoi(e);
     if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinJobs = atoll(e);
     if (g_tpj_tpb != 32 && g_tpj_tpb != 64) g_tpj_tpb = 128;
     if (g_tpj_pool > kTpjPool) g_tpj_pool = kTpjPool;
@@ -897,10 +923,24 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     h3d_count_launches(1);
     // thread per job while jobs are plentiful and small, warp per job above
     if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel && ((long long)TPJ_REC_BYTES << lv) <= kTpjPool) {
-      // threads per CTA and shared pool per level: the pool holds the CTA's
-      // jobs at an assumed fill of nS <= 2^lv * fill (rounds absorb overflow)
+      // threads per CTA and shared pool per level: the pool is the largest
+      // CTA's actual need (one small read-back per level), capped
       const int tpb = g_tpj_tpb;
-      long long pool = (long long)tpb * align8((long long)(TPJ_REC_BYTES * g_tpj_fill * (1ll << lv)));
+      long long pool;
+      if (g_tpj_measure) {
+        cudaMemsetAsync(w0.need, 0, sizeof(unsigned long long), s);
+        const long long chunks = (jobs + tpb - 1) / tpb;
+        h3d_count_launches(1);
+        k_tpj_need<<<dim3(h3d_grid(chunks, 128) > 2048 ? 2048 : h3d_grid(chunks, 128), 2), 128, 0,
+                     s>>>(P, n, lv, j0, j1, tpb, w0.need);
+        unsigned long long hneed = 0;
+        if (h3d_check(cudaMemcpyAsync(&hneed, w0.need, sizeof(hneed), cudaMemcpyDeviceToHost, s)) ||
+            h3d_check(cudaStreamSynchronize(s)))
+          return H3D_E_CUDA;
+        pool = static_cast<long long>(hneed);
+      } else {
+        pool = (long long)tpb * align8((long long)(TPJ_REC_BYTES * g_tpj_fill * (1ll << lv)));
+      }
       if (pool > g_tpj_pool) pool = g_tpj_pool;
       if (pool < (long long)TPJ_REC_BYTES << lv) pool = align8((long long)TPJ_REC_BYTES << lv);
       if (pool < 2048) pool = 2048;
