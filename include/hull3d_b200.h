@@ -155,7 +155,7 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
                          size_t workspace_bytes, void *stream);
 
 /* bytes of workspace one h3d_fast_pass needs for n points (two compact
- * group buffers: headers, 32-byte point records, ids, 24-byte events) */
+ * group buffers: headers, int2 links, ids, 24-byte events; HBM scratch) */
 size_t h3d_fast_pass_workspace_bytes(int64_t n);
 
 /* Both hull passes (build_movie, pkg/src/hull3d/parallel.py:68-112) over the
@@ -183,11 +183,12 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0,
                               int32_t verify, void *stream);
 
 /* Byte offsets of the compact-group arrays inside one pass workspace:
- * A.hdr, A.rec, A.gid, A.ev, B.hdr, B.rec, B.gid, B.ev, seq (host int64[9]).
- * hdr = int2 (nS, k) per group; rec = 32-byte records (x, y, z f64, prev,
- * next i32 group-local); gid = i32; ev = 24-byte events (t f64, a, b, c,
- * kind i32); a group [L, R) at level l has header l, records at [L, L+nS)
- * and events at [2L, 2L+k).  Used to ship groups between GPUs. */
+ * A.hdr, A.lnk, A.gid, A.ev, B.hdr, B.lnk, B.gid, B.ev, seq (host int64[9]).
+ * hdr = int2 (nS, k) per group; lnk = int2 (prev, next) group-local ids of
+ * each kept point at t = -inf; gid = i32 sorted index of each kept point
+ * (coordinates are read from sorted_pts); ev = 24-byte events (t f64, a, b,
+ * c, kind i32); a group [L, R) at level l has header l, links/ids at
+ * [L, L+nS) and events at [2L, 2L+k).  Used to ship groups between GPUs. */
 int64_t h3d_fast_layout(int64_t n, int64_t *offsets);
 
 /* Facets of both passes from their final groups (extract_faces,

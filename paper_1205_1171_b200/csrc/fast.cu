@@ -1,28 +1,31 @@
 // fast.cu -- the fused fast path: all merge levels of a pass over compact groups.
 //
-// Level scheduler (parallel.py:68-112 on the device), no host synchronisation
-// inside a pass; a device error word is read once per hull:
+// Level scheduler (parallel.py:68-112 on the device); a device error word is
+// read once per hull:
 //
-//  * k_fast_tpj    one launch per level while jobs are plentiful: one THREAD
-//                  per merge job (merge_tpj, the reference's sequential sweep
-//                  with cached candidate times), int16 links in a packed
-//                  shared-memory slice, coordinates and child events streamed
-//                  from HBM, merged events written straight back, and the
-//                  start-of-time links rebuilt from the merged -inf chain and
-//                  first events (no sequential rewind).
-//  * k_fast_warp   one launch per level above the leaf.  One WARP per merge
-//                  job (merge_warp): the kinetic sweep advances through the
+//  * k_fast_init1  level 1 (pairs of one-point groups) written directly.
+//  * k_fast_tpj    one launch per level while jobs are plentiful: one LANE per
+//                  merge job (merge_tpj2, the reference's sequential sweep with
+//                  stored child event times and the bridge neighbourhood in
+//                  registers); int16 links, gids and first-event info in a
+//                  packed shared-memory slice per job (plus coordinates when
+//                  they fit), staged and written back warp-cooperatively; the
+//                  start-of-time links are rebuilt from the merged -inf chain
+//                  and first events (no sequential rewind).
+//  * k_fast_warp   one launch per level above.  One WARP per merge job
+//                  (merge_warp): the kinetic sweep advances through the
 //                  time-merged child logs 32 events at a time -- every event
 //                  that neither touches the bridge feet nor comes after the
 //                  next bridge event is retired in parallel (survivor
 //                  emission by ballot prefix, link writes resolved
 //                  last-writer-wins with __match_any_sync) -- and only foot
-//                  events and bridge events are sequential.  The start-of-time
-//                  links of the merged group are rebuilt in parallel (merged
-//                  -inf chain + each point's first facet) instead of the
-//                  reference's sequential rewind.  Jobs are staged in a
-//                  shared-memory pool when they fit, else run in place in HBM.
+//                  events and bridge events are sequential.  Jobs are staged
+//                  in a shared-memory pool when they fit, else run in HBM.
 //  * k_fast_extract  facets of both passes straight from the final events.
+//
+// Coordinates are never copied between levels: a group stores each kept
+// point's gid and kernels read the sorted point array (z negated on the
+// upper pass).
 #include <cstdlib>
 
 #include <cub/cub.cuh>
@@ -33,10 +36,10 @@
 namespace h3d {
 
 struct GroupBuf {
-  int2 *hdr;
-  Rec *rec;
-  int *gid;
-  Ev *ev;
+  int2 *hdr;  // (nS, k) per group
+  int2 *lnk;  // start-of-time links (group-local ids) per kept point
+  int *gid;   // global sorted index per kept point
+  Ev *ev;     // events, 2 slots per point
 };
 
 // both passes of a level in one launch: blockIdx.y = 0 lower, 1 upper
@@ -49,116 +52,241 @@ constexpr int FIRST_FLAG = 1 << 30;        // "on a child's -inf chain"
 constexpr int FIRST_NONE = FIRST_FLAG - 1; // no event yet
 
 __host__ __device__ __forceinline__ long long align8(long long b) { return (b + 7) & ~7ll; }
+__host__ __device__ __forceinline__ long long align16(long long b) { return (b + 15) & ~15ll; }
 
-// --------------------------------------------------------- thread per job
-// level 0: every point is a one-point group with an empty log
-__global__ void k_fast_init(const double *__restrict__ pts, long long p0, long long p1, Pass2 P) {
-  const GroupBuf g = blockIdx.y ? P.in1 : P.in0;
-  const double zs = blockIdx.y ? -1.0 : 1.0;
-  for (long long i = p0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p1;
-       i += (long long)gridDim.x * blockDim.x) {
-    Rec r;
-    r.x = pts[3 * i];
-    r.y = pts[3 * i + 1];
-    r.z = zs * pts[3 * i + 2];
-    r.prev = NIL;
-    r.next = NIL;
-    g.rec[i] = r;
-    g.gid[i] = static_cast<int>(i);
-    g.hdr[i] = make_int2(1, 0);
+// coordinates of sorted point g; z negated on the upper pass (exact)
+struct P3 {
+  double x, y, z;
+};
+__device__ __forceinline__ P3 load_pt(const double *__restrict__ pts, int g, double zs) {
+  P3 r;
+  r.x = __ldg(pts + 3ll * g);
+  r.y = __ldg(pts + 3ll * g + 1);
+  r.z = zs * __ldg(pts + 3ll * g + 2);
+  return r;
+}
+
+__device__ __forceinline__ double evt3(int a, int b, int c, const P3 &A, const P3 &B, const P3 &C) {
+  if (a == NIL || b == NIL || c == NIL) return INF;
+  return evtime_xyz(A.x, A.y, A.z, B.x, B.y, B.z, C.x, C.y, C.z);
+}
+
+// ----------------------------------------------------------- level 1 init
+// Level 1 merges two one-point groups: the bridge walk stops at once (both
+// feet have NIL neighbours), no event can occur and the stitch links the
+// pair -- so the level-1 groups are written directly, without reading a
+// coordinate: (nS, k) = (2, 0), links 0 <-> 1, or a one-point carry.
+__global__ void k_fast_init1(long long n, long long j0, long long j1, Pass2 P) {
+  const GroupBuf g = blockIdx.y ? P.out1 : P.out0;
+  for (long long j = j0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; j < j1;
+       j += (long long)gridDim.x * blockDim.x) {
+    const long long L = 2 * j;
+    if (L + 1 < n) {
+      g.hdr[j] = make_int2(2, 0);
+      reinterpret_cast<int4 *>(g.lnk + L)[0] = make_int4(NIL, 1, 0, NIL);
+      reinterpret_cast<int2 *>(g.gid + L)[0] = make_int2(static_cast<int>(L), static_cast<int>(L + 1));
+    } else {
+      g.hdr[j] = make_int2(1, 0);
+      g.lnk[L] = make_int2(NIL, NIL);
+      g.gid[L] = static_cast<int>(L);
+    }
   }
 }
 
-constexpr unsigned short INFO_CHAIN = 0x8000;  // on its child's -inf chain
-constexpr unsigned short INFO_NONE = 0x7fff;   // no merged event yet
+// --------------------------------------------------------- thread per job
+// One WARP = 32 merge jobs, one per lane (levels with many small jobs).
+//
+// Each job owns a slice of the CTA's shared memory, packed by a warp prefix
+// sum of the slice sizes:
+//   [XYZ: x[nS], y[nS], z[nS] f64]  lk[nS] short2 current links
+//   gd[nS] int gid                   fi[nS] u32 first-event / chain info
+// Staging and write-out are warp-cooperative per job (coalesced); the
+// kinetic sweep runs on the job's own lane with the bridge feet, their four
+// neighbours, their coordinates and the four bridge candidate times held in
+// registers, so one step costs a handful of shared-memory accesses: the two
+// link stores of the child event's act, one link load and one coordinate
+// fetch for the one point that changes, and the candidates whose inputs
+// changed.  Without XYZ staging, coordinates come from the sorted point
+// array through the point's gid.
+constexpr unsigned FI_CHAIN = 1u << 31;  // on its child's -inf chain
+constexpr unsigned FI_EV = 1u << 30;     // has a merged event; bits 0-14 a, 15-29 c
 
-// Thread-per-job merge state: the job's records (coordinates + int16 links
-// would not save a cycle on the dependency chain, so records stay 32 B) and
-// its info table live in this thread's shared-memory slice.
-struct TpjJob {
-  Rec *R;                 // nS records, left [0,nSL), right [nSL,nS)
-  unsigned short *info;   // nS: INFO_CHAIN | first merged event index
-  int nSL;
+__host__ __device__ __forceinline__ int tpj_slice_bytes(int nS, bool xyz) {
+  return static_cast<int>(align16((long long)(xyz ? 36 : 12) * nS));
+}
+
+template <bool XYZ>
+struct TpjSlice {
+  double *x, *y, *z;
+  short2 *lk;
+  int *gd;
+  unsigned *fi;
+  __device__ __forceinline__ TpjSlice(unsigned char *base, int nS) {
+    unsigned char *p = base;
+    if (XYZ) {
+      x = reinterpret_cast<double *>(p);
+      y = x + nS;
+      z = y + nS;
+      p += 24ll * nS;
+    }
+    lk = reinterpret_cast<short2 *>(p);
+    gd = reinterpret_cast<int *>(lk + nS);
+    fi = reinterpret_cast<unsigned *>(gd + nS);
+  }
+  __device__ __forceinline__ P3 pt(int p, const double *__restrict__ pts, double zs) const {
+    P3 r;
+    if (p == NIL) {
+      r.x = r.y = r.z = 0.0;
+      return r;
+    }
+    if (XYZ) {
+      r.x = x[p];
+      r.y = y[p];
+      r.z = z[p];
+      return r;
+    }
+    return load_pt(pts, gd[p], zs);
+  }
 };
 
 // The reference's kinetic sweep (_merge_one phase 1, _ckernels.pyx:86-183)
-// for one job on one thread, written branch-free so the 32 lanes of a warp
-// (32 different jobs) stay converged: every lane evaluates the quantities of
-// all six cases and selects; the four bridge candidates are recomputed every
-// step.  Child candidate times are the stored times (the time the facet got
-// when it was emitted one level down, same expression, same triple); events
-// go straight to HBM with their facet and kind; each point's first merged
-// event is recorded for the link rebuild that replaces the rewind.
-// Returns k or a negative code.
-__device__ long long merge_tpj(TpjJob &J, const Ev *__restrict__ evL, int kL,
-                               const Ev *__restrict__ evR, int kR, Ev *out, long long capRef,
-                               long long limitRef, int *pu0, int *pv0, unsigned mask) {
-  Rec *R = J.R;
-  const int nSL = J.nSL;
+// for one job on one lane.  Child candidate times are the stored times (the
+// time the facet got when it was emitted one level down: same expression,
+// same operand order, F4); each child event's stored facet and kind are
+// checked against the current links (a mismatch hands the input to the
+// exact engine).  Emitted events go straight to HBM with their facet and
+// kind; the first merged event of each point is kept for the link rebuild
+// that replaces the reference's rewind.  Returns k or a negative code.
+template <bool XYZ>
+__device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
+                                const double *__restrict__ pts, double zs,
+                                const Ev *__restrict__ evL, int kL, const Ev *__restrict__ evR,
+                                int kR, Ev *__restrict__ out, long long capRef,
+                                long long limitRef, int *pu0, int *pv0) {
+  long long err = 0;
+  // ---- bridge at t = -inf (_find_bridge, _ckernels.pyx:63-83)
   int u = nSL - 1, v = nSL;
-  const int bst = bridge_rec(R, &u, &v, limitRef);
-  __syncwarp(mask);
-  if (bst < 0) return H3D_E_BRIDGE;
+  P3 U, V;
+  U.x = U.y = U.z = V.x = V.y = V.z = 0.0;
+  if (active) {
+    U = S.pt(u, pts, zs);
+    V = S.pt(v, pts, zs);
+    long long moves = 0;
+    for (;;) {
+      const int vn = S.lk[v].y;
+      if (vn != NIL) {
+        const P3 W = S.pt(vn, pts, zs);
+        if (turn_xy(U.x, U.y, V.x, V.y, W.x, W.y) < 0.0) {
+          v = vn;
+          V = W;
+          if (++moves > limitRef) break;
+          continue;
+        }
+      }
+      const int up = S.lk[u].x;
+      if (up != NIL) {
+        const P3 W = S.pt(up, pts, zs);
+        if (turn_xy(W.x, W.y, U.x, U.y, V.x, V.y) < 0.0) {
+          u = up;
+          U = W;
+          if (++moves > limitRef) break;
+          continue;
+        }
+      }
+      break;
+    }
+    if (moves > limitRef) {
+      err = H3D_E_BRIDGE;
+      active = false;
+    }
+  }
   *pu0 = u;
   *pv0 = v;
-  int i = 0, j = 0, k = 0;
-  double tcur = -INF;
-  double c0 = INF, c1 = INF;
-  int bL = 0, bR = 0;
-  Ev nL, nR;  // prefetched next child events
-  nL.t = INF;
-  nR.t = INF;
-  if (kL > 0) {
-    c0 = evL[0].t;
-    bL = evL[0].b;
-    if (kL > 1) nL = evL[1];
+  int un = NIL, up = NIL, vn = NIL, vp = NIL;
+  if (active) {
+    un = S.lk[u].y;
+    up = S.lk[u].x;
+    vn = S.lk[v].y;
+    vp = S.lk[v].x;
   }
-  if (kR > 0) {
-    c1 = evR[0].t;
-    bR = evR[0].b + nSL;
+  P3 UN = S.pt(un, pts, zs), UP = S.pt(up, pts, zs), VN = S.pt(vn, pts, zs),
+     VP = S.pt(vp, pts, zs);
+  double c2 = evt3(u, un, v, U, UN, V);
+  double c3 = evt3(up, u, v, UP, U, V);
+  double c4 = evt3(u, v, vn, U, V, VN);
+  double c5 = evt3(u, vp, v, U, VP, V);
+  // child event streams with one event of prefetch
+  int i = 0, j = 0;
+  Ev cL, cR, nL, nR;
+  cL.t = cR.t = nL.t = nR.t = INF;
+  if (active) {
+    if (kL > 0) cL = evL[0];
+    if (kL > 1) nL = evL[1];
+    if (kR > 0) cR = evR[0];
     if (kR > 1) nR = evR[1];
   }
-  double c2 = evt_rec(R, u, R[u].next, v);
-  double c3 = evt_rec(R, R[u].prev, u, v);
-  double c4 = evt_rec(R, u, v, R[v].next);
-  double c5 = evt_rec(R, u, R[v].prev, v);
-  int err = 0;
-  for (;;) {
+  long long k = 0;
+  double tcur = -INF;
+  // Branch-free step: all 32 lanes (32 different jobs) iterate together until
+  // every job is done -- the vote at the loop head keeps the warp converged;
+  // a finished lane's step is a no-op (every store and load predicated).
+  while (__any_sync(FULL, active)) {
     double best = INF;
     int which = -1;
-    if (c0 > tcur && c0 < best) { best = c0; which = 0; }
-    if (c1 > tcur && c1 < best) { best = c1; which = 1; }
+    if (cL.t > tcur && cL.t < best) { best = cL.t; which = 0; }
+    if (cR.t > tcur && cR.t < best) { best = cR.t; which = 1; }
     if (c2 > tcur && c2 < best) { best = c2; which = 2; }
     if (c3 > tcur && c3 < best) { best = c3; which = 3; }
     if (c4 > tcur && c4 < best) { best = c4; which = 4; }
     if (c5 > tcur && c5 < best) { best = c5; which = 5; }
-    if (which < 0) break;
-    const bool left = which == 0, right = which == 1, child = which <= 1;
-    const int e = left ? bL : (right ? bR : u);
-    const int p = R[e].prev, q = R[e].next;
-    const int un = R[u].next, up = R[u].prev, vn = R[v].next, vp = R[v].prev;
-    const bool nilnb = (p == NIL) | (q == NIL);
-    const int ps = nilnb ? e : p;
-    const bool del = R[ps].next == e;
-    int ea = u, eb = un, ec = v, ek = EV_INS;  // case 2
-    if (child) { ea = p; eb = e; ec = q; ek = del ? EV_DEL : EV_INS; }
-    if (which == 3) { ea = up; eb = u; ek = EV_DEL; }
-    if (which == 4) { eb = v; ec = vn; ek = EV_DEL; }
-    if (which == 5) { eb = vp; }
-    const bool emit = child ? (left ? e < u : e > v) : true;
-    if (child && nilnb) {
-      err = H3D_E_CHAIN;
-      break;
+    active = active && which >= 0;
+    const bool left = active && which == 0, right = active && which == 1;
+    const bool child = left || right;
+    const bool b2 = active && which == 2, b3 = active && which == 3;
+    const bool b4 = active && which == 4, b5 = active && which == 5;
+    const int off = left ? 0 : nSL;
+    const int Ea = (left ? cL.a : cR.a) + off, Eb = (left ? cL.b : cR.b) + off,
+              Ec = (left ? cL.c : cR.c) + off, Ek = left ? cL.kind : cR.kind;
+    // the one link word this step reads: the child event's point, or the
+    // new bridge foot (whose far neighbour becomes the cached neighbour)
+    const int nf = b2 ? un : (b3 ? up : (b4 ? vn : vp));
+    const int z = child ? Eb : ((b2 | b3 | b4 | b5) ? nf : 0);
+    short2 lz = make_short2(NIL, NIL);
+    if (active) lz = S.lk[z];
+    const int e = Eb, p = lz.x, q = lz.y;
+    bool del = false;
+    if (child && p != NIL) del = S.lk[p].y == e;
+    if (child && (p != Ea || q != Ec || (del ? EV_DEL : EV_INS) != Ek)) {
+      err = E_FASTPATH;
+      active = false;
     }
+    const bool act = child && active;
+    // _act (_ckernels.pyx:49-60) on the child event
+    if (act) {
+      S.lk[p].y = static_cast<short>(del ? q : e);
+      S.lk[q].x = static_cast<short>(del ? p : e);
+    }
+    // the cached neighbour that changes and its new point
+    int slot = -1, newpt = NIL;
+    if (act) {
+      slot = (p == u) ? 0 : (q == u) ? 1 : (p == v) ? 2 : (q == v) ? 3 : -1;
+      newpt = del ? ((slot & 1) ? p : q) : e;
+    } else if (active) {
+      slot = which - 2;
+      newpt = (b2 | b4) ? lz.y : lz.x;
+    }
+    // emission (old feet), the reference's rules
+    bool emit = active && (child ? (left ? e < u : e > v) : true);
+    if (emit && k >= capRef - 1) {
+      err = H3D_E_OVERFLOW;
+      active = emit = false;
+      slot = -1;
+    }
+    const int ea = child ? p : (b3 ? up : u);
+    const int eb = child ? e : (b2 ? un : (b3 ? u : (b4 ? v : vp)));
+    const int ec = child ? q : (b4 ? vn : v);
+    const int ek = child ? Ek : ((b3 | b4) ? EV_DEL : EV_INS);
     if (emit) {
-      if (k >= capRef - 1) {
-        err = H3D_E_OVERFLOW;
-        break;
-      }
-      if (k >= 0x4000) {
-        err = static_cast<int>(E_FASTPATH);
-        break;
-      }
       Ev o;
       o.t = best;
       o.a = ea;
@@ -166,84 +294,88 @@ __device__ long long merge_tpj(TpjJob &J, const Ev *__restrict__ evL, int kL,
       o.c = ec;
       o.kind = ek;
       out[k] = o;
-      const unsigned short inf = J.info[eb];
-      if ((inf & INFO_NONE) == INFO_NONE)
-        J.info[eb] = static_cast<unsigned short>((inf & INFO_CHAIN) | k);
-      ++k;
+      const unsigned f = S.fi[eb];
+      if (!(f & FI_EV))
+        S.fi[eb] = f | FI_EV | static_cast<unsigned>(ea) | (static_cast<unsigned>(ec) << 15);
     }
-    if (child) {  // _act
-      R[p].next = del ? q : e;
-      R[q].prev = del ? p : e;
-    }
+    k += emit;
+    // advance the consumed child stream
     if (left) {
+      cL = nL;
       ++i;
-      c0 = nL.t;
-      bL = nL.b;
       if (i + 1 < kL) nL = evL[i + 1]; else nL.t = INF;
     }
     if (right) {
+      cR = nR;
       ++j;
-      c1 = nR.t;
-      bR = nR.b + nSL;
       if (j + 1 < kR) nR = evR[j + 1]; else nR.t = INF;
     }
-    u = (which == 2) ? un : ((which == 3) ? up : u);
-    v = (which == 4) ? vn : ((which == 5) ? vp : v);
-    c2 = evt_rec(R, u, R[u].next, v);
-    c3 = evt_rec(R, R[u].prev, u, v);
-    c4 = evt_rec(R, u, v, R[v].next);
-    c5 = evt_rec(R, u, R[v].prev, v);
-    tcur = best;
+    // rotate the bridge neighbourhood (selects), fetch the one new point
+    const P3 N = S.pt(slot >= 0 ? newpt : NIL, pts, zs);
+    const int u1 = b2 ? un : (b3 ? up : u), v1 = b4 ? vn : (b5 ? vp : v);
+    const P3 U1 = b2 ? UN : (b3 ? UP : U), V1 = b4 ? VN : (b5 ? VP : V);
+    const int un1 = (slot == 0) ? newpt : (b3 ? u : un);
+    const int up1 = (slot == 1) ? newpt : (b2 ? u : up);
+    const int vn1 = (slot == 2) ? newpt : (b5 ? v : vn);
+    const int vp1 = (slot == 3) ? newpt : (b4 ? v : vp);
+    const P3 UN1 = (slot == 0) ? N : (b3 ? U : UN);
+    const P3 UP1 = (slot == 1) ? N : (b2 ? U : UP);
+    const P3 VN1 = (slot == 2) ? N : (b5 ? V : VN);
+    const P3 VP1 = (slot == 3) ? N : (b4 ? V : VP);
+    u = u1; v = v1; un = un1; up = up1; vn = vn1; vp = vp1;
+    U = U1; V = V1; UN = UN1; UP = UP1; VN = VN1; VP = VP1;
+    if (__any_sync(FULL, slot >= 0)) {
+      c2 = evt3(u, un, v, U, UN, V);
+      c3 = evt3(up, u, v, UP, U, V);
+      c4 = evt3(u, v, vn, U, V, VN);
+      c5 = evt3(u, vp, v, U, VP, V);
+    }
+    if (active) tcur = best;
   }
   return err ? err : k;
 }
 
-constexpr int TPJ_REC_BYTES = 34;
-
-// max over CTAs (chunks of tpb consecutive jobs) of the shared bytes the
-// chunk's merges need -- sizes the thread-per-job pool so no CTA needs a
-// second round (a round serialises behind the slowest sweep)
-__global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1, int tpb,
+// Largest shared-memory need of any CTA (32 consecutive jobs) of a level, in
+// points: out[0] = max over CTAs of sum(nS), out[1] = max merge jobs per CTA
+// (one warp per CTA-chunk, coalesced header reads).
+__global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1,
                            unsigned long long *out) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const long long size = 1ll << level, half = size >> 1;
-  const long long chunks = (j1 - j0 + tpb - 1) / tpb;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < chunks;
-       c += (long long)gridDim.x * blockDim.x) {
-    unsigned long long tot = 0;
-    for (long long j = j0 + c * tpb; j < j0 + (c + 1) * tpb && j < j1; ++j) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long chunks = (j1 - j0 + 31) >> 5;
+  for (long long c = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
+       c += warps) {
+    const long long j = j0 + c * 32 + lane;
+    unsigned nS = 0;
+    if (j < j1) {
       const long long L = j << level;
       const long long R_ = (L + size < n) ? L + size : n;
-      if (R_ - L <= half) continue;
-      const int nS = in.hdr[2 * j].x + in.hdr[2 * j + 1].x;
-      tot += align8((long long)TPJ_REC_BYTES * nS);
+      if (R_ - L > half) nS = in.hdr[2 * j].x + in.hdr[2 * j + 1].x;
     }
-    atomicMax(out, tot);
+    unsigned long long tot = nS;
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+    if (lane == 0) atomicMax(out, tot);
   }
-}  // 32-byte record + 2-byte info per point
+}
 
-// One thread per merge job (levels with many jobs).  Each thread's slice of
-// the shared-memory pool holds its job's records and info table; slices are
-// packed by a block-wide prefix scan of the actual sizes (jobs that do not
-// fit wait for the next round).
-template <int TPJ_TPB>
-__global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(Pass2 P, long long n, int level,
-                                                     long long j0, long long j1,
-                                                     long long *err, int pool) {
+template <bool XYZ>
+__global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts,
+                                                 long long n, int level, long long j0,
+                                                 long long j1, long long *err, int pool) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
+  const double zs = blockIdx.y ? -1.0 : 1.0;
   extern __shared__ __align__(16) unsigned char smem[];
-  typedef cub::BlockScan<int, TPJ_TPB> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
+  const int lane = threadIdx.x;
   const long long size = 1ll << level, half = size >> 1;
-  const long long jobs = j1;
-  const long long j = j0 + blockIdx.x * (long long)TPJ_TPB + threadIdx.x;
+  const long long j = j0 + (long long)blockIdx.x * 32 + lane;
   const long long L = j << level, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
-  const bool valid = j < jobs;
   int nSL = 0, kL = 0, nSR = 0, kR = 0;
-  bool pending = false;
-  if (valid) {
+  bool merge = false;
+  if (j < j1) {
     const int2 hl = in.hdr[2 * j];
     nSL = hl.x;
     kL = hl.y;
@@ -251,10 +383,10 @@ __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(Pass2 P, long long n, int 
       const int2 hr = in.hdr[2 * j + 1];
       nSR = hr.x;
       kR = hr.y;
-      pending = true;
-    } else {  // carry (copy_log, parallel.py:107-108)
+      merge = true;
+    } else {  // carry (copy_log, parallel.py:107-108): the short last group
       for (int p = 0; p < nSL; ++p) {
-        out.rec[L + p] = in.rec[L + p];
+        out.lnk[L + p] = in.lnk[L + p];
         out.gid[L + p] = in.gid[L + p];
       }
       for (int e = 0; e < kL; ++e) out.ev[2 * L + e] = in.ev[2 * L + e];
@@ -262,109 +394,165 @@ __global__ void __launch_bounds__(TPJ_TPB) k_fast_tpj(Pass2 P, long long n, int 
     }
   }
   const int nS = nSL + nSR;
-  const int need = static_cast<int>(align8((long long)TPJ_REC_BYTES * nS));
-  if (pending && (need > pool || nS >= 0x4000)) {
-    raise_err(err, E_FASTPATH);  // the host never routes such jobs here
-    pending = false;
+  if (merge && nS >= 0x7fff) {  // int16 local ids; the host never routes such jobs here
+    raise_err(err, E_FASTPATH);
+    merge = false;
   }
-  while (__syncthreads_or(pending)) {
-    int off, total;
-    Scan(scan_tmp).ExclusiveSum(pending ? need : 0, off, total);
-    const bool run = pending && off + need <= pool;
-    // the lanes that run this round re-converge at every phase boundary
-    // (independent thread scheduling would otherwise let the variable-length
-    // staging loops split the warp and run the sweep once per split)
-    const unsigned rmask = __ballot_sync(0xffffffffu, run);
-    if (run) {
-      TpjJob J;
-      J.R = reinterpret_cast<Rec *>(smem + off);
-      J.info = reinterpret_cast<unsigned short *>(J.R + nS);
-      J.nSL = nSL;
-      Rec *R = J.R;
-      {  // stage: independent loads first, then shared stores
-        const Rec *__restrict__ gl = in.rec + L;
-        const Rec *__restrict__ gr = in.rec + M;
-        int p = 0;
-        for (; p + 4 <= nS; p += 4) {
-          Rec r0 = p < nSL ? gl[p] : gr[p - nSL];
-          Rec r1 = p + 1 < nSL ? gl[p + 1] : gr[p + 1 - nSL];
-          Rec r2 = p + 2 < nSL ? gl[p + 2] : gr[p + 2 - nSL];
-          Rec r3 = p + 3 < nSL ? gl[p + 3] : gr[p + 3 - nSL];
-          R[p] = r0;
-          R[p + 1] = r1;
-          R[p + 2] = r2;
-          R[p + 3] = r3;
-        }
-        for (; p < nS; ++p) R[p] = p < nSL ? gl[p] : gr[p - nSL];
-        for (p = nSL; p < nS; ++p) {
-          if (R[p].prev != NIL) R[p].prev += nSL;
-          if (R[p].next != NIL) R[p].next += nSL;
-        }
-      }
-      for (int p = 0; p < nS; ++p) {
-        const int pr = R[p].prev;
-        const bool chain = p == 0 || p == nSL || (pr != NIL && R[pr].next == p);
-        J.info[p] = chain ? (INFO_CHAIN | INFO_NONE) : INFO_NONE;
-      }
-      __syncwarp(rmask);
-      int u0 = 0, v0 = 0;
-      Ev *evo = out.ev + 2 * L;
-      const long long k = merge_tpj(J, in.ev + 2 * L, kL, in.ev + 2 * M, kR, evo, 2 * (R_ - L),
-                                    R_ - L, &u0, &v0, rmask);
-      __syncwarp(rmask);
-      if (k < 0) {
-        raise_err(err, k);
-      } else {
-        // start-of-time links of the merged group (see rebuild_writeout)
-        int cnt = 0;
-        for (int p = 0; p < nS; ++p) {
-          const unsigned short inf = J.info[p];
-          const bool chain = (inf & INFO_CHAIN) && (p < nSL ? p <= u0 : p >= v0);
-          const int fe = inf & INFO_NONE;
-          const bool keep = chain || fe != INFO_NONE;
-          int prv = NIL, nxt = NIL;
-          if (chain) {
-            const Rec &r = p < nSL ? in.rec[L + p] : in.rec[M + (p - nSL)];
-            const int o = p < nSL ? 0 : nSL;
-            prv = r.prev == NIL ? NIL : r.prev + o;
-            nxt = r.next == NIL ? NIL : r.next + o;
-            if (p == u0) nxt = v0;
-            if (p == v0) prv = u0;
-          } else if (keep) {
-            prv = evo[fe].a;
-            nxt = evo[fe].c;
-          }
-          R[p].prev = prv;
-          R[p].next = nxt;
-          J.info[p] = keep ? static_cast<unsigned short>(cnt++) : 0xffff;
-        }
-        bool bad = false;
-        // events first (they read arbitrary new ids), in place in HBM
-        for (int e = 0; e < k; ++e) {
-          Ev o = evo[e];
-          const unsigned short na = J.info[o.a], nb = J.info[o.b], nc = J.info[o.c];
-          bad |= (na == 0xffff) | (nb == 0xffff) | (nc == 0xffff);
-          o.a = na;
-          o.b = nb;
-          o.c = nc;
-          evo[e] = o;
-        }
-        for (int p = 0; p < nS; ++p) {
-          const unsigned short id = J.info[p];
-          if (id == 0xffff) continue;
-          Rec r = R[p];
-          r.prev = r.prev == NIL ? NIL : J.info[r.prev];
-          r.next = r.next == NIL ? NIL : J.info[r.next];
-          bad |= (r.prev == 0xffff) | (r.next == 0xffff);
-          out.rec[L + id] = r;
-          out.gid[L + id] = in.gid[p < nSL ? L + p : M + (p - nSL)];
-        }
-        if (bad) raise_err(err, E_FASTPATH);
-        out.hdr[j] = make_int2(cnt, static_cast<int>(k));
-      }
-      pending = false;
+  // pack the slices: warp exclusive prefix sum of the slice sizes
+  const int bytes = merge ? tpj_slice_bytes(nS, XYZ) : 0;
+  int off = bytes;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, off, o);
+    if (lane >= o) off += t;
+  }
+  const int total = __shfl_sync(FULL, off, 31);
+  off -= bytes;
+  if (total > pool) {  // the host sizes the pool from the measured need
+    if (lane == 0) raise_err(err, E_FASTPATH);
+    return;
+  }
+  // per-job metadata for the cooperative phases (shared, no shuffles); the
+  // cooperative loops run over the concatenated points (events) of the 32
+  // jobs, 32 elements per iteration, each lane locating its job by a binary
+  // search of the prefix sums
+  __shared__ long long s_L[32], s_M[32];
+  __shared__ int s_off[32], s_nSL[32], s_pre[33], s_epre[33], s_cnt[32];
+  s_L[lane] = L;
+  s_M[lane] = M;
+  s_off[lane] = off;
+  s_nSL[lane] = nSL;
+  {
+    int c = merge ? nS : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(FULL, c, o);
+      if (lane >= o) c += t;
+    }
+    s_pre[lane + 1] = c;
+    if (lane == 0) s_pre[0] = 0;
+  }
+  __syncwarp();
+  const int tot_pts = s_pre[32];
+  auto job_of = [&](const int *pre, int x) {
+    int jj = 0;
+#pragma unroll
+    for (int st = 16; st; st >>= 1)
+      if (pre[jj + st] <= x) jj += st;
+    return jj;
+  };
+  // ---- stage (cooperative, coalesced)
+  for (int x = lane; x < tot_pts; x += 32) {
+    const int jj = job_of(s_pre, x);
+    const int p = x - s_pre[jj];
+    const int m_nS = s_pre[jj + 1] - s_pre[jj], m_nSL = s_nSL[jj];
+    const TpjSlice<XYZ> S(smem + s_off[jj], m_nS);
+    const bool left = p < m_nSL;
+    const long long src = left ? s_L[jj] + p : s_M[jj] + (p - m_nSL);
+    int2 l = in.lnk[src];
+    const int g = in.gid[src];
+    if (!left) {
+      if (l.x != NIL) l.x += m_nSL;
+      if (l.y != NIL) l.y += m_nSL;
+    }
+    S.lk[p] = make_short2(static_cast<short>(l.x), static_cast<short>(l.y));
+    S.gd[p] = g;
+    if (XYZ) {
+      const P3 c = load_pt(pts, g, zs);
+      S.x[p] = c.x;
+      S.y[p] = c.y;
+      S.z[p] = c.z;
     }
   }
+  __syncwarp();
+  long long k = 0;
+  int u0 = 0, v0 = 0;
+  const TpjSlice<XYZ> S(smem + off, nS);
+  if (merge) {
+    // chain flags: p is on its child's -inf chain iff its prev points back
+    for (int p = 0; p < nS; ++p) {
+      const int pr = S.lk[p].x;
+      const bool chain = p == 0 || p == nSL || (pr != NIL && S.lk[pr].y == p);
+      S.fi[p] = chain ? FI_CHAIN : 0u;
+    }
+  }
+  // all 32 lanes enter the sweep together (idle lanes inactive)
+  k = merge_tpj2<XYZ>(S, merge, nSL, pts, zs, in.ev + 2 * L, kL, in.ev + 2 * M, kR,
+                      out.ev + 2 * L, 2 * (R_ - L), R_ - L, &u0, &v0);
+  if (merge && k < 0) {
+    raise_err(err, k);
+    merge = false;
+  }
+  int cnt = 0;
+  if (merge) {
+    // ---- start-of-time links of the merged group (replaces the rewind,
+    // DESIGN.md 3.3): the merged -inf chain is every chain-flagged point
+    // left of u0 (inclusive) or right of v0, linked in x order; every other
+    // kept point gets the neighbours of its first merged event (its
+    // insertion).  fi becomes the old -> new id map.
+    int last = NIL;
+    for (int p = 0; p < nS; ++p) {
+      const unsigned f = S.fi[p];
+      const bool chain = (f & FI_CHAIN) && (p < nSL ? p <= u0 : p >= v0);
+      if (chain) {
+        S.lk[p].x = static_cast<short>(last);
+        if (last != NIL) S.lk[last].y = static_cast<short>(p);
+        last = p;
+      } else if (f & FI_EV) {
+        S.lk[p] = make_short2(static_cast<short>(f & 0x7fff), static_cast<short>((f >> 15) & 0x7fff));
+      }
+      S.fi[p] = (chain || (f & FI_EV)) ? static_cast<unsigned>(cnt++) : FULL;
+    }
+    if (last != NIL) S.lk[last].y = NIL;
+  }
+  __syncwarp();
+  {  // prefix sums of the surviving jobs' kept points and events
+    int c = merge ? nS : 0, e = merge ? static_cast<int>(k) : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(FULL, c, o), te = __shfl_up_sync(FULL, e, o);
+      if (lane >= o) {
+        c += t;
+        e += te;
+      }
+    }
+    __syncwarp();
+    s_pre[lane + 1] = c;
+    s_epre[lane + 1] = e;
+    if (lane == 0) s_pre[0] = s_epre[0] = 0;
+    s_cnt[lane] = cnt;
+    if (merge) out.hdr[j] = make_int2(cnt, static_cast<int>(k));
+  }
+  __syncwarp();
+  // ---- write-out (cooperative): links + gids at their new ids, events
+  // remapped in place
+  bool bad = false;
+  const int tot_p2 = s_pre[32], tot_ev = s_epre[32];
+  for (int x = lane; x < tot_p2; x += 32) {
+    const int jj = job_of(s_pre, x);
+    const int p = x - s_pre[jj];
+    const TpjSlice<XYZ> T(smem + s_off[jj], s_pre[jj + 1] - s_pre[jj]);
+    const unsigned id = T.fi[p];
+    if (id == FULL) continue;
+    const short2 l = T.lk[p];
+    int2 o;
+    o.x = l.x == NIL ? NIL : static_cast<int>(T.fi[l.x]);
+    o.y = l.y == NIL ? NIL : static_cast<int>(T.fi[l.y]);
+    bad |= (o.x == -1 && l.x != NIL) | (o.y == -1 && l.y != NIL);
+    out.lnk[s_L[jj] + id] = o;
+    out.gid[s_L[jj] + id] = T.gd[p];
+  }
+  for (int x = lane; x < tot_ev; x += 32) {
+    const int jj = job_of(s_epre, x);
+    const int e = x - s_epre[jj];
+    const TpjSlice<XYZ> T(smem + s_off[jj], s_pre[jj + 1] - s_pre[jj]);
+    Ev *evo = out.ev + 2 * s_L[jj];
+    Ev o = evo[e];
+    const unsigned na = T.fi[o.a], nb = T.fi[o.b], nc = T.fi[o.c];
+    bad |= (na == FULL) | (nb == FULL) | (nc == FULL);
+    o.a = static_cast<int>(na);
+    o.b = static_cast<int>(nb);
+    o.c = static_cast<int>(nc);
+    evo[e] = o;
+  }
+  if (__any_sync(FULL, bad) && lane == 0) raise_err(err, E_FASTPATH);
 }
 
 // -------------------------------------------------------------- warp merge
@@ -609,10 +797,10 @@ __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R
     const bool hasev = fe != FIRST_NONE;
     int prv = NIL, nxt = NIL;
     if (chain) {
-      const Rec o = (p < nSL) ? in.rec[L + p] : in.rec[M + (p - nSL)];
+      const int2 o = (p < nSL) ? in.lnk[L + p] : in.lnk[M + (p - nSL)];
       const int off = (p < nSL) ? 0 : nSL;
-      prv = (o.prev == NIL) ? NIL : o.prev + off;
-      nxt = (o.next == NIL) ? NIL : o.next + off;
+      prv = (o.x == NIL) ? NIL : o.x + off;
+      nxt = (o.y == NIL) ? NIL : o.y + off;
       if (p == u0) nxt = v0;
       if (p == v0) prv = u0;
     } else if (hasev) {
@@ -657,22 +845,22 @@ __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R
     }
   }
   __syncwarp();
-  // E: move records and gids (chunked read-all / write; ids only move left,
+  // E: move links and gids (chunked read-all / write; ids only move left,
   // and a gid write only lands on ids already consumed)
   for (int p0 = 0; p0 < nS; p0 += 32) {
     const int p = p0 + lane;
     int id = -1, g = 0;
-    Rec r;
+    int2 l;
     if (p < nS) {
       id = first[p];
       if (id >= 0) {
-        r = R[p];
+        l = make_int2(R[p].prev, R[p].next);
         g = in.gid[p < nSL ? L + p : M + (p - nSL)];
       }
     }
     __syncwarp();
     if (id >= 0) {
-      out.rec[L + id] = r;
+      out.lnk[L + id] = l;
       out.gid[L + id] = g;
     }
     __syncwarp();
@@ -693,13 +881,17 @@ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
 // out.rec[L..], first table in out.gid[L..]) with the merged child events
 // in the pass's HBM scratch (PassWS::seq).
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, int level,
+__global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, const double *__restrict__ pts,
+                                                          long long n, int level,
                                                           long long j0, long long j1,
                                                           long long *err, int pool,
-                                                          Ev *gseq0, Ev *gseq1) {
+                                                          Ev *gseq0, Ev *gseq1, Rec *grec0,
+                                                          Rec *grec1) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   Ev *gseq = blockIdx.y ? gseq1 : gseq0;
+  Rec *grec = blockIdx.y ? grec1 : grec0;
+  const double zs = blockIdx.y ? -1.0 : 1.0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ long long s_need[WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -722,7 +914,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, 
       kR = hr.y;
     } else {  // carry (copy_log, parallel.py:107-108)
       for (int p = lane; p < nSL; p += 32) {
-        out.rec[L + p] = in.rec[L + p];
+        out.lnk[L + p] = in.lnk[L + p];
         out.gid[L + p] = in.gid[L + p];
       }
       for (int e = lane; e < kL; e += 32) out.ev[2 * L + e] = in.ev[2 * L + e];
@@ -735,7 +927,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, 
   bool pending = merge && !global_mode;
   auto run_job = [&](Rec *Rr, int *first, Ev *seq) {
     for (int p = lane; p < nS; p += 32) {
-      Rec r = (p < nSL) ? in.rec[L + p] : in.rec[M + (p - nSL)];
+      const long long src = (p < nSL) ? L + p : M + (p - nSL);
+      const int2 l = in.lnk[src];
+      const P3 c = load_pt(pts, in.gid[src], zs);
+      Rec r;
+      r.x = c.x;
+      r.y = c.y;
+      r.z = c.z;
+      r.prev = l.x;
+      r.next = l.y;
       if (p >= nSL) {
         if (r.prev != NIL) r.prev += nSL;
         if (r.next != NIL) r.next += nSL;
@@ -761,9 +961,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, long long n, 
     }
   };
   if (global_mode) {
-    // in HBM: records at out.rec[L..L+nS) (nS <= R-L), first table in
-    // out.gid[L..), merged child events in the level scratch at gseq[2L..)
-    run_job(out.rec + L, out.gid + L, gseq + 2 * L);
+    // in HBM: records in the pass's record scratch at grec[L..L+nS) (nS <=
+    // R-L), first table in out.gid[L..), merged child events in the level
+    // scratch at gseq[2L..)
+    run_job(grec + L, out.gid + L, gseq + 2 * L);
   }
   // shared-memory pool: warps whose jobs fit run together, the rest wait
   for (;;) {
@@ -821,45 +1022,49 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kPool = 64 * 1024;
 constexpr int kTpjPool = 200 * 1024;
-int kTpjMaxLevel = 9;  // H3D_TPJ_MAX_LEVEL
+int kTpjMaxLevel = 9;           // H3D_TPJ_MAX_LEVEL
 long long kTpjMinJobs = 16384;  // H3D_TPJ_MIN_JOBS (per pass)
+long long kTpjXyzMax = 48 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the pool fits
 
 struct PassWS {
   GroupBuf A, B;
   Ev *seq;                  // merged child events of HBM-resident warp jobs (2n)
+  Rec *rec;                 // records of HBM-resident warp jobs (n)
   unsigned long long *need; // thread-per-job pool sizing
 };
 
 bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
   for (GroupBuf *g : {&w.A, &w.B}) {
     g->hdr = ar.take<int2>(n);
-    g->rec = ar.take<Rec>(n);
+    g->lnk = ar.take<int2>(n);
     g->gid = ar.take<int>(n);
     g->ev = ar.take<Ev>(2 * n);
   }
   w.seq = ar.take<Ev>(2 * n);
+  w.rec = ar.take<Rec>(n);
   w.need = ar.take<unsigned long long>(4);
   return ar.base == nullptr || w.need != nullptr;
 }
 
 bool g_attr_done = false;
-// thread-per-job tuning (H3D_TPJ_TPB, H3D_TPJ_FILL, H3D_TPJ_POOL_KB override)
-int g_tpj_tpb = 32;
-double g_tpj_fill = 0.5;
-long long g_tpj_pool = 200 * 1024;
-int g_tpj_measure = 1;  // H3D_TPJ_MEASURE=0: size the pool by H3D_TPJ_FILL instead
+
+template <bool XYZ>
+void launch_tpj(dim3 grid, int pool, cudaStream_t s, Pass2 P, const double *pts, long long n,
+                int lv, long long j0, long long j1, long long *err) {
+  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool);
+}
 
 }  // namespace
 
 extern "C" {
 
 int64_t h3d_fast_layout(int64_t n, int64_t *offsets) {
-  // byte offsets of A.hdr, A.rec, A.gid, A.ev, B.hdr, B.rec, B.gid, B.ev, seq
+  // byte offsets of A.hdr, A.lnk, A.gid, A.ev, B.hdr, B.lnk, B.gid, B.ev, seq
   char *base = reinterpret_cast<char *>(size_t(1) << 40);
   h3d_arena ar(base, ~size_t(0) >> 4);
   PassWS w;
   if (!carve_pass(ar, n, w)) return H3D_E_ARG;
-  const void *p[9] = {w.A.hdr, w.A.rec, w.A.gid, w.A.ev, w.B.hdr, w.B.rec, w.B.gid, w.B.ev, w.seq};
+  const void *p[9] = {w.A.hdr, w.A.lnk, w.A.gid, w.A.ev, w.B.hdr, w.B.lnk, w.B.gid, w.B.ev, w.seq};
   for (int i = 0; i < 9; ++i) offsets[i] = static_cast<const char *>(p[i]) - base;
   return 0;
 }
@@ -885,21 +1090,14 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   if (!g_attr_done) {
     if (h3d_check(cudaFuncSetAttribute(k_fast_warp<kWarps>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kPool)) ||
-        h3d_check(cudaFuncSetAttribute(k_fast_tpj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kTpjPool)) ||
-        h3d_check(cudaFuncSetAttribute(k_fast_tpj<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kTpjPool)) ||
-        h3d_check(cudaFuncSetAttribute(k_fast_tpj<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kTpjPool)))
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)))
       return H3D_E_CUDA;
-    if (const char *e = getenv("H3D_TPJ_TPB")) g_tpj_tpb = atoi(e);
-    if (const char *e = getenv("H3D_TPJ_FILL")) g_tpj_fill = atof(e);
-    if (const char *e = getenv("H3D_TPJ_POOL_KB")) g_tpj_pool = atoll(e) * 1024;
     if (const char *e = getenv("H3D_TPJ_MAX_LEVEL")) kTpjMaxLevel = atoi(e);
-    if (const char *e = getenv("H3D_TPJ_MEASURE")) g_tpj_measure = atoi(e);
     if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinJobs = atoll(e);
-    if (g_tpj_tpb != 32 && g_tpj_tpb != 64) g_tpj_tpb = 128;
-    if (g_tpj_pool > kTpjPool) g_tpj_pool = kTpjPool;
+    if (const char *e = getenv("H3D_TPJ_XYZ_KB")) kTpjXyzMax = atoll(e) * 1024;
     g_attr_done = true;
   }
   long long *err = reinterpret_cast<long long *>(err_dev);
@@ -908,53 +1106,50 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   if (lv_hi > levels) lv_hi = levels;
   // level l reads buffer (l-1)&1 and writes buffer l&1 (A = 0, B = 1)
   Pass2 P = (lv_lo & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
-  if (lv_lo == 1) {
+  int lv = lv_lo;
+  if (lv_lo == 1) {  // level 1 written directly (no coordinates needed)
+    const long long j0 = p0 >> 1, j1 = (p1 + 1) >> 1;
+    void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
     h3d_count_launches(1);
-    const long long np = p1 - p0;
-    const unsigned gi = h3d_grid(np, 256) > 4096 ? 4096 : h3d_grid(np, 256);
-    k_fast_init<<<dim3(gi, 2), 256, 0, s>>>(sorted_pts, p0, p1, P);
+    const unsigned gi = h3d_grid(j1 - j0, 256) > 8192 ? 8192 : h3d_grid(j1 - j0, 256);
+    k_fast_init1<<<dim3(gi, 2), 256, 0, s>>>(n, j0, j1, P);
+    h3d_prof_end(e0, 1 + 2000, 2, s);
+    P = Pass2{P.out0, P.out1, P.in0, P.in1};
+    lv = 2;
   }
-  for (int lv = lv_lo; lv <= lv_hi; ++lv) {
+  for (; lv <= lv_hi; ++lv) {
     // the jobs of this level inside the point range [p0, p1)
     const long long j0 = p0 >> lv;
     const long long j1 = (p1 + (1ll << lv) - 1) >> lv;
     const long long jobs = j1 - j0;
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
-    h3d_count_launches(1);
-    // thread per job while jobs are plentiful and small, warp per job above
-    if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel && ((long long)TPJ_REC_BYTES << lv) <= kTpjPool) {
-      // threads per CTA and shared pool per level: the pool is the largest
-      // CTA's actual need (one small read-back per level), capped
-      const int tpb = g_tpj_tpb;
-      long long pool;
-      if (g_tpj_measure) {
-        cudaMemsetAsync(w0.need, 0, sizeof(unsigned long long), s);
-        const long long chunks = (jobs + tpb - 1) / tpb;
-        h3d_count_launches(1);
-        k_tpj_need<<<dim3(h3d_grid(chunks, 128) > 2048 ? 2048 : h3d_grid(chunks, 128), 2), 128, 0,
-                     s>>>(P, n, lv, j0, j1, tpb, w0.need);
-        unsigned long long hneed = 0;
-        if (h3d_check(cudaMemcpyAsync(&hneed, w0.need, sizeof(hneed), cudaMemcpyDeviceToHost, s)) ||
-            h3d_check(cudaStreamSynchronize(s)))
-          return H3D_E_CUDA;
-        pool = static_cast<long long>(hneed);
+    // one lane per job while jobs are plentiful and small, one warp per job above
+    if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel && (1ll << lv) < 0x7fff) {
+      // shared pool = the largest CTA's measured need (one small read-back)
+      cudaMemsetAsync(w0.need, 0, sizeof(unsigned long long), s);
+      const long long chunks = (jobs + 31) / 32;
+      h3d_count_launches(2);
+      k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 4096 ? 4096 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
+          P, n, lv, j0, j1, w0.need);
+      unsigned long long maxpts = 0;
+      if (h3d_check(cudaMemcpyAsync(&maxpts, w0.need, sizeof(maxpts), cudaMemcpyDeviceToHost, s)) ||
+          h3d_check(cudaStreamSynchronize(s)))
+        return H3D_E_CUDA;
+      const long long pool_xyz = 36ll * maxpts + 32 * 16;
+      const long long pool_lk = 12ll * maxpts + 32 * 16;
+      const dim3 grid(h3d_grid(jobs, 32), 2);
+      if (pool_xyz <= kTpjXyzMax) {
+        const int pool = static_cast<int>(pool_xyz < 1024 ? 1024 : pool_xyz);
+        launch_tpj<true>(grid, pool, s, P, sorted_pts, n, lv, j0, j1, err);
       } else {
-        pool = (long long)tpb * align8((long long)(TPJ_REC_BYTES * g_tpj_fill * (1ll << lv)));
+        const long long pl = pool_lk > kTpjPool ? kTpjPool : pool_lk;
+        launch_tpj<false>(grid, static_cast<int>(pl), s, P, sorted_pts, n, lv, j0, j1, err);
       }
-      if (pool > g_tpj_pool) pool = g_tpj_pool;
-      if (pool < (long long)TPJ_REC_BYTES << lv) pool = align8((long long)TPJ_REC_BYTES << lv);
-      if (pool < 2048) pool = 2048;
-      const dim3 grid(h3d_grid(jobs, tpb), 2);
-      if (tpb == 32)
-        k_fast_tpj<32><<<grid, 32, pool, s>>>(P, n, lv, j0, j1, err, static_cast<int>(pool));
-      else if (tpb == 64)
-        k_fast_tpj<64><<<grid, 64, pool, s>>>(P, n, lv, j0, j1, err, static_cast<int>(pool));
-      else
-        k_fast_tpj<128><<<grid, 128, pool, s>>>(P, n, lv, j0, j1, err, static_cast<int>(pool));
       h3d_prof_end(e0, lv + 1000, 2, s);
     } else {
+      h3d_count_launches(1);
       k_fast_warp<kWarps><<<dim3(h3d_grid(jobs, kWarps), 2), kWarps * 32, kPool, s>>>(
-          P, n, lv, j0, j1, err, kPool, w0.seq, w1.seq);
+          P, sorted_pts, n, lv, j0, j1, err, kPool, w0.seq, w1.seq, w0.rec, w1.rec);
       h3d_prof_end(e0, lv, 2, s);
     }
     P = Pass2{P.out0, P.out1, P.in0, P.in1};

@@ -10,7 +10,7 @@ one `plan_level` (pkg/src/hull3d/parallel.py:49-65) would produce.
   (`h3d_fast_passes_range`).
 * Each of the last log2 G levels pairs slabs: at level l a group spans
   2^(l-s) slabs; the owner of its right half sends its compact group (header,
-  records, ids, events of both passes -- everything the merge reads) to the
+  links, ids, events of both passes -- everything the merge reads) to the
   owner of the left half, which runs that one merge job.  A left half with no
   right half (ragged n) is a carry and needs no message.
 * Rank 0 ends with the final groups and runs facet extraction and the
@@ -90,7 +90,7 @@ class GroupLayout:
     """Views of one pass workspace's compact-group arrays (see
     h3d_fast_layout in include/hull3d_b200.h)."""
 
-    REC = 32
+    LNK = 8
     EV = 24
 
     def __init__(self, ws: torch.Tensor, n: int):
@@ -107,9 +107,9 @@ class GroupLayout:
         o = self._arr(buf, 0) + 8 * g
         return self.ws[o:o + 8]
 
-    def rec_view(self, buf: int, L: int, nS: int) -> torch.Tensor:
-        o = self._arr(buf, 1) + self.REC * L
-        return self.ws[o:o + self.REC * nS]
+    def lnk_view(self, buf: int, L: int, nS: int) -> torch.Tensor:
+        o = self._arr(buf, 1) + self.LNK * L
+        return self.ws[o:o + self.LNK * nS]
 
     def gid_view(self, buf: int, L: int, nS: int) -> torch.Tensor:
         o = self._arr(buf, 2) + 4 * L
@@ -158,7 +158,7 @@ def send_group(layouts, buf: int, level: int, g: int, dst: int) -> None:
     h = hdr.cpu().tolist()
     for p, lay in enumerate(layouts):
         nS, k = h[2 * p], h[2 * p + 1]
-        for view in (lay.rec_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
+        for view in (lay.lnk_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
             if view.numel():
                 _send(view.contiguous(), dst)
 
@@ -174,7 +174,7 @@ def recv_group(layouts, buf: int, level: int, g: int, src: int) -> None:
     for p, lay in enumerate(layouts):
         nS, k = h[2 * p], h[2 * p + 1]
         lay.hdr_view(buf, g).copy_(hdr[2 * p:2 * p + 2].view(torch.uint8))
-        for view in (lay.rec_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
+        for view in (lay.lnk_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
             if view.numel():
                 tmp = torch.empty_like(view)
                 _recv(tmp, src)

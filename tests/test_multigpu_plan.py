@@ -93,7 +93,7 @@ def _worker(rank, world, port, n, q):
             for p, lay in enumerate(lays):
                 nS, k = sizes[p]
                 lay.hdr_view(buf, g).copy_(torch.tensor([nS, k], dtype=torch.int32).view(torch.uint8))
-                for v in (lay.rec_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
+                for v in (lay.lnk_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
                     v.copy_(torch.randint(0, 256, (v.numel(),), generator=gen, dtype=torch.uint8))
             send_group(lays, buf, level, g, 0)
             q.put(("sent", [w.clone().numpy() for w in ws]))
