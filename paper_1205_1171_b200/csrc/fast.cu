@@ -335,9 +335,16 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
   return err ? err : k;
 }
 
-// Largest shared-memory need of any CTA (32 consecutive jobs) of a level, in
-// points: out[0] = max over CTAs of sum(nS), out[1] = max merge jobs per CTA
-// (one warp per CTA-chunk, coalesced header reads).
+// shared bytes of one warp job: records, first table, merged child events
+__host__ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
+  return align8(32ll * nS + 4ll * nS) + 24ll * kin;
+}
+
+// Shared-memory need of the thread-per-job launch, for every jobs-per-CTA
+// choice at once: out[r] = max over CTAs of sum(nS) when a CTA takes
+// 32 >> r consecutive jobs (r = 0..5); out[6] = largest single nS; out[7] =
+// largest shared-memory need of one warp-per-job merge.  One warp per 32
+// jobs, coalesced header reads.
 __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1,
                            unsigned long long *out) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
@@ -345,37 +352,59 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long chunks = (j1 - j0 + 31) >> 5;
+  unsigned long long mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (long long c = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
     const long long j = j0 + c * 32 + lane;
-    unsigned nS = 0;
+    unsigned long long nS = 0, wb = 0;
     if (j < j1) {
       const long long L = j << level;
       const long long R_ = (L + size < n) ? L + size : n;
-      if (R_ - L > half) nS = in.hdr[2 * j].x + in.hdr[2 * j + 1].x;
+      if (R_ - L > half) {
+        const int2 hl = in.hdr[2 * j], hr = in.hdr[2 * j + 1];
+        nS = hl.x + hr.x;
+        wb = warp_job_bytes(static_cast<int>(nS), hl.y + hr.y);
+      }
     }
-    unsigned long long tot = nS;
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
-    if (lane == 0) atomicMax(out, tot);
+    mx[6] = nS > mx[6] ? nS : mx[6];
+    mx[7] = wb > mx[7] ? wb : mx[7];
+    unsigned long long t = nS;
+    mx[5] = t > mx[5] ? t : mx[5];  // 1 job per CTA
+#pragma unroll
+    for (int r = 4; r >= 0; --r) {  // 2, 4, 8, 16, 32 jobs per CTA
+      t += __shfl_xor_sync(FULL, t, 1 << (4 - r));
+      mx[r] = t > mx[r] ? t : mx[r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    unsigned long long m = mx[r];
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(FULL, m, o);
+      m = x > m ? x : m;
+    }
+    if (lane == 0 && m) atomicMax(out + r, m);
   }
 }
 
 template <bool XYZ>
 __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int level, long long j0,
-                                                 long long j1, long long *err, int pool) {
+                                                 long long j1, long long *err, int pool,
+                                                 int jpc) {
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   const double zs = blockIdx.y ? -1.0 : 1.0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x;
   const long long size = 1ll << level, half = size >> 1;
-  const long long j = j0 + (long long)blockIdx.x * 32 + lane;
+  // jpc (1..32) jobs per CTA: lanes >= jpc idle (large jobs, few per CTA)
+  const long long j = j0 + (long long)blockIdx.x * jpc + lane;
   const long long L = j << level, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
   int nSL = 0, kL = 0, nSR = 0, kR = 0;
   bool merge = false;
-  if (j < j1) {
+  if (lane < jpc && j < j1) {
     const int2 hl = in.hdr[2 * j];
     nSL = hl.x;
     kL = hl.y;
@@ -869,10 +898,6 @@ __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R
   if (lane == 0) out.hdr[gidx] = make_int2(cnt, k);
 }
 
-// shared bytes of one warp job: records, first table, merged child events
-__device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
-  return align8(32ll * nS + 4ll * nS) + 24ll * kin;
-}
 
 // One warp per merge job (levels with few, large jobs).  A job's records,
 // first table and time-merged child events are staged in the CTA's shared
@@ -1019,12 +1044,11 @@ using namespace h3d;
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kPool = 64 * 1024;
+constexpr long long kWarpPoolMax = 200 * 1024;
+long long kTpjMinTotalJobs = 148 * 32;  // H3D_TPJ_MIN_JOBS (both passes)
 constexpr int kTpjPool = 200 * 1024;
-int kTpjMaxLevel = 9;           // H3D_TPJ_MAX_LEVEL
-long long kTpjMinJobs = 16384;  // H3D_TPJ_MIN_JOBS (per pass)
-long long kTpjXyzMax = 48 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the pool fits
+int kTpjMaxLevel = 40;          // H3D_TPJ_MAX_LEVEL
+long long kTpjXyzMax = 16 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the pool fits
 
 struct PassWS {
   GroupBuf A, B;
@@ -1042,16 +1066,16 @@ bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
   }
   w.seq = ar.take<Ev>(2 * n);
   w.rec = ar.take<Rec>(n);
-  w.need = ar.take<unsigned long long>(4);
+  w.need = ar.take<unsigned long long>(8);
   return ar.base == nullptr || w.need != nullptr;
 }
 
 bool g_attr_done = false;
 
 template <bool XYZ>
-void launch_tpj(dim3 grid, int pool, cudaStream_t s, Pass2 P, const double *pts, long long n,
-                int lv, long long j0, long long j1, long long *err) {
-  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool);
+void launch_tpj(dim3 grid, int pool, int jpc, cudaStream_t s, Pass2 P, const double *pts,
+                long long n, int lv, long long j0, long long j1, long long *err) {
+  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc);
 }
 
 }  // namespace
@@ -1088,16 +1112,16 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   PassWS w0, w1;
   if (!carve_pass(a0, n, w0) || !carve_pass(a1, n, w1)) return H3D_E_ARG;
   if (!g_attr_done) {
-    if (h3d_check(cudaFuncSetAttribute(k_fast_warp<kWarps>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kPool)) ||
+    if (h3d_check(cudaFuncSetAttribute(k_fast_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kWarpPoolMax))) ||
         h3d_check(cudaFuncSetAttribute(k_fast_tpj<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
         h3d_check(cudaFuncSetAttribute(k_fast_tpj<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)))
       return H3D_E_CUDA;
     if (const char *e = getenv("H3D_TPJ_MAX_LEVEL")) kTpjMaxLevel = atoi(e);
-    if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinJobs = atoll(e);
     if (const char *e = getenv("H3D_TPJ_XYZ_KB")) kTpjXyzMax = atoll(e) * 1024;
+    if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinTotalJobs = atoll(e);
     g_attr_done = true;
   }
   long long *err = reinterpret_cast<long long *>(err_dev);
@@ -1123,33 +1147,56 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     const long long j1 = (p1 + (1ll << lv) - 1) >> lv;
     const long long jobs = j1 - j0;
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
-    // one lane per job while jobs are plentiful and small, one warp per job above
-    if (jobs >= kTpjMinJobs && lv <= kTpjMaxLevel && (1ll << lv) < 0x7fff) {
-      // shared pool = the largest CTA's measured need (one small read-back)
-      cudaMemsetAsync(w0.need, 0, sizeof(unsigned long long), s);
-      const long long chunks = (jobs + 31) / 32;
-      h3d_count_launches(2);
-      k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 4096 ? 4096 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
-          P, n, lv, j0, j1, w0.need);
-      unsigned long long maxpts = 0;
-      if (h3d_check(cudaMemcpyAsync(&maxpts, w0.need, sizeof(maxpts), cudaMemcpyDeviceToHost, s)) ||
-          h3d_check(cudaStreamSynchronize(s)))
-        return H3D_E_CUDA;
-      const long long pool_xyz = 36ll * maxpts + 32 * 16;
-      const long long pool_lk = 12ll * maxpts + 32 * 16;
-      const dim3 grid(h3d_grid(jobs, 32), 2);
-      if (pool_xyz <= kTpjXyzMax) {
-        const int pool = static_cast<int>(pool_xyz < 1024 ? 1024 : pool_xyz);
-        launch_tpj<true>(grid, pool, s, P, sorted_pts, n, lv, j0, j1, err);
+    // Level routing from the measured group sizes (one small read-back):
+    // one lane per job while the level has enough jobs to fill the GPU and
+    // they fit a shared-memory slice (int16 local ids); one warp per job
+    // (1-warp CTAs, pool = the largest job's need, HBM mode above it) for
+    // the few-job levels.
+    cudaMemsetAsync(w0.need, 0, 8 * sizeof(unsigned long long), s);
+    const long long chunks = (jobs + 31) / 32;
+    h3d_count_launches(1);
+    k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 4096 ? 4096 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
+        P, n, lv, j0, j1, w0.need);
+    unsigned long long need[8];
+    if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
+        h3d_check(cudaStreamSynchronize(s)))
+      return H3D_E_CUDA;
+    bool tpj = lv <= kTpjMaxLevel && 2 * jobs >= kTpjMinTotalJobs && need[6] < 0x7fff;
+    int jpc = 32;
+    bool xyz = false;
+    long long pool = 0;
+    if (tpj) {
+      int r = 0;
+      while (r < 5 && 12ll * need[r] + 32 * 16 > kTpjPool) ++r;
+      if (12ll * need[r] + 32 * 16 > kTpjPool) {
+        tpj = false;
       } else {
-        const long long pl = pool_lk > kTpjPool ? kTpjPool : pool_lk;
-        launch_tpj<false>(grid, static_cast<int>(pl), s, P, sorted_pts, n, lv, j0, j1, err);
+        jpc = 32 >> r;
+        // stage coordinates when the pool stays small, or when there are
+        // too few CTAs for shared memory to limit occupancy
+        const long long ctas = 2 * ((jobs + jpc - 1) / jpc);
+        xyz = 36ll * need[r] + 32 * 16 <= kTpjXyzMax ||
+              (ctas <= 4 * 148 && 36ll * need[r] + 32 * 16 <= kTpjPool);
+        pool = (xyz ? 36ll : 12ll) * need[r] + 32 * 16;
+        if (pool < 1024) pool = 1024;
       }
+    }
+    if (tpj) {
+      h3d_count_launches(1);
+      const dim3 grid(h3d_grid(jobs, jpc), 2);
+      if (xyz)
+        launch_tpj<true>(grid, static_cast<int>(pool), jpc, s, P, sorted_pts, n, lv, j0, j1, err);
+      else
+        launch_tpj<false>(grid, static_cast<int>(pool), jpc, s, P, sorted_pts, n, lv, j0, j1, err);
       h3d_prof_end(e0, lv + 1000, 2, s);
     } else {
+      long long wpool = static_cast<long long>(need[7]);
+      if (wpool > kWarpPoolMax) wpool = kWarpPoolMax;
+      if (wpool < 1024) wpool = 1024;
       h3d_count_launches(1);
-      k_fast_warp<kWarps><<<dim3(h3d_grid(jobs, kWarps), 2), kWarps * 32, kPool, s>>>(
-          P, sorted_pts, n, lv, j0, j1, err, kPool, w0.seq, w1.seq, w0.rec, w1.rec);
+      k_fast_warp<1><<<dim3(h3d_grid(jobs, 1), 2), 32, wpool, s>>>(
+          P, sorted_pts, n, lv, j0, j1, err, static_cast<int>(wpool), w0.seq, w1.seq, w0.rec,
+          w1.rec);
       h3d_prof_end(e0, lv, 2, s);
     }
     P = Pass2{P.out0, P.out1, P.in0, P.in1};
