@@ -27,6 +27,7 @@
 // point's gid and kernels read the sorted point array (z negated on the
 // upper pass).
 #include <cstdlib>
+#include <type_traits>
 
 #include <cub/cub.cuh>
 
@@ -115,12 +116,16 @@ __host__ __device__ __forceinline__ int tpj_slice_bytes(int nS, bool xyz) {
   return static_cast<int>(align16((long long)(xyz ? 36 : 12) * nS));
 }
 
-template <bool XYZ>
+// A job's point table: coordinates (XYZ) or gids, links, first-event info.
+// STRIDE = 1: a packed slice (thread-per-job kernel); STRIDE = 32: lane-
+// interleaved arrays (leaf kernel, conflict-free whatever the index).
+template <bool XYZ, int STRIDE = 1>
 struct TpjSlice {
   double *x, *y, *z;
   short2 *lk;
   int *gd;
   unsigned *fi;
+  __device__ __forceinline__ TpjSlice() {}
   __device__ __forceinline__ TpjSlice(unsigned char *base, int nS) {
     unsigned char *p = base;
     if (XYZ) {
@@ -133,6 +138,21 @@ struct TpjSlice {
     gd = reinterpret_cast<int *>(lk + nS);
     fi = reinterpret_cast<unsigned *>(gd + nS);
   }
+  __device__ __forceinline__ short2 &LK(int p) const { return lk[p * STRIDE]; }
+  __device__ __forceinline__ unsigned &FI(int p) const { return fi[p * STRIDE]; }
+  __device__ __forceinline__ int &GD(int p) const { return gd[p * STRIDE]; }
+  __device__ __forceinline__ TpjSlice shifted(int d) const {  // ids relative to point d
+    TpjSlice r = *this;
+    if (XYZ) {
+      r.x += d * STRIDE;
+      r.y += d * STRIDE;
+      r.z += d * STRIDE;
+    }
+    r.lk += d * STRIDE;
+    if (!XYZ) r.gd += d * STRIDE;
+    r.fi += d * STRIDE;
+    return r;
+  }
   __device__ __forceinline__ P3 pt(int p, const double *__restrict__ pts, double zs) const {
     P3 r;
     if (p == NIL) {
@@ -140,12 +160,49 @@ struct TpjSlice {
       return r;
     }
     if (XYZ) {
-      r.x = x[p];
-      r.y = y[p];
-      r.z = z[p];
+      r.x = x[p * STRIDE];
+      r.y = y[p * STRIDE];
+      r.z = z[p * STRIDE];
       return r;
     }
-    return load_pt(pts, gd[p], zs);
+    return load_pt(pts, gd[p * STRIDE], zs);
+  }
+};
+
+// event streams of the sweep: HBM (24-byte Ev) ...
+struct GEvIn {
+  static constexpr bool kPrefetch = true;  // HBM: one event of prefetch
+  const Ev *__restrict__ p;
+  __device__ __forceinline__ Ev get(int i) const { return p[i]; }
+};
+struct GEvOut {
+  Ev *__restrict__ p;
+  __device__ __forceinline__ void put(long long k, const Ev &o) const { p[k] = o; }
+};
+// ... or lane-interleaved shared memory (leaf kernel): time + one word with
+// the 8-bit ids a, b, c and the kind
+struct LEvIn {
+  static constexpr bool kPrefetch = false;  // shared memory: read when consumed
+  const double *t;
+  const unsigned *w;
+  __device__ __forceinline__ Ev get(int i) const {
+    Ev e;
+    e.t = t[i * 32];
+    const unsigned x = w[i * 32];
+    e.a = x & 0xff;
+    e.b = (x >> 8) & 0xff;
+    e.c = (x >> 16) & 0xff;
+    e.kind = x >> 24;
+    return e;
+  }
+};
+struct LEvOut {
+  double *t;
+  unsigned *w;
+  __device__ __forceinline__ void put(long long k, const Ev &o) const {
+    t[k * 32] = o.t;
+    w[k * 32] = static_cast<unsigned>(o.a) | (static_cast<unsigned>(o.b) << 8) |
+                (static_cast<unsigned>(o.c) << 16) | (static_cast<unsigned>(o.kind) << 24);
   }
 };
 
@@ -157,15 +214,16 @@ struct TpjSlice {
 // exact engine).  Emitted events go straight to HBM with their facet and
 // kind; the first merged event of each point is kept for the link rebuild
 // that replaces the reference's rewind.  Returns k or a negative code.
-template <bool XYZ>
-__device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
-                                const double *__restrict__ pts, double zs,
-                                const Ev *__restrict__ evL, int kL, const Ev *__restrict__ evR,
-                                int kR, Ev *__restrict__ out, long long capRef,
-                                long long limitRef, int *pu0, int *pv0) {
+// u_init: the left child's last point (its right neighbour is the right
+// child's first); roff: added to the right child's event ids.
+template <class SL, class EIN, class EOUT>
+__device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
+                                const double *__restrict__ pts, double zs, EIN evL, int kL,
+                                EIN evR, int kR, EOUT out, long long capRef, long long limitRef,
+                                int *pu0, int *pv0) {
   long long err = 0;
   // ---- bridge at t = -inf (_find_bridge, _ckernels.pyx:63-83)
-  int u = nSL - 1, v = nSL;
+  int u = u_init, v = u_init + 1;
   P3 U, V;
   U.x = U.y = U.z = V.x = V.y = V.z = 0.0;
   if (active) {
@@ -173,7 +231,7 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
     V = S.pt(v, pts, zs);
     long long moves = 0;
     for (;;) {
-      const int vn = S.lk[v].y;
+      const int vn = S.LK(v).y;
       if (vn != NIL) {
         const P3 W = S.pt(vn, pts, zs);
         if (turn_xy(U.x, U.y, V.x, V.y, W.x, W.y) < 0.0) {
@@ -183,7 +241,7 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
           continue;
         }
       }
-      const int up = S.lk[u].x;
+      const int up = S.LK(u).x;
       if (up != NIL) {
         const P3 W = S.pt(up, pts, zs);
         if (turn_xy(W.x, W.y, U.x, U.y, V.x, V.y) < 0.0) {
@@ -204,10 +262,10 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
   *pv0 = v;
   int un = NIL, up = NIL, vn = NIL, vp = NIL;
   if (active) {
-    un = S.lk[u].y;
-    up = S.lk[u].x;
-    vn = S.lk[v].y;
-    vp = S.lk[v].x;
+    un = S.LK(u).y;
+    up = S.LK(u).x;
+    vn = S.LK(v).y;
+    vp = S.LK(v).x;
   }
   P3 UN = S.pt(un, pts, zs), UP = S.pt(up, pts, zs), VN = S.pt(vn, pts, zs),
      VP = S.pt(vp, pts, zs);
@@ -220,10 +278,12 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
   Ev cL, cR, nL, nR;
   cL.t = cR.t = nL.t = nR.t = INF;
   if (active) {
-    if (kL > 0) cL = evL[0];
-    if (kL > 1) nL = evL[1];
-    if (kR > 0) cR = evR[0];
-    if (kR > 1) nR = evR[1];
+    if (kL > 0) cL = evL.get(0);
+    if (kR > 0) cR = evR.get(0);
+    if (EIN::kPrefetch) {  // HBM streams: one event of prefetch
+      if (kL > 1) nL = evL.get(1);
+      if (kR > 1) nR = evR.get(1);
+    }
   }
   long long k = 0;
   double tcur = -INF;
@@ -244,7 +304,7 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
     const bool child = left || right;
     const bool b2 = active && which == 2, b3 = active && which == 3;
     const bool b4 = active && which == 4, b5 = active && which == 5;
-    const int off = left ? 0 : nSL;
+    const int off = left ? 0 : roff;
     const int Ea = (left ? cL.a : cR.a) + off, Eb = (left ? cL.b : cR.b) + off,
               Ec = (left ? cL.c : cR.c) + off, Ek = left ? cL.kind : cR.kind;
     // the one link word this step reads: the child event's point, or the
@@ -252,10 +312,10 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
     const int nf = b2 ? un : (b3 ? up : (b4 ? vn : vp));
     const int z = child ? Eb : ((b2 | b3 | b4 | b5) ? nf : 0);
     short2 lz = make_short2(NIL, NIL);
-    if (active) lz = S.lk[z];
+    if (active) lz = S.LK(z);
     const int e = Eb, p = lz.x, q = lz.y;
     bool del = false;
-    if (child && p != NIL) del = S.lk[p].y == e;
+    if (child && p != NIL) del = S.LK(p).y == e;
     if (child && (p != Ea || q != Ec || (del ? EV_DEL : EV_INS) != Ek)) {
       err = E_FASTPATH;
       active = false;
@@ -263,8 +323,8 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
     const bool act = child && active;
     // _act (_ckernels.pyx:49-60) on the child event
     if (act) {
-      S.lk[p].y = static_cast<short>(del ? q : e);
-      S.lk[q].x = static_cast<short>(del ? p : e);
+      S.LK(p).y = static_cast<short>(del ? q : e);
+      S.LK(q).x = static_cast<short>(del ? p : e);
     }
     // the cached neighbour that changes and its new point
     int slot = -1, newpt = NIL;
@@ -293,22 +353,30 @@ __device__ long long merge_tpj2(const TpjSlice<XYZ> &S, bool active, int nSL,
       o.b = eb;
       o.c = ec;
       o.kind = ek;
-      out[k] = o;
-      const unsigned f = S.fi[eb];
+      out.put(k, o);
+      const unsigned f = S.FI(eb);
       if (!(f & FI_EV))
-        S.fi[eb] = f | FI_EV | static_cast<unsigned>(ea) | (static_cast<unsigned>(ec) << 15);
+        S.FI(eb) = f | FI_EV | static_cast<unsigned>(ea) | (static_cast<unsigned>(ec) << 15);
     }
     k += emit;
     // advance the consumed child stream
     if (left) {
-      cL = nL;
       ++i;
-      if (i + 1 < kL) nL = evL[i + 1]; else nL.t = INF;
+      if (EIN::kPrefetch) {
+        cL = nL;
+        if (i + 1 < kL) nL = evL.get(i + 1); else nL.t = INF;
+      } else {
+        if (i < kL) cL = evL.get(i); else cL.t = INF;
+      }
     }
     if (right) {
-      cR = nR;
       ++j;
-      if (j + 1 < kR) nR = evR[j + 1]; else nR.t = INF;
+      if (EIN::kPrefetch) {
+        cR = nR;
+        if (j + 1 < kR) nR = evR.get(j + 1); else nR.t = INF;
+      } else {
+        if (j < kR) cR = evR.get(j); else cR.t = INF;
+      }
     }
     // rotate the bridge neighbourhood (selects), fetch the one new point
     const P3 N = S.pt(slot >= 0 ? newpt : NIL, pts, zs);
@@ -392,6 +460,8 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
                                                  long long n, int level, long long j0,
                                                  long long j1, long long *err, int pool,
                                                  int jpc) {
+  // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
+  if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0)) return;
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   const double zs = blockIdx.y ? -1.0 : 1.0;
@@ -504,8 +574,8 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
     }
   }
   // all 32 lanes enter the sweep together (idle lanes inactive)
-  k = merge_tpj2<XYZ>(S, merge, nSL, pts, zs, in.ev + 2 * L, kL, in.ev + 2 * M, kR,
-                      out.ev + 2 * L, 2 * (R_ - L), R_ - L, &u0, &v0);
+  k = merge_tpj2(S, merge, nSL - 1, nSL, pts, zs, GEvIn{in.ev + 2 * L}, kL, GEvIn{in.ev + 2 * M}, kR,
+                 GEvOut{out.ev + 2 * L}, 2 * (R_ - L), R_ - L, &u0, &v0);
   if (merge && k < 0) {
     raise_err(err, k);
     merge = false;
@@ -582,6 +652,186 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
     evo[e] = o;
   }
   if (__any_sync(FULL, bad) && lane == 0) raise_err(err, E_FASTPATH);
+}
+
+// ------------------------------------------------------------- leaf levels
+// Levels 1..B fused: one LANE owns a block of 2^B consecutive sorted points
+// and runs every merge of levels 1..B inside its block (parallel.py's level
+// loop restricted to the block: the jobs of a level never cross a 2^B
+// boundary), with all state in lane-interleaved shared memory -- points,
+// links, first-event info and two event buffers (8-bit block-local ids).
+// Nothing touches HBM between levels; groups stay uncompacted inside the
+// block (a hidden point is never referenced again), and the level-B group
+// is compacted and written in the compact-group format the per-level
+// kernels read.  Per lane: 32 B per point + 2 x 2 x 12 B event slots.
+template <int B>
+__host__ __device__ constexpr int leaf_lane_bytes() {
+  return (1 << B) * (24 + 4 + 4) + 2 * (2 << B) * 12 + ((1 << B) / 2) * 4;
+}
+
+template <int B>
+__global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restrict__ pts,
+                                                  long long n, long long p0, long long p1,
+                                                  long long *err) {
+  // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
+  if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0)) return;
+  constexpr int NP = 1 << B;
+  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
+  const double zs = blockIdx.y ? -1.0 : 1.0;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  const long long blk = (p0 >> B) + (long long)blockIdx.x * 32 + lane;
+  const long long base = blk << B;
+  const long long top = p1 < n ? p1 : n;
+  const int cnt = base < top ? static_cast<int>((top - base) < NP ? (top - base) : NP) : 0;
+  // lane-interleaved arrays: element i of this lane at [i * 32 + lane]
+  double *X = reinterpret_cast<double *>(smem) + lane;
+  double *Y = X + 32 * NP;
+  double *Z = Y + 32 * NP;
+  double *ET0 = Z + 32 * NP;
+  double *ET1 = ET0 + 32 * 2 * NP;
+  short2 *LK = reinterpret_cast<short2 *>(reinterpret_cast<double *>(smem) + 32 * 7 * NP) + lane;
+  unsigned *FI = reinterpret_cast<unsigned *>(LK - lane + 32 * NP) + lane;
+  unsigned *EW0 = FI + 32 * NP;
+  unsigned *EW1 = EW0 + 32 * 2 * NP;
+  int *KG = reinterpret_cast<int *>(EW1 - lane + 32 * 2 * NP);
+  for (int p = 0; p < NP; ++p) {
+    double x = 0.0, y = 0.0, z = 0.0;
+    if (p < cnt) {
+      const double *q = pts + 3 * (base + p);
+      x = q[0];
+      y = q[1];
+      z = zs * q[2];
+    }
+    X[p * 32] = x;
+    Y[p * 32] = y;
+    Z[p * 32] = z;
+    // level 1: pairs linked (a lone last point is a carry)
+    const bool has_pair = (p ^ 1) < cnt;
+    LK[p * 32] = (p & 1) ? make_short2(has_pair ? p - 1 : NIL, NIL)
+                         : make_short2(NIL, has_pair ? p + 1 : NIL);
+  }
+  for (int g = 0; g < NP / 2; ++g) KG[g * 32 + lane] = 0;
+  TpjSlice<true, 32> S;
+  S.x = X;
+  S.y = Y;
+  S.z = Z;
+  S.lk = LK;
+  S.gd = nullptr;
+  S.fi = FI;
+  bool ok = true;
+  int u0 = 0, v0 = 0;
+  long long kfin = 0;
+  double *ETi = ET0, *ETo = ET1;
+  unsigned *EWi = EW0, *EWo = EW1;
+#pragma unroll 1
+  for (int lv = 2; lv <= B; ++lv) {
+    const int size = 1 << lv, half = size >> 1;
+#pragma unroll 1
+    for (int g = 0; g < NP / size; ++g) {
+      const int L = g * size, M = L + half, R = (L + size < cnt) ? L + size : cnt;
+      const bool merge = ok && R - L > half;
+      const int kL = KG[(2 * g) * 32 + lane], kR = KG[(2 * g + 1) * 32 + lane];
+      if (!merge && L < cnt) {  // carry (copy_log): the short last group
+        for (int e = 0; e < kL; ++e) {
+          ETo[(2 * L + e) * 32] = ETi[(2 * L + e) * 32];
+          EWo[(2 * L + e) * 32] = EWi[(2 * L + e) * 32];
+        }
+      }
+      // block-relative ids throughout (links, events, first-event info)
+      if (merge) {
+        for (int p = L; p < R; ++p) {
+          const int pr = S.LK(p).x;
+          const bool chain = p == L || p == M || (pr != NIL && S.LK(pr).y == p);
+          S.FI(p) = chain ? FI_CHAIN : 0u;
+        }
+      }
+      const long long k = merge_tpj2(
+          S, merge, M - 1, 0, pts, zs, LEvIn{ETi + 2 * L * 32, EWi + 2 * L * 32}, kL,
+          LEvIn{ETi + 2 * M * 32, EWi + 2 * M * 32}, kR, LEvOut{ETo + 2 * L * 32, EWo + 2 * L * 32},
+          2 * (R - L), R - L, &u0, &v0);
+      if (merge && k < 0) {
+        raise_err(err, k);
+        ok = false;
+      }
+      if (merge && ok) {
+        // start-of-time links, no compaction inside the block
+        int last = NIL;
+        for (int p = L; p < R; ++p) {
+          const unsigned f = S.FI(p);
+          const bool chain = (f & FI_CHAIN) && (p < M ? p <= u0 : p >= v0);
+          if (chain) {
+            S.LK(p).x = static_cast<short>(last);
+            if (last != NIL) S.LK(last).y = static_cast<short>(p);
+            last = p;
+          } else if (f & FI_EV) {
+            S.LK(p) = make_short2(static_cast<short>(f & 0x7fff),
+                                  static_cast<short>((f >> 15) & 0x7fff));
+          } else {
+            // hidden from here on: NIL links, so no later chain test can
+            // take a stale link for a chain link (the compact kernels drop
+            // such points instead)
+            S.LK(p) = make_short2(NIL, NIL);
+          }
+          if (lv == B) S.FI(p) = (chain || (f & FI_EV)) ? 1u : 0u;  // keep flag
+        }
+        if (last != NIL) S.LK(last).y = NIL;
+      }
+      KG[g * 32 + lane] = merge ? static_cast<int>(k) : (L < cnt ? kL : 0);
+      kfin = KG[g * 32 + lane];
+    }
+    double *tt = ETi; ETi = ETo; ETo = tt;
+    unsigned *tw = EWi; EWi = EWo; EWo = tw;
+    __syncwarp();
+  }
+  // ---- level-B group: compact (kept = merged -inf chain U logged points)
+  // and write it out; a short last block whose top merge was a carry keeps
+  // the flags of its last merged level
+  if (!ok || cnt == 0) return;
+  const bool top_merged = cnt > NP / 2;
+  if (!top_merged) {
+    // re-derive keep flags: chain membership + logged points of the group
+    for (int p = 0; p < cnt; ++p) FI[p * 32] = 0u;
+    int p = 0;
+    while (p != NIL && p < cnt) {  // -inf chain from point 0
+      FI[p * 32] = 1u;
+      p = LK[p * 32].y;
+    }
+    for (int e = 0; e < kfin; ++e) FI[((EWi[e * 32] >> 8) & 0xff) * 32] = 1u;
+  }
+  int m = 0;
+  for (int p = 0; p < cnt; ++p) {
+    const bool keep = FI[p * 32] != 0u;
+    FI[p * 32] = keep ? static_cast<unsigned>(m++) : FULL;
+  }
+  bool bad = false;
+  for (int p = 0; p < cnt; ++p) {
+    const unsigned id = FI[p * 32];
+    if (id == FULL) continue;
+    const short2 l = LK[p * 32];
+    int2 o;
+    o.x = l.x == NIL ? NIL : static_cast<int>(FI[l.x * 32]);
+    o.y = l.y == NIL ? NIL : static_cast<int>(FI[l.y * 32]);
+    bad |= (o.x == -1 && l.x != NIL) | (o.y == -1 && l.y != NIL);
+    out.lnk[base + id] = o;
+    out.gid[base + id] = static_cast<int>(base + p);
+  }
+  Ev *evo = out.ev + 2 * base;
+  for (int e = 0; e < kfin; ++e) {
+    const unsigned w = EWi[e * 32];
+    Ev o;
+    o.t = ETi[e * 32];
+    const unsigned na = FI[(w & 0xff) * 32], nb = FI[((w >> 8) & 0xff) * 32],
+                   nc = FI[((w >> 16) & 0xff) * 32];
+    bad |= (na == FULL) | (nb == FULL) | (nc == FULL);
+    o.a = static_cast<int>(na);
+    o.b = static_cast<int>(nb);
+    o.c = static_cast<int>(nc);
+    o.kind = static_cast<int>(w >> 24);
+    evo[e] = o;
+  }
+  out.hdr[blk] = make_int2(m, static_cast<int>(kfin));
+  if (bad) raise_err(err, E_FASTPATH);
 }
 
 // -------------------------------------------------------------- warp merge
@@ -912,6 +1162,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, const double 
                                                           long long *err, int pool,
                                                           Ev *gseq0, Ev *gseq1, Rec *grec0,
                                                           Rec *grec1) {
+  // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
+  if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0)) return;
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   Ev *gseq = blockIdx.y ? gseq1 : gseq0;
@@ -1071,6 +1323,7 @@ bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
 }
 
 bool g_attr_done = false;
+int g_leaf_b = 3;  // H3D_LEAF_B: levels 1..B fused (0 = off)
 
 template <bool XYZ>
 void launch_tpj(dim3 grid, int pool, int jpc, cudaStream_t s, Pass2 P, const double *pts,
@@ -1122,6 +1375,15 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     if (const char *e = getenv("H3D_TPJ_MAX_LEVEL")) kTpjMaxLevel = atoi(e);
     if (const char *e = getenv("H3D_TPJ_XYZ_KB")) kTpjXyzMax = atoll(e) * 1024;
     if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinTotalJobs = atoll(e);
+    if (const char *e = getenv("H3D_LEAF_B")) g_leaf_b = atoi(e);
+    if (g_leaf_b > 5) g_leaf_b = 5;
+    if (h3d_check(cudaFuncSetAttribute(k_fast_leaf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       32 * leaf_lane_bytes<3>())) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_leaf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       32 * leaf_lane_bytes<4>())) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_leaf<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       32 * leaf_lane_bytes<5>())))
+      return H3D_E_CUDA;
     g_attr_done = true;
   }
   long long *err = reinterpret_cast<long long *>(err_dev);
@@ -1131,7 +1393,31 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   // level l reads buffer (l-1)&1 and writes buffer l&1 (A = 0, B = 1)
   Pass2 P = (lv_lo & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
   int lv = lv_lo;
-  if (lv_lo == 1) {  // level 1 written directly (no coordinates needed)
+  const int NPB = 1 << g_leaf_b;
+  if (lv_lo == 1 && g_leaf_b >= 2 && lv_hi >= g_leaf_b && (p0 & (NPB - 1)) == 0) {
+    // levels 1..B fused in shared memory, one lane per 2^B-point block
+    const long long blocks = (p1 - p0 + NPB - 1) / NPB;
+    void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
+    h3d_count_launches(1);
+    const dim3 grid(h3d_grid(blocks, 32), 2);
+    // level B's groups go to buffer B&1
+    const Pass2 LP = (g_leaf_b & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
+    switch (g_leaf_b) {
+      case 3:
+        k_fast_leaf<3><<<grid, 32, 32 * leaf_lane_bytes<3>(), s>>>(LP, sorted_pts, n, p0, p1, err);
+        break;
+      case 4:
+        k_fast_leaf<4><<<grid, 32, 32 * leaf_lane_bytes<4>(), s>>>(LP, sorted_pts, n, p0, p1, err);
+        break;
+      default:
+        k_fast_leaf<5><<<grid, 32, 32 * leaf_lane_bytes<5>(), s>>>(LP, sorted_pts, n, p0, p1, err);
+        break;
+    }
+    h3d_prof_end(e0, 3000 + g_leaf_b, 2, s);
+    // the leaf writes level B's groups into buffer B&1
+    P = (g_leaf_b & 1) ? Pass2{w0.B, w1.B, w0.A, w1.A} : Pass2{w0.A, w1.A, w0.B, w1.B};
+    lv = g_leaf_b + 1;
+  } else if (lv_lo == 1) {  // level 1 written directly (no coordinates needed)
     const long long j0 = p0 >> 1, j1 = (p1 + 1) >> 1;
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
     h3d_count_launches(1);

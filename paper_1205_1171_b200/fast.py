@@ -49,6 +49,8 @@ def profile_enable(on: bool) -> None:
 
 def kernel_of(tag: int):
     """Decode a profile row's level tag -> (kernel name, level)."""
+    if tag >= 3000:
+        return "k_fast_leaf", -(tag - 3000)
     if tag >= 2000:
         return "k_fast_init1", tag - 2000
     if tag >= 1000:
