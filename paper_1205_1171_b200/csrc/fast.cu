@@ -36,42 +36,6 @@
 
 namespace h3d {
 
-struct GroupBuf {
-  int2 *hdr;  // (nS, k) per group
-  int2 *lnk;  // start-of-time links (group-local ids) per kept point
-  int *gid;   // global sorted index per kept point
-  Ev *ev;     // events, 2 slots per point
-};
-
-// both passes of a level in one launch: blockIdx.y = 0 lower, 1 upper
-struct Pass2 {
-  GroupBuf in0, in1, out0, out1;
-};
-
-constexpr unsigned FULL = 0xffffffffu;
-constexpr int FIRST_FLAG = 1 << 30;        // "on a child's -inf chain"
-constexpr int FIRST_NONE = FIRST_FLAG - 1; // no event yet
-
-__host__ __device__ __forceinline__ long long align8(long long b) { return (b + 7) & ~7ll; }
-__host__ __device__ __forceinline__ long long align16(long long b) { return (b + 15) & ~15ll; }
-
-// coordinates of sorted point g; z negated on the upper pass (exact)
-struct P3 {
-  double x, y, z;
-};
-__device__ __forceinline__ P3 load_pt(const double *__restrict__ pts, int g, double zs) {
-  P3 r;
-  r.x = __ldg(pts + 3ll * g);
-  r.y = __ldg(pts + 3ll * g + 1);
-  r.z = zs * __ldg(pts + 3ll * g + 2);
-  return r;
-}
-
-__device__ __forceinline__ double evt3(int a, int b, int c, const P3 &A, const P3 &B, const P3 &C) {
-  if (a == NIL || b == NIL || c == NIL) return INF;
-  return evtime_xyz(A.x, A.y, A.z, B.x, B.y, B.z, C.x, C.y, C.z);
-}
-
 // ----------------------------------------------------------- level 1 init
 // Level 1 merges two one-point groups: the bridge walk stops at once (both
 // feet have NIL neighbours), no event can occur and the stitch links the
@@ -411,7 +375,8 @@ __host__ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
 // Shared-memory need of the thread-per-job launch, for every jobs-per-CTA
 // choice at once: out[r] = max over CTAs of sum(nS) when a CTA takes
 // 32 >> r consecutive jobs (r = 0..5); out[6] = largest single nS; out[7] =
-// largest shared-memory need of one warp-per-job merge.  One warp per 32
+// largest shared-memory need of one warp-per-job merge; out[8] = largest
+// merged child log of one job.  One warp per 32
 // jobs, coalesced header reads.
 __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1,
                            unsigned long long *out) {
@@ -420,22 +385,24 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long chunks = (j1 - j0 + 31) >> 5;
-  unsigned long long mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long mx[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (long long c = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
     const long long j = j0 + c * 32 + lane;
-    unsigned long long nS = 0, wb = 0;
+    unsigned long long nS = 0, wb = 0, kin = 0;
     if (j < j1) {
       const long long L = j << level;
       const long long R_ = (L + size < n) ? L + size : n;
       if (R_ - L > half) {
         const int2 hl = in.hdr[2 * j], hr = in.hdr[2 * j + 1];
         nS = hl.x + hr.x;
+        kin = hl.y + hr.y;
         wb = warp_job_bytes(static_cast<int>(nS), hl.y + hr.y);
       }
     }
     mx[6] = nS > mx[6] ? nS : mx[6];
     mx[7] = wb > mx[7] ? wb : mx[7];
+    mx[8] = kin > mx[8] ? kin : mx[8];
     unsigned long long t = nS;
     mx[5] = t > mx[5] ? t : mx[5];  // 1 job per CTA
 #pragma unroll
@@ -445,7 +412,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
     }
   }
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < 9; ++r) {
     unsigned long long m = mx[r];
     for (int o = 16; o; o >>= 1) {
       const unsigned long long x = __shfl_xor_sync(FULL, m, o);
@@ -1301,26 +1268,7 @@ long long kTpjMinTotalJobs = 148 * 32;  // H3D_TPJ_MIN_JOBS (both passes)
 constexpr int kTpjPool = 200 * 1024;
 int kTpjMaxLevel = 40;          // H3D_TPJ_MAX_LEVEL
 long long kTpjXyzMax = 16 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the pool fits
-
-struct PassWS {
-  GroupBuf A, B;
-  Ev *seq;                  // merged child events of HBM-resident warp jobs (2n)
-  Rec *rec;                 // records of HBM-resident warp jobs (n)
-  unsigned long long *need; // thread-per-job pool sizing
-};
-
-bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
-  for (GroupBuf *g : {&w.A, &w.B}) {
-    g->hdr = ar.take<int2>(n);
-    g->lnk = ar.take<int2>(n);
-    g->gid = ar.take<int>(n);
-    g->ev = ar.take<Ev>(2 * n);
-  }
-  w.seq = ar.take<Ev>(2 * n);
-  w.rec = ar.take<Rec>(n);
-  w.need = ar.take<unsigned long long>(8);
-  return ar.base == nullptr || w.need != nullptr;
-}
+long long kBigKin = 512;           // H3D_BIG_KIN: time-split pipeline from this job log size
 
 bool g_attr_done = false;
 int g_leaf_b = 3;  // H3D_LEAF_B: levels 1..B fused (0 = off)
@@ -1346,12 +1294,16 @@ int64_t h3d_fast_layout(int64_t n, int64_t *offsets) {
   return 0;
 }
 
-size_t h3d_fast_pass_workspace_bytes(int64_t n) {  // per pass
-  if (n < 1) n = 1;
+static size_t base_pass_bytes(long long n) {
   h3d_arena ar(nullptr, 0);
   PassWS w;
   carve_pass(ar, n, w);
-  return ar.used + 4096;
+  return (ar.used + 4095) & ~size_t(4095);
+}
+
+size_t h3d_fast_pass_workspace_bytes(int64_t n) {  // per pass (+ the big-job scratch)
+  if (n < 1) n = 1;
+  return base_pass_bytes(n) + big_workspace_bytes(big_capacity(n)) + 4096;
 }
 
 int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, int64_t p1,
@@ -1364,6 +1316,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   h3d_arena a0(ws_lower, workspace_bytes), a1(ws_upper, workspace_bytes);
   PassWS w0, w1;
   if (!carve_pass(a0, n, w0) || !carve_pass(a1, n, w1)) return H3D_E_ARG;
+  // the big-job scratch lives after the lower pass's arrays
+  const size_t bb = base_pass_bytes(n);
+  void *big_ws = workspace_bytes > bb ? static_cast<char *>(ws_lower) + bb : nullptr;
+  const size_t big_bytes = workspace_bytes > bb ? workspace_bytes - bb : 0;
   if (!g_attr_done) {
     if (h3d_check(cudaFuncSetAttribute(k_fast_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kWarpPoolMax))) ||
@@ -1376,6 +1332,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     if (const char *e = getenv("H3D_TPJ_XYZ_KB")) kTpjXyzMax = atoll(e) * 1024;
     if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinTotalJobs = atoll(e);
     if (const char *e = getenv("H3D_LEAF_B")) g_leaf_b = atoi(e);
+    if (const char *e = getenv("H3D_BIG_KIN")) kBigKin = atoll(e);
     if (g_leaf_b > 5) g_leaf_b = 5;
     if (h3d_check(cudaFuncSetAttribute(k_fast_leaf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        32 * leaf_lane_bytes<3>())) ||
@@ -1438,15 +1395,25 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     // they fit a shared-memory slice (int16 local ids); one warp per job
     // (1-warp CTAs, pool = the largest job's need, HBM mode above it) for
     // the few-job levels.
-    cudaMemsetAsync(w0.need, 0, 8 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(w0.need, 0, 9 * sizeof(unsigned long long), s);
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
     k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 4096 ? 4096 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
         P, n, lv, j0, j1, w0.need);
-    unsigned long long need[8];
+    unsigned long long need[9];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
+    // large merge jobs: the time-split pipeline (big.cu)
+    if (static_cast<long long>(need[8]) >= kBigKin && big_ws) {
+      const long long rb = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s);
+      if (rb < 0) return rb;
+      if (rb == 0) {
+        h3d_prof_end(e0, lv + 4000, 2, s);
+        P = Pass2{P.out0, P.out1, P.in0, P.in1};
+        continue;
+      }
+    }
     bool tpj = lv <= kTpjMaxLevel && 2 * jobs >= kTpjMinTotalJobs && need[6] < 0x7fff;
     int jpc = 32;
     bool xyz = false;

@@ -35,6 +35,42 @@ struct __align__(8) Ev {
 static_assert(sizeof(Rec) == 32, "Rec must be one 32-byte sector");
 static_assert(sizeof(Ev) == 24, "Ev is 24 bytes");
 
+struct GroupBuf {
+  int2 *hdr;  // (nS, k) per group
+  int2 *lnk;  // start-of-time links (group-local ids) per kept point
+  int *gid;   // global sorted index per kept point
+  Ev *ev;     // events, 2 slots per point
+};
+
+// both passes of a level in one launch: blockIdx.y = 0 lower, 1 upper
+struct Pass2 {
+  GroupBuf in0, in1, out0, out1;
+};
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int FIRST_FLAG = 1 << 30;        // "on a child's -inf chain"
+constexpr int FIRST_NONE = FIRST_FLAG - 1; // no event yet
+
+__host__ __device__ __forceinline__ long long align8(long long b) { return (b + 7) & ~7ll; }
+__host__ __device__ __forceinline__ long long align16(long long b) { return (b + 15) & ~15ll; }
+
+// coordinates of sorted point g; z negated on the upper pass (exact)
+struct P3 {
+  double x, y, z;
+};
+__device__ __forceinline__ P3 load_pt(const double *__restrict__ pts, int g, double zs) {
+  P3 r;
+  r.x = __ldg(pts + 3ll * g);
+  r.y = __ldg(pts + 3ll * g + 1);
+  r.z = zs * __ldg(pts + 3ll * g + 2);
+  return r;
+}
+
+__device__ __forceinline__ double evt3(int a, int b, int c, const P3 &A, const P3 &B, const P3 &C) {
+  if (a == NIL || b == NIL || c == NIL) return INF;
+  return evtime_xyz(A.x, A.y, A.z, B.x, B.y, B.z, C.x, C.y, C.z);
+}
+
 constexpr int EV_INS = 0;
 constexpr int EV_DEL = 1;
 
@@ -87,5 +123,45 @@ __device__ __forceinline__ int bridge_rec(const Rec *R, int *pu, int *pv, long l
     if (++moves > limit) return -1;
   }
 }
+
+}  // namespace h3d
+
+// ---------------------------------------------------------------- host side
+#include "h3d_host.h"
+
+namespace h3d {
+
+struct PassWS {
+  GroupBuf A, B;
+  Ev *seq;                  // merged child events of HBM-resident warp jobs (2n)
+  Rec *rec;                 // records of HBM-resident warp jobs (n)
+  unsigned long long *need; // thread-per-job pool sizing
+};
+
+inline bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
+  for (GroupBuf *g : {&w.A, &w.B}) {
+    g->hdr = ar.take<int2>(n);
+    g->lnk = ar.take<int2>(n);
+    g->gid = ar.take<int>(n);
+    g->ev = ar.take<Ev>(2 * n);
+  }
+  w.seq = ar.take<Ev>(2 * n);
+  w.rec = ar.take<Rec>(n);
+  w.need = ar.take<unsigned long long>(16);
+  return ar.base == nullptr || w.need != nullptr;
+}
+
+
+// Scratch of the time-split pipeline for large merge jobs (big.cu), carved
+// from the lower pass's workspace; sized for m points (sum of group sizes
+// of a level, both passes) -- levels above that use the warp kernel.
+struct BigWS;
+size_t big_workspace_bytes(long long m);
+long long big_capacity(long long n);
+// one merge level of both passes through the pipeline; returns 0, or 1 when
+// the level does not fit the scratch (caller falls back), or a negative code
+long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double *pts,
+                    long long n, int lv, long long j0, long long j1, long long *err,
+                    cudaStream_t s);
 
 }  // namespace h3d

@@ -49,6 +49,8 @@ def profile_enable(on: bool) -> None:
 
 def kernel_of(tag: int):
     """Decode a profile row's level tag -> (kernel name, level)."""
+    if tag >= 4000:
+        return "k_big_level", tag - 4000
     if tag >= 3000:
         return "k_fast_leaf", -(tag - 3000)
     if tag >= 2000:
