@@ -505,27 +505,51 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
       if (pre[jj + st] <= x) jj += st;
     return jj;
   };
-  // ---- stage (cooperative, coalesced)
-  for (int x = lane; x < tot_pts; x += 32) {
-    const int jj = job_of(s_pre, x);
-    const int p = x - s_pre[jj];
-    const int m_nS = s_pre[jj + 1] - s_pre[jj], m_nSL = s_nSL[jj];
-    const TpjSlice<XYZ> S(smem + s_off[jj], m_nS);
-    const bool left = p < m_nSL;
-    const long long src = left ? s_L[jj] + p : s_M[jj] + (p - m_nSL);
-    int2 l = in.lnk[src];
-    const int g = in.gid[src];
-    if (!left) {
-      if (l.x != NIL) l.x += m_nSL;
-      if (l.y != NIL) l.y += m_nSL;
+  // ---- stage (cooperative, coalesced; U elements per lane in flight)
+  constexpr int U = 4;
+  for (int x0 = 0; x0 < tot_pts; x0 += 32 * U) {
+    int jj[U], p[U];
+    long long src[U];
+    int2 l[U];
+    int g[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int x = x0 + q * 32 + lane;
+      jj[q] = job_of(s_pre, x < tot_pts ? x : tot_pts - 1);
+      p[q] = x - s_pre[jj[q]];
+      const int m_nSL = s_nSL[jj[q]];
+      src[q] = p[q] < m_nSL ? s_L[jj[q]] + p[q] : s_M[jj[q]] + (p[q] - m_nSL);
     }
-    S.lk[p] = make_short2(static_cast<short>(l.x), static_cast<short>(l.y));
-    S.gd[p] = g;
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      if (x0 + q * 32 + lane < tot_pts) {
+        l[q] = in.lnk[src[q]];
+        g[q] = in.gid[src[q]];
+      }
+    }
+    P3 c[U];
     if (XYZ) {
-      const P3 c = load_pt(pts, g, zs);
-      S.x[p] = c.x;
-      S.y[p] = c.y;
-      S.z[p] = c.z;
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+        if (x0 + q * 32 + lane < tot_pts) c[q] = load_pt(pts, g[q], zs);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      if (x0 + q * 32 + lane >= tot_pts) continue;
+      const int m_nS = s_pre[jj[q] + 1] - s_pre[jj[q]], m_nSL = s_nSL[jj[q]];
+      const TpjSlice<XYZ> S(smem + s_off[jj[q]], m_nS);
+      int2 lq = l[q];
+      if (p[q] >= m_nSL) {
+        if (lq.x != NIL) lq.x += m_nSL;
+        if (lq.y != NIL) lq.y += m_nSL;
+      }
+      S.lk[p[q]] = make_short2(static_cast<short>(lq.x), static_cast<short>(lq.y));
+      S.gd[p[q]] = g[q];
+      if (XYZ) {
+        S.x[p[q]] = c[q].x;
+        S.y[p[q]] = c[q].y;
+        S.z[p[q]] = c[q].z;
+      }
     }
   }
   __syncwarp();
@@ -1398,7 +1422,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     cudaMemsetAsync(w0.need, 0, 9 * sizeof(unsigned long long), s);
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
-    k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 4096 ? 4096 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
+    k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 65535 ? 65535 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
         P, n, lv, j0, j1, w0.need);
     unsigned long long need[9];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||

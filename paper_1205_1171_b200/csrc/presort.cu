@@ -115,7 +115,7 @@ __device__ __forceinline__ void cross3(double a0, double a1, double a2, double b
 // stage 1: first j >= 1 with |cross(p_i - p0, p_j - p0)| > tol*scale*scale
 // stage 2: first k >= 1 with |(p_k - p0) . normal| > tol*scale*|normal|
 __global__ void k_degenerate(const double *__restrict__ P, long long n, ScanState *st,
-                             int stage) {
+                             int stage, long long r0, long long r1) {
   const double tol = 1e-9;
   double scale = __longlong_as_double(static_cast<long long>(st->scale_bits));
   if (scale < 1e-30) scale = 1e-30;
@@ -140,7 +140,10 @@ __global__ void k_degenerate(const double *__restrict__ P, long long n, ScanStat
     thr = __dmul_rn(__dmul_rn(tol, scale), norm3(nrm[0], nrm[1], nrm[2]));
   }
   long long *slot = stage == 0 ? &st->i : (stage == 1 ? &st->j : &st->k);
-  for (long long r = 1 + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+  // rows [r0, r1): a later range only matters when no earlier row hit
+  if (*reinterpret_cast<volatile long long *>(slot) != none) return;
+  if (r1 > n) r1 = n;
+  for (long long r = r0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < r1;
        r += (long long)gridDim.x * blockDim.x) {
     if (r > *reinterpret_cast<volatile long long *>(slot)) return;
     const double dx = __dsub_rn(P[3 * r], x0), dy = __dsub_rn(P[3 * r + 1], y0),
@@ -395,8 +398,14 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   k_scan_init<<<1, 1, 0, s>>>(w.scan);
   h3d_count_launches(1);
   k_absmax<<<G, 256, 0, s>>>(sorted_pts, 3 * n, &w.scan->scale_bits);
-  h3d_count_launches(3);
-  for (int stage = 0; stage < 3; ++stage) k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage);
+  // each stage scans the first 16K rows with a small grid and the rest only
+  // when they hold no hit (random inputs stop in the first block, as the
+  // reference's block-wise scan does)
+  h3d_count_launches(6);
+  for (int stage = 0; stage < 3; ++stage) {
+    k_degenerate<<<64, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, 16384);
+    k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 16384, n);
+  }
   ScanState hs;
   int tie2 = 0;
   if (h3d_check(cudaMemcpyAsync(&hs, w.scan, sizeof(hs), cudaMemcpyDeviceToHost, s)) ||
