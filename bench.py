@@ -240,6 +240,39 @@ def level_bytes(cfg: str):
     return out
 
 
+# bench kernel names -> the ncu kernel names they cover
+NCU_NAMES = {
+    "k_fast_tpj": ("h3d::k_fast_tpj<",),
+    "k_fast_warp": ("h3d::k_fast_warp<",),
+    "k_fast_leaf": ("h3d::k_fast_leaf<",),
+    "k_fast_init1": ("h3d::k_fast_init1",),
+    "k_big_level": ("h3d::k_big_",),
+}
+
+
+def measured_traffic(cfg: str, name: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of the kernel, from the committed ncu launch list of this config
+    (profiles/r1_ncu_launches_<cfg>.json, made by tools/profile_round.sh +
+    tools/ncu_summary.py).  A big-level "launch" is the pipeline's kernels of
+    one level; it is counted per level."""
+    p = os.path.join(ROOT, "profiles", f"r1_ncu_launches_{cfg.lower()}.json")
+    if not os.path.exists(p):
+        return None, None
+    doc = json.load(open(p))
+    pre = NCU_NAMES.get(name, (name,))
+    ks = [k for k in doc["kernels"] if k["kernel"].startswith(pre)]
+    if not ks:
+        return None, None
+    total = sum(k["dram_bytes"] for k in ks)
+    if name == "k_big_level":
+        levels = sum(1 for x in doc["sequence"] if x["kernel"] == "h3d::k_big_jobs")
+        per = total // max(levels, 1)
+    else:
+        per = total // max(sum(k["launches"] for k in ks), 1)
+    return per, os.path.relpath(p, ROOT)
+
+
 def run_ours(args):
     import torch
 
@@ -303,8 +336,13 @@ def run_ours(args):
     if per_kernel:
         name, d = max(per_kernel.items(), key=lambda kv: kv[1]["time"])
         ach = d["bytes"] / d["time"] / 1e9 if d["known"] and d["time"] > 0 else None
+        nl = max(d["launches"], 1)
+        traffic, tsrc = measured_traffic(args.config, name)
         roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": None,
+                "frac": (ach / peak) if ach else None,
+                "traffic": traffic,
+                "traffic_source": tsrc,
+                "algorithmic_bytes_per_launch": d["bytes"] // nl,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "launches_per_step": d["launches"] // args.steps,
                 "kernel_ms_per_step": d["time"] * 1e3 / args.steps,

@@ -155,7 +155,10 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
                          size_t workspace_bytes, void *stream);
 
 /* bytes of workspace one h3d_fast_pass needs for n points (two compact
- * group buffers: headers, int2 links, ids, 24-byte events; HBM scratch) */
+ * group buffers: headers, int2 links, ids, 24-byte events; HBM scratch of
+ * the warp merge; and, in the lower pass's workspace, the scratch of the
+ * time-split pipeline for large merge jobs, sized for min(n, 2^21) points
+ * per pass -- levels beyond it fall back to the warp merge) */
 size_t h3d_fast_pass_workspace_bytes(int64_t n);
 
 /* Both hull passes (build_movie, pkg/src/hull3d/parallel.py:68-112) over the
