@@ -154,6 +154,14 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
                          int64_t *vertices, void *workspace,
                          size_t workspace_bytes, void *stream);
 
+/* Routing knobs of the fast path (not a reference interface; used by the
+ * tests to drive every kernel route and by tuning sweeps): "big_kin"
+ * (time-split pipeline from this merged child log size), "leaf_b" (levels
+ * 1..B fused, 0..4), "tpj_min_jobs", "tpj_xyz_kb", "tpj_max_level".  value
+ * < 0 only queries.  Returns the previous value, or -1 for an unknown name.
+ * Environment variables H3D_BIG_KIN, H3D_LEAF_B, ... set the defaults. */
+int64_t h3d_tune(const char *name, int64_t value);
+
 /* bytes of workspace one h3d_fast_pass needs for n points (two compact
  * group buffers: headers, int2 links, ids, 24-byte events; HBM scratch of
  * the warp merge; and, in the lower pass's workspace, the scratch of the

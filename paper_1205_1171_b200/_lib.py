@@ -33,6 +33,7 @@ SIGNATURES: dict[str, tuple] = {
     "h3d_fast_passes_range": (i64, [vp, i64, i64, i64, ctypes.c_int32, ctypes.c_int32, vp, vp,
                                     sz, vp, ctypes.c_int32, vp]),
     "h3d_fast_layout": (i64, [i64, vp]),
+    "h3d_tune": (i64, [ctypes.c_char_p, i64]),
     "h3d_fast_extract": (i64, [vp, vp, i64, i64, i64, vp, i64, vp, vp, vp]),
     "h3d_seam_act": (i64, [vp, i64, vp]),
     "h3d_seam_init_base_logs": (i64, [vp, vp, i64, vp]),

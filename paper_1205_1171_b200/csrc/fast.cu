@@ -27,6 +27,7 @@
 // point's gid and kernels read the sorted point array (z negated on the
 // upper pass).
 #include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include <cub/cub.cuh>
@@ -1295,7 +1296,20 @@ long long kTpjXyzMax = 16 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the
 long long kBigKin = 512;           // H3D_BIG_KIN: time-split pipeline from this job log size
 
 bool g_attr_done = false;
+bool g_env_done = false;
 int g_leaf_b = 3;  // H3D_LEAF_B: levels 1..B fused (0 = off)
+
+// tuning knobs from the environment (read once; h3d_tune overrides)
+void load_env_once() {
+  if (g_env_done) return;
+  g_env_done = true;
+  if (const char *e = getenv("H3D_TPJ_MAX_LEVEL")) kTpjMaxLevel = atoi(e);
+  if (const char *e = getenv("H3D_TPJ_XYZ_KB")) kTpjXyzMax = atoll(e) * 1024;
+  if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinTotalJobs = atoll(e);
+  if (const char *e = getenv("H3D_LEAF_B")) g_leaf_b = atoi(e);
+  if (const char *e = getenv("H3D_BIG_KIN")) kBigKin = atoll(e);
+  if (g_leaf_b > 4) g_leaf_b = 4;
+}
 
 template <bool XYZ>
 void launch_tpj(dim3 grid, int pool, int jpc, cudaStream_t s, Pass2 P, const double *pts,
@@ -1306,6 +1320,18 @@ void launch_tpj(dim3 grid, int pool, int jpc, cudaStream_t s, Pass2 P, const dou
 }  // namespace
 
 extern "C" {
+
+int64_t h3d_tune(const char *name, int64_t value) {
+  load_env_once();
+  const std::string k(name ? name : "");
+  long long old = -1;
+  if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
+  else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = value > 4 ? 4 : static_cast<int>(value); }
+  else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
+  else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
+  else if (k == "tpj_max_level") { old = kTpjMaxLevel; if (value >= 0) kTpjMaxLevel = static_cast<int>(value); }
+  return old;
+}
 
 int64_t h3d_fast_layout(int64_t n, int64_t *offsets) {
   // byte offsets of A.hdr, A.lnk, A.gid, A.ev, B.hdr, B.lnk, B.gid, B.ev, seq
@@ -1352,12 +1378,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         h3d_check(cudaFuncSetAttribute(k_fast_tpj<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)))
       return H3D_E_CUDA;
-    if (const char *e = getenv("H3D_TPJ_MAX_LEVEL")) kTpjMaxLevel = atoi(e);
-    if (const char *e = getenv("H3D_TPJ_XYZ_KB")) kTpjXyzMax = atoll(e) * 1024;
-    if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinTotalJobs = atoll(e);
-    if (const char *e = getenv("H3D_LEAF_B")) g_leaf_b = atoi(e);
-    if (const char *e = getenv("H3D_BIG_KIN")) kBigKin = atoll(e);
-    if (g_leaf_b > 5) g_leaf_b = 5;
+    load_env_once();
     if (h3d_check(cudaFuncSetAttribute(k_fast_leaf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        32 * leaf_lane_bytes<3>())) ||
         h3d_check(cudaFuncSetAttribute(k_fast_leaf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -43,6 +43,34 @@ class _WS:
         return buf
 
 
+def tune(name: str, value: int = -1) -> int:
+    """Set (value >= 0) or query a routing knob of the fast path; returns the
+    previous value (csrc/fast.cu h3d_tune)."""
+    r = int(_lib.load().h3d_tune(name.encode(), int(value)))
+    if r < 0:
+        raise KeyError(name)
+    return r
+
+
+class tuned:
+    """Context manager: temporarily set routing knobs, e.g.
+    ``with fast.tuned(big_kin=16): ...``"""
+
+    def __init__(self, **kv):
+        self.kv = kv
+        self.old: dict = {}
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            self.old[k] = tune(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            tune(k, v)
+        return False
+
+
 def profile_enable(on: bool) -> None:
     _lib.load().h3d_profile_enable(1 if on else 0)
 

@@ -1,0 +1,70 @@
+"""Every kernel route of the fused fast path, forced on its own through the
+routing knobs (csrc/fast.cu h3d_tune), reproduces the C oracle's faces bit
+for bit with no exact-engine fallback:
+
+* leaf kernel depth 0 / 3 / 4 (levels 1..B fused in shared memory);
+* the time-split pipeline (big.cu) on almost every level (big_kin=16);
+* lane-per-job on every level (tpj_min_jobs=1, pipeline off);
+* warp-per-job on every level (tpj_min_jobs huge, pipeline off).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1205_1171_b200 as H
+from paper_1205_1171_b200 import fast
+from paper_1205_1171_b200.generators import generate, integer_cloud
+
+pytestmark = pytest.mark.gpu
+
+BIG_OFF = 1 << 40
+ROUTES = {
+    "default": {},
+    "no_leaf_no_big": {"leaf_b": 0, "big_kin": BIG_OFF},
+    "leaf4": {"leaf_b": 4},
+    "big_everywhere": {"big_kin": 16},
+    "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0},
+    "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF},
+    "warp_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0},
+}
+CLOUDS = [("ball", 3001), ("sphere", 20000), ("cube", 65537), ("gauss", 9999), ("sphere", 4097)]
+
+
+@pytest.fixture(scope="module")
+def expected(oracle_mod):
+    out = {}
+    for dist, n in CLOUDS:
+        pts = generate(n, dist, n % 13)
+        out[(dist, n)] = (pts, oracle_mod.convex_hull_3d(pts))
+    return out
+
+
+@pytest.mark.parametrize("route", sorted(ROUTES))
+def test_route_matches_oracle(route, expected):
+    with fast.tuned(**ROUTES[route]):
+        for (dist, n), (pts, exp) in expected.items():
+            before = fast.FALLBACKS[0]
+            r = H.convex_hull_3d(pts)
+            assert fast.FALLBACKS[0] == before, (route, dist, n, fast.LAST_ERROR[0])
+            assert np.array_equal(r.faces, exp.faces), (route, dist, n)
+            assert np.array_equal(r.vertices, exp.vertices), (route, dist, n)
+
+
+def test_integer_cloud_pipeline(oracle_mod):
+    """Integer coordinates take the tie/perturbation path; the pipeline must
+    still agree with the oracle (or hand the input to the exact engine, which
+    then agrees)."""
+    pts = integer_cloud(50000, 3)
+    exp = oracle_mod.convex_hull_3d(pts)
+    with fast.tuned(big_kin=16):
+        r = H.convex_hull_3d(pts)
+    assert np.array_equal(r.faces, exp.faces)
+
+
+def test_tune_roundtrip():
+    old = fast.tune("big_kin", 1234)
+    assert fast.tune("big_kin", old) == 1234
+    with pytest.raises(KeyError):
+        fast.tune("no_such_knob")
