@@ -156,7 +156,8 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
 
 /* Routing knobs of the fast path (not a reference interface; used by the
  * tests to drive every kernel route and by tuning sweeps): "big_kin"
- * (time-split pipeline from this merged child log size), "leaf_b" (levels
+ * (time-split pipeline from this merged child log size), "big_total" (or
+ * half that log size with this many child events in the level), "leaf_b" (levels
  * 1..B fused, 0..4), "tpj_min_jobs", "tpj_xyz_kb", "tpj_max_level".  value
  * < 0 only queries.  Returns the previous value, or -1 for an unknown name.
  * Environment variables H3D_BIG_KIN, H3D_LEAF_B, ... set the defaults. */

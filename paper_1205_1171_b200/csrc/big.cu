@@ -51,6 +51,27 @@ struct BEv {  // a bridge event and the feet after it
   int u, v;
 };
 
+constexpr unsigned long long LS_MASK = (1ull << 22) - 1;
+constexpr unsigned long long LS_HP = 1ull << 44, LS_HN = 1ull << 45, LS_HEAD = 1ull << 46;
+
+__host__ __device__ __forceinline__ unsigned long long ls_pack(int prv, int nxt, bool hp, bool hn,
+                                                               bool head) {
+  return (static_cast<unsigned long long>(prv) & LS_MASK) |
+         ((static_cast<unsigned long long>(nxt) & LS_MASK) << 22) | (hp ? LS_HP : 0ull) |
+         (hn ? LS_HN : 0ull) | (head ? LS_HEAD : 0ull);
+}
+
+struct LinkScanOp {
+  __host__ __device__ __forceinline__ unsigned long long operator()(unsigned long long a,
+                                                                    unsigned long long b) const {
+    if (b & LS_HEAD) return b;
+    unsigned long long r = a;  // keeps a's head flag
+    if (b & LS_HP) r = (r & ~LS_MASK) | (b & LS_MASK) | LS_HP;
+    if (b & LS_HN) r = (r & ~(LS_MASK << 22)) | (b & (LS_MASK << 22)) | LS_HN;
+    return r;
+  }
+};
+
 struct BigWS {
   // per job (both passes, pass-major): J2 = 2 * jobs
   int *jkin, *jkinoff;   // child events of S, exclusive scan
@@ -65,6 +86,7 @@ struct BigWS {
   // incidences (3 per event)
   unsigned *k0, *k1, *v0, *v1;
   IncE *inc;
+  unsigned long long *sc0, *sc1;  // segmented link scan (in, out)
   // per point (compact)
   int *ibeg, *iend;
   int *first, *keep, *newid;
@@ -109,6 +131,8 @@ static bool carve_big(h3d_arena &ar, long long m, BigWS &b) {
   b.v0 = ar.take<unsigned>(3 * EK);
   b.v1 = ar.take<unsigned>(3 * EK);
   b.inc = ar.take<IncE>(3 * EK);
+  b.sc0 = ar.take<unsigned long long>(3 * EK);
+  b.sc1 = ar.take<unsigned long long>(3 * EK);
   b.ibeg = ar.take<int>(EP);
   b.iend = ar.take<int>(EP);
   b.first = ar.take<int>(EP);
@@ -127,6 +151,11 @@ static bool carve_big(h3d_arena &ar, long long m, BigWS &b) {
   cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, static_cast<int>(3 * EK));
   cub::DeviceScan::ExclusiveSum(nullptr, c, static_cast<int *>(nullptr),
                                 static_cast<int *>(nullptr), static_cast<int>(EK + 1));
+  size_t d = 0;
+  cub::DeviceScan::InclusiveScan(nullptr, d, static_cast<unsigned long long *>(nullptr),
+                                 static_cast<unsigned long long *>(nullptr), LinkScanOp(),
+                                 static_cast<int>(3 * EK));
+  if (d > a) a = d;
   b.tmp_bytes = (a > c ? a : c) + 256;
   b.tmp = ar.take<unsigned char>(b.tmp_bytes);
   return ar.base == nullptr || b.tmp != nullptr;
@@ -305,38 +334,57 @@ __global__ void k_big_incidx(const unsigned *__restrict__ key, int E, BigWS W) {
 }
 
 // ------------------------------------ K5 links after each incidence (fill)
-__global__ void k_big_fill(Pass2 P, long long n, int lv, long long j0, long long J, BigWS W,
-                           const unsigned *__restrict__ val) {
+// A point's links after each of its incidences are a forward fill over its
+// list: an event naming it as a sets its next, as c its prev, its own
+// insertion sets both (its deletion sets nothing: _act never writes the
+// deleted point's links).  One segmented inclusive scan over all lists:
+// element = prv (22 bits) | nxt (22 bits) << 22 | has-prv << 44 |
+// has-nxt << 45 | list-head << 46.
+__global__ void k_big_fill_init(Pass2 P, long long n, int lv, long long j0, long long J, BigWS W,
+                                const unsigned *__restrict__ key, const unsigned *__restrict__ val,
+                                int E) {
   const int J2 = static_cast<int>(2 * J);
-  const int total = W.jnsoff[J2];
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
-    const int b0 = W.ibeg[x], b1 = W.iend[x];
-    if (b0 >= b1) continue;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < E; k += gridDim.x * blockDim.x) {
+    const int x = static_cast<int>(key[k]);
     const int jb = find_job(W.jnsoff, J2, x);
-    const JobRef r = job_ref(P, jb, J, j0, lv, n);
     const int p = x - W.jnsoff[jb];
-    const int gbase = W.jkinoff[jb];
-    int2 l = minf_links(r, p);
-    for (int k = b0; k < b1; ++k) {
-      const int g = static_cast<int>(val[k]);
-      const Ev e = W.seq[g];
-      const bool ins = (e.kind & 1) == EV_INS;
-      if (e.a == p) {
-        l.y = ins ? e.b : e.c;
-      } else if (e.c == p) {
-        l.x = ins ? e.b : e.a;
-      } else if (ins) {  // p inserted between a and c
-        l.x = e.a;
-        l.y = e.c;
-      }  // p deleted: its own links are never written (_act)
-      IncE o;
-      o.t = e.t;
-      o.idx = g - gbase;
-      o.prv = l.x;
-      o.nxt = l.y;
-      o.pad = 0;
-      W.inc[k] = o;
+    const Ev e = W.seq[val[k]];
+    const bool ins = (e.kind & 1) == EV_INS;
+    int prv = 0, nxt = 0;
+    bool hp = false, hn = false;
+    if (e.a == p) {
+      nxt = ins ? e.b : e.c;
+      hn = true;
+    } else if (e.c == p) {
+      prv = ins ? e.b : e.a;
+      hp = true;
+    } else if (ins) {  // p inserted between a and c
+      prv = e.a;
+      nxt = e.c;
+      hp = hn = true;
     }
+    W.sc0[k] = ls_pack(prv, nxt, hp, hn, k == W.ibeg[x]);
+  }
+}
+
+__global__ void k_big_fill_final(Pass2 P, long long n, int lv, long long j0, long long J, BigWS W,
+                                 const unsigned *__restrict__ key, const unsigned *__restrict__ val,
+                                 int E) {
+  const int J2 = static_cast<int>(2 * J);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < E; k += gridDim.x * blockDim.x) {
+    const int x = static_cast<int>(key[k]);
+    const int jb = find_job(W.jnsoff, J2, x);
+    const int p = x - W.jnsoff[jb];
+    const unsigned long long sv = W.sc1[k];
+    int2 l = make_int2(NIL, NIL);
+    if (!(sv & LS_HP) || !(sv & LS_HN)) l = minf_links(job_ref(P, jb, J, j0, lv, n), p);
+    const int g = static_cast<int>(val[k]);
+    IncE o;
+    o.t = W.seq[g].t;
+    o.idx = g - W.jkinoff[jb];
+    o.prv = (sv & LS_HP) ? static_cast<int>(sv & LS_MASK) : l.x;
+    o.nxt = (sv & LS_HN) ? static_cast<int>((sv >> 22) & LS_MASK) : l.y;
+    W.inc[k] = o;
   }
 }
 
@@ -912,7 +960,14 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
                                                   bits, s)))
       return H3D_E_CUDA;
     k_big_incidx<<<grid_of(3 * kin), 256, 0, s>>>(kb.Current(), static_cast<int>(3 * kin), W);
-    k_big_fill<<<grid_of(pts_n), 256, 0, s>>>(P, n, lv, j0, J, W, vb.Current());
+    k_big_fill_init<<<grid_of(3 * kin), 256, 0, s>>>(P, n, lv, j0, J, W, kb.Current(), vb.Current(),
+                                                    static_cast<int>(3 * kin));
+    size_t tb2 = W.tmp_bytes;
+    if (h3d_check(cub::DeviceScan::InclusiveScan(W.tmp, tb2, W.sc0, W.sc1, LinkScanOp(),
+                                                 static_cast<int>(3 * kin), s)))
+      return H3D_E_CUDA;
+    k_big_fill_final<<<grid_of(3 * kin), 256, 0, s>>>(P, n, lv, j0, J, W, kb.Current(), vb.Current(),
+                                                     static_cast<int>(3 * kin));
   }
   k_big_walk<<<grid_of(nseg), 256, 0, s>>>(P, pts, n, lv, j0, J, W, static_cast<int>(SEG), err);
   {

@@ -377,7 +377,7 @@ __host__ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
 // choice at once: out[r] = max over CTAs of sum(nS) when a CTA takes
 // 32 >> r consecutive jobs (r = 0..5); out[6] = largest single nS; out[7] =
 // largest shared-memory need of one warp-per-job merge; out[8] = largest
-// merged child log of one job.  One warp per 32
+// merged child log of one job; out[9] = all merged child logs.  One warp per 32
 // jobs, coalesced header reads.
 __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1,
                            unsigned long long *out) {
@@ -387,6 +387,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long chunks = (j1 - j0 + 31) >> 5;
   unsigned long long mx[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ksum = 0;
   for (long long c = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
     const long long j = j0 + c * 32 + lane;
@@ -404,6 +405,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
     mx[6] = nS > mx[6] ? nS : mx[6];
     mx[7] = wb > mx[7] ? wb : mx[7];
     mx[8] = kin > mx[8] ? kin : mx[8];
+    ksum += kin;
     unsigned long long t = nS;
     mx[5] = t > mx[5] ? t : mx[5];  // 1 job per CTA
 #pragma unroll
@@ -412,6 +414,8 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
       mx[r] = t > mx[r] ? t : mx[r];
     }
   }
+  for (int o = 16; o; o >>= 1) ksum += __shfl_xor_sync(FULL, ksum, o);
+  if (lane == 0 && ksum) atomicAdd(out + 9, ksum);
 #pragma unroll
   for (int r = 0; r < 9; ++r) {
     unsigned long long m = mx[r];
@@ -1293,7 +1297,8 @@ long long kTpjMinTotalJobs = 148 * 32;  // H3D_TPJ_MIN_JOBS (both passes)
 constexpr int kTpjPool = 200 * 1024;
 int kTpjMaxLevel = 40;          // H3D_TPJ_MAX_LEVEL
 long long kTpjXyzMax = 16 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the pool fits
-long long kBigKin = 512;           // H3D_BIG_KIN: time-split pipeline from this job log size
+long long kBigKin = 1000;          // H3D_BIG_KIN: time-split pipeline from this job log size
+long long kBigTotal = 200000;     // H3D_BIG_TOTAL: ... or half that with this many child events in the level
 
 bool g_attr_done = false;
 bool g_env_done = false;
@@ -1308,6 +1313,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_TPJ_MIN_JOBS")) kTpjMinTotalJobs = atoll(e);
   if (const char *e = getenv("H3D_LEAF_B")) g_leaf_b = atoi(e);
   if (const char *e = getenv("H3D_BIG_KIN")) kBigKin = atoll(e);
+  if (const char *e = getenv("H3D_BIG_TOTAL")) kBigTotal = atoll(e);
   if (g_leaf_b > 4) g_leaf_b = 4;
 }
 
@@ -1327,6 +1333,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   long long old = -1;
   if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
   else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = value > 4 ? 4 : static_cast<int>(value); }
+  else if (k == "big_total") { old = kBigTotal; if (value >= 0) kBigTotal = value; }
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
   else if (k == "tpj_max_level") { old = kTpjMaxLevel; if (value >= 0) kTpjMaxLevel = static_cast<int>(value); }
@@ -1440,17 +1447,19 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     // they fit a shared-memory slice (int16 local ids); one warp per job
     // (1-warp CTAs, pool = the largest job's need, HBM mode above it) for
     // the few-job levels.
-    cudaMemsetAsync(w0.need, 0, 9 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(w0.need, 0, 10 * sizeof(unsigned long long), s);
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
     k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 65535 ? 65535 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
         P, n, lv, j0, j1, w0.need);
-    unsigned long long need[9];
+    unsigned long long need[10];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
     // large merge jobs: the time-split pipeline (big.cu)
-    if (static_cast<long long>(need[8]) >= kBigKin && big_ws) {
+    // (its fixed cost, ~25 launches, only pays when the level has work)
+    const long long maxkin = static_cast<long long>(need[8]), sumkin = static_cast<long long>(need[9]);
+    if (big_ws && (maxkin >= kBigKin || (2 * maxkin >= kBigKin && sumkin >= kBigTotal))) {
       const long long rb = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s);
       if (rb < 0) return rb;
       if (rb == 0) {
