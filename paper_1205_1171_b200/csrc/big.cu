@@ -637,18 +637,29 @@ __global__ void __launch_bounds__(128) k_big_sweep(Pass2 P, const double *__rest
         ++cv;
       }
     } else if (bridge) {
+      // the new foot takes both links from its list (the other one is the
+      // old foot unless a child event deleted the old foot while it was a
+      // foot -- a near-degenerate input)
       if (which == 2) {  // u advances: the new foot enters the merged chain
         o.a = u; o.b = un; o.c = v; o.kind = EV_INS;
+        const int of = u;
         up = u; UP = U; u = un; U = UN; un = fl.y; q1 = un;
+        if (fl.x != of) { up = fl.x; q2 = up; }
       } else if (which == 3) {  // u leaves the merged chain
         o.a = up; o.b = u; o.c = v; o.kind = EV_DEL;
+        const int of = u;
         un = u; UN = U; u = up; U = UP; up = fl.x; q2 = up;
+        if (fl.y != of) { un = fl.y; q1 = un; }
       } else if (which == 4) {  // v leaves the merged chain
         o.a = u; o.b = v; o.c = vn; o.kind = EV_DEL;
+        const int of = v;
         vp = v; VP = V; v = vn; V = VN; vn = fl.y; q1 = vn;
+        if (fl.x != of) { vp = fl.x; q2 = vp; }
       } else {  // v retreats: the new foot enters the merged chain
         o.a = u; o.b = vp; o.c = v; o.kind = EV_INS;
+        const int of = v;
         vn = v; VN = V; v = vp; V = VP; vp = fl.x; q2 = vp;
+        if (fl.y != of) { vn = fl.y; q1 = vn; }
       }
       if (sideU) {
         cu = lo;

@@ -344,17 +344,28 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
       }
     }
     // rotate the bridge neighbourhood (selects), fetch the one new point
+    // A bridge move's new foot takes BOTH its links from its link word: the
+    // other one is normally the old foot, but not when a child event has
+    // deleted the old foot from its chain while it was still a foot (a
+    // near-degenerate input; the reference then reads the current links)
+    const bool bm = b2 | b3 | b4 | b5;
+    const int oth = bm ? ((b2 | b4) ? lz.x : lz.y) : NIL;
+    const int oldfoot = (b2 | b3) ? u : v;
+    const bool oth_new = bm && oth != oldfoot;
     const P3 N = S.pt(slot >= 0 ? newpt : NIL, pts, zs);
+    const P3 N2 = S.pt(oth_new ? oth : NIL, pts, zs);
+    const P3 OF = (b2 | b3) ? U : V;
+    const P3 O2 = oth_new ? N2 : OF;
     const int u1 = b2 ? un : (b3 ? up : u), v1 = b4 ? vn : (b5 ? vp : v);
     const P3 U1 = b2 ? UN : (b3 ? UP : U), V1 = b4 ? VN : (b5 ? VP : V);
-    const int un1 = (slot == 0) ? newpt : (b3 ? u : un);
-    const int up1 = (slot == 1) ? newpt : (b2 ? u : up);
-    const int vn1 = (slot == 2) ? newpt : (b5 ? v : vn);
-    const int vp1 = (slot == 3) ? newpt : (b4 ? v : vp);
-    const P3 UN1 = (slot == 0) ? N : (b3 ? U : UN);
-    const P3 UP1 = (slot == 1) ? N : (b2 ? U : UP);
-    const P3 VN1 = (slot == 2) ? N : (b5 ? V : VN);
-    const P3 VP1 = (slot == 3) ? N : (b4 ? V : VP);
+    const int un1 = (slot == 0) ? newpt : (b3 ? oth : un);
+    const int up1 = (slot == 1) ? newpt : (b2 ? oth : up);
+    const int vn1 = (slot == 2) ? newpt : (b5 ? oth : vn);
+    const int vp1 = (slot == 3) ? newpt : (b4 ? oth : vp);
+    const P3 UN1 = (slot == 0) ? N : (b3 ? O2 : UN);
+    const P3 UP1 = (slot == 1) ? N : (b2 ? O2 : UP);
+    const P3 VN1 = (slot == 2) ? N : (b5 ? O2 : VN);
+    const P3 VP1 = (slot == 3) ? N : (b4 ? O2 : VP);
     u = u1; v = v1; un = un1; up = up1; vn = vn1; vp = vp1;
     U = U1; V = V1; UN = UN1; UP = UP1; VN = VN1; VP = VP1;
     if (__any_sync(FULL, slot >= 0)) {

@@ -46,6 +46,94 @@ __global__ void k_adjacent_tie(const unsigned long long *__restrict__ keys, long
   }
 }
 
+// ---- fast stable argsort of x: 32-bit monotone fixed-point keys (4 radix
+// passes instead of 8), then the rare runs of equal 32-bit keys re-sorted by
+// the exact 64-bit order key (stable: equal x keep index order).  Any run
+// longer than RUN_MAX sends the sort to the 64-bit path.
+constexpr int RUN_MAX = 64;
+
+__global__ void k_xminmax(const double *__restrict__ pts, long long n, unsigned long long *mm) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = order_key(pts[3 * i]);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
+__device__ __forceinline__ double key_to_double(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__global__ void k_keys32(const double *__restrict__ pts, long long n,
+                         const unsigned long long *__restrict__ mm, unsigned *keys, int *vals) {
+  const double lo = key_to_double(mm[0]), hi = key_to_double(mm[1]);
+  const double span = __dsub_rn(hi, lo);
+  const double sc = span > 0.0 ? __ddiv_rn(4294967295.0, span) : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double x = pts[3 * i];
+    if (x == 0.0) x = 0.0;
+    double f = __dmul_rn(__dsub_rn(x, lo), sc);  // monotone in x
+    if (!(f >= 0.0)) f = 0.0;
+    if (f > 4294967295.0) f = 4294967295.0;
+    keys[i] = static_cast<unsigned>(f);
+    vals[i] = static_cast<int>(i);
+  }
+}
+
+// runs of equal 32-bit keys: insertion sort by (64-bit order key, index)
+__global__ void k_tiefix(const double *__restrict__ pts, const unsigned *__restrict__ k32,
+                         int *vals, long long n, int *flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i + 1 < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned k = k32[i];
+    if (k32[i + 1] != k || (i > 0 && k32[i - 1] == k)) continue;  // i: head of a run
+    long long e = i + 1;
+    while (e < n && k32[e] == k && e - i <= RUN_MAX) ++e;
+    if (e - i > RUN_MAX) {
+      *flag = 1;  // degenerate distribution: use the 64-bit sort
+      continue;
+    }
+    for (long long a = i + 1; a < e; ++a) {
+      const int va = vals[a];
+      const unsigned long long ka = order_key(pts[3ll * va]);
+      long long b = a - 1;
+      while (b >= i) {
+        const int vb = vals[b];
+        const unsigned long long kb = order_key(pts[3ll * vb]);
+        if (kb < ka || (kb == ka && vb < va)) break;
+        vals[b + 1] = vb;
+        --b;
+      }
+      vals[b + 1] = va;
+    }
+  }
+}
+
+// adjacent equal x in the sorted order (through the permutation)
+__global__ void k_adjacent_tie_perm(const double *__restrict__ pts, const int *__restrict__ perm,
+                                    long long n, int *flag) {
+  for (long long i = 1 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (pts[3ll * perm[i]] == pts[3ll * perm[i - 1]]) {
+      *flag = 1;
+      return;
+    }
+  }
+}
+
 __global__ void k_gather_rows(const double *__restrict__ pts, const int *__restrict__ perm,
                               long long n, double *out, long long *order,
                               const int *__restrict__ outer) {
@@ -256,6 +344,7 @@ struct PresortWS {
   double *partial;
   double *centroid;
   long long *count;
+  unsigned long long *mm;
 };
 
 constexpr int kColsumBlocks = 296;
@@ -291,7 +380,8 @@ bool carve(h3d_arena &ar, long long n, PresortWS &w) {
   w.partial = ar.take<double>(3 * kColsumBlocks);
   w.centroid = ar.take<double>(4);
   w.count = ar.take<long long>(2);
-  return ar.base == nullptr || w.count != nullptr;
+  w.mm = ar.take<unsigned long long>(2);
+  return ar.base == nullptr || w.mm != nullptr;
 }
 
 // stable sort of (keys, vals) pairs; result in (*ko, *vo)
@@ -338,17 +428,39 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   cudaMemsetAsync(w.flag, 0, sizeof(int) * 4, s);
   h3d_count_launches(1);
   k_nonfinite<<<G, 256, 0, s>>>(pts, 3 * n, w.flag + 1);
-  // stable argsort of x (api.py:97)
-  h3d_count_launches(1);
-  k_keys<<<G, 256, 0, s>>>(pts, nullptr, 0, n, w.k0, w.v0);
-  if (!radix(w, w.k0, w.v0, w.k1, w.v1, n, &ks, &vs, s)) return H3D_E_CUDA;
-  h3d_count_launches(1);
-  k_adjacent_tie<<<G, 256, 0, s>>>(ks, n, w.flag);
-  int hflag[2] = {0, 0};
-  if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+  // stable argsort of x (api.py:97): 32-bit fixed-point keys + tie-run fix
+  unsigned long long mm_init[2] = {~0ull, 0ull};
+  cudaMemcpyAsync(w.mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, s);
+  h3d_count_launches(4);
+  k_xminmax<<<G, 256, 0, s>>>(pts, n, w.mm);
+  unsigned *k32a = reinterpret_cast<unsigned *>(w.k0), *k32b = reinterpret_cast<unsigned *>(w.k1);
+  k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, w.v0);
+  {
+    cub::DoubleBuffer<unsigned> kb(k32a, k32b);
+    cub::DoubleBuffer<int> vb(w.v0, w.v1);
+    size_t bytes = w.cub_bytes;
+    if (h3d_check(cub::DeviceRadixSort::SortPairs(w.cub_tmp, bytes, kb, vb, static_cast<int>(n),
+                                                  0, 32, s)))
+      return H3D_E_CUDA;
+    vs = vb.Current();
+    k_tiefix<<<G, 256, 0, s>>>(pts, kb.Current(), vs, n, w.flag + 2);
+  }
+  k_adjacent_tie_perm<<<G, 256, 0, s>>>(pts, vs, n, w.flag);
+  int hflag[3] = {0, 0, 0};
+  if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
       h3d_check(cudaStreamSynchronize(s)))
     return H3D_E_CUDA;
   if (hflag[1]) return H3D_E_NONFINITE;
+  if (hflag[2]) {  // long runs of equal 32-bit keys: the exact 64-bit sort
+    cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+    h3d_count_launches(2);
+    k_keys<<<G, 256, 0, s>>>(pts, nullptr, 0, n, w.k0, w.v0);
+    if (!radix(w, w.k0, w.v0, w.k1, w.v1, n, &ks, &vs, s)) return H3D_E_CUDA;
+    k_adjacent_tie<<<G, 256, 0, s>>>(ks, n, w.flag);
+    if (h3d_check(cudaMemcpyAsync(hflag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+        h3d_check(cudaStreamSynchronize(s)))
+      return H3D_E_CUDA;
+  }
   const int tie = hflag[0];
   if (!tie) {
     h3d_count_launches(1);

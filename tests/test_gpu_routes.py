@@ -68,3 +68,16 @@ def test_tune_roundtrip():
     assert fast.tune("big_kin", old) == 1234
     with pytest.raises(KeyError):
         fast.tune("no_such_knob")
+
+
+def test_presort_clustered_x_fallback(oracle_mod):
+    """A tight x-cluster collapses the presort's 32-bit fixed-point keys into
+    long equal runs; the presort must fall back to the exact 64-bit sort and
+    still reproduce the reference."""
+    rng = np.random.default_rng(11)
+    pts = rng.uniform(-1.0, 1.0, (20000, 3))
+    pts[:19990, 0] = rng.uniform(0.0, 1e-12, 19990)  # 19990 points within 1e-12 in x
+    exp = oracle_mod.convex_hull_3d(pts)
+    r = H.convex_hull_3d(pts)
+    assert np.array_equal(r.faces, exp.faces)
+    assert np.array_equal(r.vertices, exp.vertices)
