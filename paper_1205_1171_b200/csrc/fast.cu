@@ -181,7 +181,9 @@ struct LEvOut {
 // that replaces the reference's rewind.  Returns k or a negative code.
 // u_init: the left child's last point (its right neighbour is the right
 // child's first); roff: added to the right child's event ids.
-template <class SL, class EIN, class EOUT>
+// CHILD = false: both child logs are empty (level 2: two linked pairs), so
+// the child-event machinery compiles away.
+template <class SL, class EIN, class EOUT, bool CHILD = true>
 __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
                                 const double *__restrict__ pts, double zs, EIN evL, int kL,
                                 EIN evR, int kR, EOUT out, long long capRef, long long limitRef,
@@ -265,7 +267,7 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
     if (c4 > tcur && c4 < best) { best = c4; which = 4; }
     if (c5 > tcur && c5 < best) { best = c5; which = 5; }
     active = active && which >= 0;
-    const bool left = active && which == 0, right = active && which == 1;
+    const bool left = CHILD && active && which == 0, right = CHILD && active && which == 1;
     const bool child = left || right;
     const bool b2 = active && which == 2, b3 = active && which == 3;
     const bool b4 = active && which == 4, b5 = active && which == 5;

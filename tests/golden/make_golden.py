@@ -1,6 +1,6 @@
 """Generate the golden fixtures from the UNMODIFIED reference (run here only).
 
-    python tests/golden/make_golden.py [--large]
+    python tests/golden/make_golden.py [--large [--c4]] | --c5
 
 Needs oracle/_ref/site (oracle/build_ref.sh).  Writes:
 
@@ -152,7 +152,7 @@ def level_stats(pts_sorted: np.ndarray):
     return rows
 
 
-def make_large(ref, with_c4: bool):
+def make_large(ref, with_c4: bool, only_c5: bool = False):
     from paper_1205_1171_b200.generators import generate, integer_cloud
 
     configs = [("C2_ball_2^20", lambda: generate(2**20, "ball", 0)),
@@ -160,6 +160,8 @@ def make_large(ref, with_c4: bool):
                ("int_2^20_R2^31", lambda: integer_cloud(2**20, 0))]
     if with_c4:
         configs.append(("C4_cube_2^24", lambda: generate(2**24, "cube", 0)))
+    if only_c5:  # C5 (2^27 mixed): digests only, no per-level statistics
+        configs = [("C5_mixed_2^27", lambda: generate(2**27, "mixed", 0))]
     large = {}
     stats = {}
     path = os.path.join(HERE, "large.json")
@@ -182,7 +184,7 @@ def make_large(ref, with_c4: bool):
             "ref_seconds_threads": round(dt, 3), "ref_threads": os.cpu_count(),
         }
         print(name, large[name])
-        if not name.startswith("int"):
+        if not name.startswith(("int", "C5")):
             sp, _, _ = O.sort_and_perturb(pts)
             up = sp.copy()
             up[:, 2] = -up[:, 2]
@@ -195,6 +197,9 @@ if __name__ == "__main__":
     ref = O.reference()
     if ref is None:
         sys.exit("build the reference first: oracle/build_ref.sh")
+    if "--c5" in sys.argv:
+        make_large(ref, with_c4=False, only_c5=True)
+        sys.exit(0)
     make_small(ref)
     make_levels(ref)
     if "--large" in sys.argv:

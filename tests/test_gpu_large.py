@@ -19,6 +19,7 @@ GEN = {
     "C3_sphere_2^20": lambda: generate(2**20, "sphere", 0),
     "int_2^20_R2^31": lambda: integer_cloud(2**20, 0),
     "C4_cube_2^24": lambda: generate(2**24, "cube", 0),
+    "C5_mixed_2^27": lambda: generate(2**27, "mixed", 0),
 }
 
 
