@@ -1316,6 +1316,8 @@ long long kBigTotal = 200000;     // H3D_BIG_TOTAL: ... or half that with this m
 bool g_attr_done = false;
 bool g_env_done = false;
 int g_leaf_b = 3;  // H3D_LEAF_B: levels 1..B fused (0 = off)
+int g_mini = 1;    // H3D_MINI: few small jobs -> mini.cu (0 = warp kernel)
+long long kMiniMaxCtas = 2 * 148;  // H3D_MINI_CTAS
 
 // tuning knobs from the environment (read once; h3d_tune overrides)
 void load_env_once() {
@@ -1327,6 +1329,8 @@ void load_env_once() {
   if (const char *e = getenv("H3D_LEAF_B")) g_leaf_b = atoi(e);
   if (const char *e = getenv("H3D_BIG_KIN")) kBigKin = atoll(e);
   if (const char *e = getenv("H3D_BIG_TOTAL")) kBigTotal = atoll(e);
+  if (const char *e = getenv("H3D_MINI")) g_mini = atoi(e);
+  if (const char *e = getenv("H3D_MINI_CTAS")) kMiniMaxCtas = atoll(e);
   if (g_leaf_b > 4) g_leaf_b = 4;
 }
 
@@ -1346,6 +1350,8 @@ int64_t h3d_tune(const char *name, int64_t value) {
   long long old = -1;
   if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
   else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = value > 4 ? 4 : static_cast<int>(value); }
+  else if (k == "mini") { old = g_mini; if (value >= 0) g_mini = value ? 1 : 0; }
+  else if (k == "mini_ctas") { old = kMiniMaxCtas; if (value >= 0) kMiniMaxCtas = value; }
   else if (k == "big_total") { old = kBigTotal; if (value >= 0) kBigTotal = value; }
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
@@ -1469,9 +1475,24 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
+    const long long maxkin = static_cast<long long>(need[8]), sumkin = static_cast<long long>(need[9]);
+    // few small jobs: the in-shared-memory time-split merge (mini.cu)
+    // (154 KB of shared memory per CTA: one CTA per SM, so only for levels of
+    // at most a few CTAs per SM)
+    const bool mini_small = static_cast<long long>(need[6]) <= kMiniSmallPoints &&
+                            maxkin <= kMiniSmallEvents;
+    if (g_mini && 2 * jobs < kTpjMinTotalJobs &&
+        ((mini_small && 2 * jobs <= 4 * kMiniMaxCtas) ||
+         (2 * jobs <= kMiniMaxCtas && static_cast<long long>(need[6]) <= kMiniMaxPoints &&
+          maxkin <= kMiniMaxEvents))) {
+      const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, mini_small ? 0 : 1);
+      if (rm < 0) return rm;
+      h3d_prof_end(e0, lv + 5000, 2, s);
+      P = Pass2{P.out0, P.out1, P.in0, P.in1};
+      continue;
+    }
     // large merge jobs: the time-split pipeline (big.cu)
     // (its fixed cost, ~25 launches, only pays when the level has work)
-    const long long maxkin = static_cast<long long>(need[8]), sumkin = static_cast<long long>(need[9]);
     if (big_ws && (maxkin >= kBigKin || (2 * maxkin >= kBigKin && sumkin >= kBigTotal))) {
       const long long rb = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s);
       if (rb < 0) return rb;

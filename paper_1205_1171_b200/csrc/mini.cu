@@ -1,0 +1,583 @@
+// mini.cu -- the time-split merge (big.cu) for SMALL jobs, one CTA per job,
+// everything in shared memory.
+//
+// Levels with few jobs whose merged child log is a few hundred to two
+// thousand events (the top levels of cube/ball clouds) are sequential
+// chains: ~800 dependent steps per job whatever the kernel.  Here the same
+// decomposition as big.cu runs inside one CTA: merged child sequence S,
+// per-point incidence lists (counting sort + per-list insertion sort), links
+// after each incidence, segment start bridges by walks at the segment time,
+// segment sweeps over only the foot-touching events and the bridge events,
+// classification of every child event by the bridge at its time, and the
+// start-of-time link rebuild + compaction -- with shared-memory latencies
+// instead of HBM ones, and one launch per level.
+#include <cub/cub.cuh>
+
+#include "fast.cuh"
+
+namespace h3d {
+
+constexpr int MINI_S = 64;     // largest number of time segments
+constexpr int MINI_NIL = -1;
+
+// MINI_T threads per CTA (one job), MINI_K largest merged child log,
+// MINI_N largest job (points), MINI_B largest number of bridge events
+template <int MINI_T, int MINI_K, int MINI_N>
+struct MiniSmem {
+  static constexpr int MINI_B = MINI_K;
+  double st[MINI_K];            // S: event times
+  unsigned sw[MINI_K];          // S: a | b << 10 | c << 20 | kind << 30 | side << 31
+  double X[MINI_N], Y[MINI_N], Z[MINI_N];
+  int G[MINI_N];                // gid
+  short2 LN[MINI_N];            // links at t = -inf (job-local)
+  short2 KL[MINI_N];            // rebuilt links
+  int ib[MINI_N + 1];           // incidence list bounds (exclusive scan)
+  int cur[MINI_N];              // scatter cursors, then first output event
+  short ei[3 * MINI_K];         // incidence: event index
+  short2 el[3 * MINI_K];        // incidence: links after the event
+  int cpos[MINI_K + 1];         // kept child events: flags, then exclusive scan
+  int nid[MINI_N + 1];          // keep flags, then new ids (exclusive scan)
+  double bt[MINI_B];            // bridge events: time
+  unsigned bw[MINI_B];          //   facet a | b << 10 | c << 20 | kind << 30
+  short2 buv[MINI_B];           //   feet after
+  short2 sst[MINI_S];           // segment start bridges
+  int sbn[MINI_S + 1];          // bridge events per segment, then offsets
+  int flag, nb;
+  typename cub::BlockScan<int, MINI_T>::TempStorage scan;
+};
+
+__device__ __forceinline__ int swa(unsigned w) { return static_cast<int>(w & 1023u); }
+__device__ __forceinline__ int swb(unsigned w) { return static_cast<int>((w >> 10) & 1023u); }
+__device__ __forceinline__ int swc(unsigned w) { return static_cast<int>((w >> 20) & 1023u); }
+__device__ __forceinline__ int swk(unsigned w) { return static_cast<int>((w >> 30) & 1u); }
+__device__ __forceinline__ int sws(unsigned w) { return static_cast<int>(w >> 31); }
+
+template <class MS>
+__device__ __forceinline__ P3 mpt(const MS &m, int p) {
+  P3 r;
+  if (p == MINI_NIL) {
+    r.x = r.y = r.z = 0.0;
+    return r;
+  }
+  r.x = m.X[p];
+  r.y = m.Y[p];
+  r.z = m.Z[p];
+  return r;
+}
+
+template <class MS>
+__device__ __forceinline__ double mevt(const MS &m, int a, int b, int c) {
+  if (a == MINI_NIL || b == MINI_NIL || c == MINI_NIL) return INF;
+  return evtime_xyz(m.X[a], m.Y[a], m.Z[a], m.X[b], m.Y[b], m.Z[b], m.X[c], m.Y[c], m.Z[c]);
+}
+
+// links of p after the first `pos` events of S; *first = its first
+// incidence at or after pos
+template <class MS>
+__device__ __forceinline__ short2 mlinks(const MS &m, int p, int pos, int *first) {
+  int lo = m.ib[p], hi = m.ib[p + 1];
+  const int b0 = lo;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (m.ei[mid] < pos) lo = mid + 1; else hi = mid;
+  }
+  *first = lo;
+  return lo == b0 ? m.LN[p] : m.el[lo - 1];
+}
+
+template <class MS>
+__device__ __forceinline__ bool mturn_neg_at(const MS &m, int a, int b, int c, double T) {
+  const double den = turn_xy(m.X[a], m.Y[a], m.X[b], m.Y[b], m.X[c], m.Y[c]);
+  const double tau = mevt(m, a, b, c);
+  return tau <= T ? den > 0.0 : den < 0.0;
+}
+
+// the sequential core of one segment (see big.cu k_big_sweep); MODE 0
+// counts, MODE 1 writes.  Returns false on an exact tie.
+template <int MODE, class MS>
+__device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int *nb_out,
+                           int2 *end_uv) {
+  const int pos0 = s * seg, pos1 = (pos0 + seg < kin) ? pos0 + seg : kin;
+  const double tend = (s == nseg - 1) ? INF : m.st[pos1 - 1];
+  double tcur = (s == 0) ? -INF : m.st[pos0 - 1];
+  int u = m.sst[s].x, v = m.sst[s].y;
+  int pos = pos0, cu, cv;
+  short2 lu = mlinks(m, u, pos, &cu), lw = mlinks(m, v, pos, &cv);
+  int up = lu.x, un = lu.y, vp = lw.x, vn = lw.y;
+  double c2 = mevt(m, u, un, v), c3 = mevt(m, up, u, v);
+  double c4 = mevt(m, u, v, vn), c5 = mevt(m, u, vp, v);
+  int nb = 0;
+  const int base = (MODE == 1) ? m.sbn[s] : 0;
+  for (;;) {
+    double tu = INF, tv = INF;
+    if (cu < m.ib[u + 1] && m.ei[cu] < pos1) tu = m.st[m.ei[cu]];
+    if (cv < m.ib[v + 1] && m.ei[cv] < pos1) tv = m.st[m.ei[cv]];
+    double best = INF;
+    int which = -1;
+    if (tu > tcur && tu < best) { best = tu; which = 0; }
+    if (tv > tcur && tv < best) { best = tv; which = 1; }
+    if (c2 > tcur && c2 < best) { best = c2; which = 2; }
+    if (c3 > tcur && c3 < best) { best = c3; which = 3; }
+    if (c4 > tcur && c4 < best) { best = c4; which = 4; }
+    if (c5 > tcur && c5 < best) { best = c5; which = 5; }
+    if (which < 0 || best > tend) break;
+    if ((which != 0 && tu == best) || (which != 1 && tv == best) || (which != 2 && c2 == best) ||
+        (which != 3 && c3 == best) || (which != 4 && c4 == best) || (which != 5 && c5 == best))
+      return false;
+    if (which == 0) {  // a child event naming u
+      pos = m.ei[cu] + 1;
+      up = m.el[cu].x;
+      un = m.el[cu].y;
+      ++cu;
+      c2 = mevt(m, u, un, v);
+      c3 = mevt(m, up, u, v);
+    } else if (which == 1) {  // a child event naming v
+      pos = m.ei[cv] + 1;
+      vp = m.el[cv].x;
+      vn = m.el[cv].y;
+      ++cv;
+      c4 = mevt(m, u, v, vn);
+      c5 = mevt(m, u, vp, v);
+    } else {
+      {  // the child events before this time are all applied
+        int lo = pos, hi = pos1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (m.st[mid] < best) lo = mid + 1; else hi = mid;
+        }
+        pos = lo;
+      }
+      int a, b, c, kind;
+      // the new foot takes both links from its list (see big.cu)
+      if (which == 2) {
+        a = u; b = un; c = v; kind = EV_INS;
+        u = un;
+        const short2 l = mlinks(m, u, pos, &cu);
+        up = l.x; un = l.y;
+      } else if (which == 3) {
+        a = up; b = u; c = v; kind = EV_DEL;
+        u = up;
+        const short2 l = mlinks(m, u, pos, &cu);
+        up = l.x; un = l.y;
+      } else if (which == 4) {
+        a = u; b = v; c = vn; kind = EV_DEL;
+        v = vn;
+        const short2 l = mlinks(m, v, pos, &cv);
+        vp = l.x; vn = l.y;
+      } else {
+        a = u; b = vp; c = v; kind = EV_INS;
+        v = vp;
+        const short2 l = mlinks(m, v, pos, &cv);
+        vp = l.x; vn = l.y;
+      }
+      if (MODE == 1 && base + nb < MS::MINI_B) {
+        m.bt[base + nb] = best;
+        m.bw[base + nb] = static_cast<unsigned>(a) | (static_cast<unsigned>(b) << 10) |
+                          (static_cast<unsigned>(c) << 20) | (static_cast<unsigned>(kind) << 30);
+        m.buv[base + nb] = make_short2(static_cast<short>(u), static_cast<short>(v));
+      }
+      ++nb;
+      c2 = mevt(m, u, un, v);
+      c3 = mevt(m, up, u, v);
+      c4 = mevt(m, u, v, vn);
+      c5 = mevt(m, u, vp, v);
+    }
+    tcur = best;
+  }
+  *nb_out = nb;
+  *end_uv = make_int2(u, v);
+  return true;
+}
+
+template <int MINI_T, int MINI_K, int MINI_N>
+__global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restrict__ pts,
+                                                 long long n, int lv, long long j0, long long j1,
+                                                 long long *err) {
+  typedef MiniSmem<MINI_T, MINI_K, MINI_N> MS;
+  constexpr int MINI_B = MS::MINI_B;
+  constexpr int PER = (MINI_K + MINI_T) / MINI_T;  // blocked-scan items per thread
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MS &m = *reinterpret_cast<MS *>(smem_raw);
+  typedef cub::BlockScan<int, MINI_T> Scan;
+  const int tid = threadIdx.x, T = MINI_T;
+  const long long j = j0 + blockIdx.x;
+  if (j >= j1) return;
+  if (*reinterpret_cast<volatile long long *>(err) != 0) return;
+  const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
+  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
+  const double zs = blockIdx.y ? -1.0 : 1.0;
+  const long long size = 1ll << lv, half = size >> 1;
+  const long long L = j << lv, M = L + half;
+  const long long R_ = (L + size < n) ? L + size : n;
+  const int2 hl = in.hdr[2 * j];
+  if (R_ - L <= half) {  // carry (copy_log, parallel.py:107-108)
+    for (int p = tid; p < hl.x; p += T) {
+      out.lnk[L + p] = in.lnk[L + p];
+      out.gid[L + p] = in.gid[L + p];
+    }
+    for (int e = tid; e < hl.y; e += T) out.ev[2 * L + e] = in.ev[2 * L + e];
+    if (tid == 0) out.hdr[j] = hl;
+    return;
+  }
+  const int2 hr = in.hdr[2 * j + 1];
+  const int nSL = hl.x, nS = hl.x + hr.x, kL = hl.y, kR = hr.y, kin = kL + kR;
+  if (nS > MINI_N || kin > MINI_K) {  // the host routes only fitting levels here
+    if (tid == 0) raise_err(err, E_FASTPATH);
+    return;
+  }
+  if (tid == 0) m.flag = 0;
+  // ---- points
+  for (int p = tid; p < nS; p += T) {
+    const long long src = p < nSL ? L + p : M + (p - nSL);
+    int2 l = in.lnk[src];
+    if (p >= nSL) {
+      if (l.x != NIL) l.x += nSL;
+      if (l.y != NIL) l.y += nSL;
+    }
+    const int g = in.gid[src];
+    const P3 c = load_pt(pts, g, zs);
+    m.X[p] = c.x;
+    m.Y[p] = c.y;
+    m.Z[p] = c.z;
+    m.G[p] = g;
+    m.LN[p] = make_short2(static_cast<short>(l.x), static_cast<short>(l.y));
+    m.cur[p] = 0;
+  }
+  // ---- merged child sequence S (merge path, left first on equal times)
+  const Ev *evL = in.ev + 2 * L, *evR = in.ev + 2 * M;
+  for (int d = tid; d < kin; d += T) {
+    int lo = d - kR > 0 ? d - kR : 0, hi = d < kL ? d : kL;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (evL[mid].t <= evR[d - mid - 1].t) lo = mid + 1; else hi = mid;
+    }
+    const int i = lo, jj = d - lo;
+    Ev o;
+    unsigned side = 0;
+    if (i < kL && (jj >= kR || evL[i].t <= evR[jj].t)) {
+      o = evL[i];
+    } else {
+      o = evR[jj];
+      o.a += nSL;
+      o.b += nSL;
+      o.c += nSL;
+      side = 1;
+    }
+    m.st[d] = o.t;
+    m.sw[d] = static_cast<unsigned>(o.a) | (static_cast<unsigned>(o.b) << 10) |
+              (static_cast<unsigned>(o.c) << 20) | (static_cast<unsigned>(o.kind & 1) << 30) |
+              (side << 31);
+  }
+  __syncthreads();
+  // ---- incidence lists: counts, scan, scatter, per-list sort, links after
+  for (int d = tid; d < kin; d += T) {
+    if (d > 0 && m.st[d] == m.st[d - 1]) m.flag = 1;  // exact tie
+    const unsigned w = m.sw[d];
+    atomicAdd(&m.cur[swa(w)], 1);
+    atomicAdd(&m.cur[swb(w)], 1);
+    atomicAdd(&m.cur[swc(w)], 1);
+  }
+  __syncthreads();
+  {
+    const int per = (nS + T) / T;  // blocked scan: `per` consecutive items per thread
+    int local[PER];
+    int sum = 0;
+    for (int q = 0; q < per && q < PER; ++q) {
+      const int p = tid * per + q;
+      local[q] = p < nS ? m.cur[p] : 0;
+      sum += local[q];
+    }
+    int off;
+    Scan(m.scan).ExclusiveSum(sum, off);
+    for (int q = 0; q < per && q < PER; ++q) {
+      const int p = tid * per + q;
+      if (p <= nS) m.ib[p] = off;
+      off += local[q];
+    }
+  }
+  __syncthreads();
+  for (int p = tid; p < nS; p += T) m.cur[p] = m.ib[p];
+  __syncthreads();
+  for (int d = tid; d < kin; d += T) {
+    const unsigned w = m.sw[d];
+    m.ei[atomicAdd(&m.cur[swa(w)], 1)] = static_cast<short>(d);
+    m.ei[atomicAdd(&m.cur[swb(w)], 1)] = static_cast<short>(d);
+    m.ei[atomicAdd(&m.cur[swc(w)], 1)] = static_cast<short>(d);
+  }
+  __syncthreads();
+  for (int p = tid; p < nS; p += T) {
+    const int b0 = m.ib[p], b1 = m.ib[p + 1];
+    for (int a = b0 + 1; a < b1; ++a) {  // insertion sort by event index (lists are short)
+      const short x = m.ei[a];
+      int b = a - 1;
+      while (b >= b0 && m.ei[b] > x) {
+        m.ei[b + 1] = m.ei[b];
+        --b;
+      }
+      m.ei[b + 1] = x;
+    }
+    short2 l = m.LN[p];
+    for (int k = b0; k < b1; ++k) {  // links after each incidence (forward fill)
+      const unsigned w = m.sw[m.ei[k]];
+      const bool ins = swk(w) == EV_INS;
+      if (swa(w) == p) {
+        l.y = static_cast<short>(ins ? swb(w) : swc(w));
+      } else if (swc(w) == p) {
+        l.x = static_cast<short>(ins ? swb(w) : swa(w));
+      } else if (ins) {
+        l.x = static_cast<short>(swa(w));
+        l.y = static_cast<short>(swc(w));
+      }
+      m.el[k] = l;
+    }
+  }
+  __syncthreads();
+  // ---- segments: start bridges by walks
+  int nseg = kin / 16;
+  if (nseg > MINI_S) nseg = MINI_S;
+  if (nseg < 1) nseg = 1;
+  const int seg = (kin + nseg - 1) / nseg > 0 ? (kin + nseg - 1) / nseg : 1;
+  nseg = kin > 0 ? (kin + seg - 1) / seg : 1;
+  const long long limit = nS + 2;
+  if (tid < nseg) {
+    const int s = tid;
+    int u = nSL - 1, v = nSL;
+    long long moves = 0;
+    bool bad = false;
+    if (s == 0) {  // _find_bridge (_ckernels.pyx:63-83)
+      for (;;) {
+        const int vn = m.LN[v].y;
+        if (vn != NIL && turn_xy(m.X[u], m.Y[u], m.X[v], m.Y[v], m.X[vn], m.Y[vn]) < 0.0) {
+          v = vn;
+          if (++moves > limit) { bad = true; break; }
+          continue;
+        }
+        const int up = m.LN[u].x;
+        if (up != NIL && turn_xy(m.X[up], m.Y[up], m.X[u], m.Y[u], m.X[v], m.Y[v]) < 0.0) {
+          u = up;
+          if (++moves > limit) { bad = true; break; }
+          continue;
+        }
+        break;
+      }
+    } else {  // just after the last child event before the segment
+      const int pos = s * seg;
+      const double T0 = m.st[pos - 1];
+      int dummy;
+      for (;;) {
+        const int vn = mlinks(m, v, pos, &dummy).y;
+        if (vn != NIL && mturn_neg_at(m, u, v, vn, T0)) {
+          v = vn;
+          if (++moves > limit) { bad = true; break; }
+          continue;
+        }
+        const int up = mlinks(m, u, pos, &dummy).x;
+        if (up != NIL && mturn_neg_at(m, up, u, v, T0)) {
+          u = up;
+          if (++moves > limit) { bad = true; break; }
+          continue;
+        }
+        break;
+      }
+    }
+    if (bad) m.flag = 1;
+    m.sst[s] = make_short2(static_cast<short>(u), static_cast<short>(v));
+  }
+  __syncthreads();
+  // ---- segment sweeps: count, offsets, write
+  if (tid < nseg) {
+    int nb;
+    int2 e;
+    if (!mini_sweep<0>(m, tid, nseg, seg, kin, &nb, &e)) m.flag = 1;
+    if (tid + 1 < nseg && (m.sst[tid + 1].x != e.x || m.sst[tid + 1].y != e.y)) m.flag = 1;
+    m.sbn[tid] = nb;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0;
+    for (int s = 0; s < nseg; ++s) {
+      const int c = m.sbn[s];
+      m.sbn[s] = o;
+      o += c;
+    }
+    m.sbn[nseg] = o;
+    m.nb = o;
+    if (o > MINI_B) m.flag = 1;
+  }
+  __syncthreads();
+  if (m.flag) {  // exact tie, walk/sweep disagreement or capacity: exact engine
+    if (tid == 0) raise_err(err, E_FASTPATH);
+    return;
+  }
+  if (tid < nseg) {
+    int nb;
+    int2 e;
+    mini_sweep<1>(m, tid, nseg, seg, kin, &nb, &e);
+  }
+  __syncthreads();
+  const int NB = m.nb;
+  const int2 uv0 = make_int2(m.sst[0].x, m.sst[0].y);
+  // ---- every child event kept or hidden by the bridge at its time
+  auto bridges_before = [&](double t) {
+    int lo = 0, hi = NB;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (m.bt[mid] < t) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  {
+    const int per = (kin + T) / T;
+    int local[PER];
+    int sum = 0;
+    for (int q = 0; q < per && q < PER; ++q) {
+      const int d = tid * per + q;
+      int keep = 0;
+      if (d < kin) {
+        const double t = m.st[d];
+        const unsigned w = m.sw[d];
+        const int nbf = bridges_before(t);
+        if (nbf < NB && m.bt[nbf] == t) m.flag = 1;
+        const int u = nbf ? m.buv[nbf - 1].x : uv0.x, v = nbf ? m.buv[nbf - 1].y : uv0.y;
+        keep = sws(w) ? (swb(w) > v) : (swb(w) < u);  // _merge_one cases 0/1
+      }
+      local[q] = keep;
+      sum += keep;
+    }
+    int off;
+    Scan(m.scan).ExclusiveSum(sum, off);
+    for (int q = 0; q < per && q < PER; ++q) {
+      const int d = tid * per + q;
+      if (d <= kin) m.cpos[d] = local[q] ? (off | (1 << 30)) : off;
+      off += local[q];
+    }
+  }
+  for (int p = tid; p < nS; p += T) m.cur[p] = 0x7fffffff;  // first output event
+  __syncthreads();
+  const int kept = m.cpos[kin] & ~(1 << 30);
+  const int kout = kept + NB;
+  if (m.flag || kout > 2 * (R_ - L) - 1) {
+    if (tid == 0) raise_err(err, m.flag ? E_FASTPATH : H3D_E_OVERFLOW);
+    return;
+  }
+  // ---- merged log (job-local ids) straight to HBM, first event per point
+  Ev *evo = out.ev + 2 * L;
+  for (int d = tid; d < kin; d += T) {
+    const int cp = m.cpos[d];
+    if (!(cp & (1 << 30))) continue;
+    const double t = m.st[d];
+    const unsigned w = m.sw[d];
+    const int idx = (cp & ~(1 << 30)) + bridges_before(t);
+    Ev o;
+    o.t = t;
+    o.a = swa(w);
+    o.b = swb(w);
+    o.c = swc(w);
+    o.kind = swk(w);
+    evo[idx] = o;
+    atomicMin(&m.cur[o.b], idx);
+  }
+  for (int i = tid; i < NB; i += T) {
+    const double t = m.bt[i];
+    int lo = 0, hi = kin;  // first child event after t
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (m.st[mid] < t) lo = mid + 1; else hi = mid;
+    }
+    const int idx = i + (m.cpos[lo] & ~(1 << 30));
+    const unsigned w = m.bw[i];
+    Ev o;
+    o.t = t;
+    o.a = swa(w);
+    o.b = swb(w);
+    o.c = swc(w);
+    o.kind = swk(w);
+    evo[idx] = o;
+    atomicMin(&m.cur[o.b], idx);
+  }
+  __syncthreads();
+  // ---- start-of-time links + compaction
+  {
+    const int per = (nS + T) / T;
+    int local[PER];
+    int sum = 0;
+    for (int q = 0; q < per && q < PER; ++q) {
+      const int p = tid * per + q;
+      int keep = 0;
+      if (p < nS) {
+        const short2 l = m.LN[p];
+        bool chain = p == 0 || p == nSL || (l.x != NIL && m.LN[l.x].y == p);
+        chain = chain && (p < nSL ? p <= uv0.x : p >= uv0.y);
+        const int f = m.cur[p];
+        keep = chain || f != 0x7fffffff;
+        short2 o = make_short2(NIL, NIL);
+        if (chain) {
+          o = l;
+          if (p == uv0.x) o.y = static_cast<short>(uv0.y);
+          if (p == uv0.y) o.x = static_cast<short>(uv0.x);
+        } else if (keep) {
+          const Ev e = evo[f];
+          o = make_short2(static_cast<short>(e.a), static_cast<short>(e.c));
+        }
+        m.KL[p] = o;
+      }
+      local[q] = keep;
+      sum += keep;
+    }
+    int off;
+    Scan(m.scan).ExclusiveSum(sum, off);
+    for (int q = 0; q < per && q < PER; ++q) {
+      const int p = tid * per + q;
+      if (p <= nS) m.nid[p] = local[q] ? off : -1;
+      off += local[q];
+    }
+    if (tid == T - 1) m.sbn[MINI_S] = off;  // kept points
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int p = tid; p < nS; p += T) {
+    const int id = m.nid[p];
+    if (id < 0) continue;
+    const short2 l = m.KL[p];
+    int2 o;
+    o.x = l.x == NIL ? NIL : m.nid[l.x];
+    o.y = l.y == NIL ? NIL : m.nid[l.y];
+    bad |= (l.x != NIL && o.x < 0) | (l.y != NIL && o.y < 0);
+    out.lnk[L + id] = o;
+    out.gid[L + id] = m.G[p];
+  }
+  for (int e = tid; e < kout; e += T) {
+    Ev o = evo[e];
+    o.a = m.nid[o.a];
+    o.b = m.nid[o.b];
+    o.c = m.nid[o.c];
+    bad |= (o.a < 0) | (o.b < 0) | (o.c < 0);
+    evo[e] = o;
+  }
+  if (bad) raise_err(err, E_FASTPATH);
+  if (tid == 0) out.hdr[j] = make_int2(m.sbn[MINI_S], kout);
+}
+
+template <int T, int K, int N>
+static long long launch_mini(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
+                             long long j1, long long *err, cudaStream_t s) {
+  static bool attr = false;
+  const size_t bytes = sizeof(MiniSmem<T, K, N>);
+  if (!attr) {
+    if (h3d_check(cudaFuncSetAttribute(k_mini<T, K, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(bytes))))
+      return H3D_E_CUDA;
+    attr = true;
+  }
+  h3d_count_launches(1);
+  k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, bytes, s>>>(P, pts, n, lv, j0, j1, err);
+  return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
+}
+
+long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
+                     long long j1, long long *err, cudaStream_t s, int variant) {
+  if (variant == 0) return launch_mini<128, 512, 256>(P, pts, n, lv, j0, j1, err, s);
+  return launch_mini<512, 2048, 1024>(P, pts, n, lv, j0, j1, err, s);
+}
+
+}  // namespace h3d

@@ -77,6 +77,8 @@ def profile_enable(on: bool) -> None:
 
 def kernel_of(tag: int):
     """Decode a profile row's level tag -> (kernel name, level)."""
+    if tag >= 5000:
+        return "k_mini", tag - 5000
     if tag >= 4000:
         return "k_big_level", tag - 4000
     if tag >= 3000:

@@ -24,10 +24,12 @@ ROUTES = {
     "default": {},
     "no_leaf_no_big": {"leaf_b": 0, "big_kin": BIG_OFF},
     "leaf4": {"leaf_b": 4},
-    "big_everywhere": {"big_kin": 16},
-    "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0},
+    "big_everywhere": {"big_kin": 16, "mini": 0},
+    "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0, "mini": 0},
     "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF},
-    "warp_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0},
+    "warp_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 0},
+    "mini_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
+                        "mini_ctas": BIG_OFF},
 }
 CLOUDS = [("ball", 3001), ("sphere", 20000), ("cube", 65537), ("gauss", 9999), ("sphere", 4097)]
 
@@ -58,7 +60,7 @@ def test_integer_cloud_pipeline(oracle_mod):
     then agrees)."""
     pts = integer_cloud(50000, 3)
     exp = oracle_mod.convex_hull_3d(pts)
-    with fast.tuned(big_kin=16):
+    with fast.tuned(big_kin=16, mini=0):
         r = H.convex_hull_3d(pts)
     assert np.array_equal(r.faces, exp.faces)
 

@@ -18,7 +18,8 @@ BIG = 1 << 40
 routes = {
     "default": {}, "leaf0": {"leaf_b": 0}, "leaf0_bigoff": {"leaf_b": 0, "big_kin": BIG},
     "tpj_all": {"tpj_min_jobs": 1, "big_kin": BIG, "leaf_b": 0},
-    "warp_all": {"tpj_min_jobs": BIG, "big_kin": BIG, "leaf_b": 0},
+    "warp_all": {"tpj_min_jobs": BIG, "big_kin": BIG, "leaf_b": 0, "mini": 0},
+    "mini_all": {"tpj_min_jobs": BIG, "big_kin": BIG, "leaf_b": 0, "mini": 1},
     "big_all": {"big_kin": 2, "leaf_b": 0},
     "leaf3_warp": {"tpj_min_jobs": BIG, "big_kin": BIG},
 }
