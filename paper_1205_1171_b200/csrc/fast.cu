@@ -427,8 +427,10 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
       mx[r] = t > mx[r] ? t : mx[r];
     }
   }
+  // warp, then block reduction; one atomic per value per block
+  __shared__ unsigned long long red[32][10];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int o = 16; o; o >>= 1) ksum += __shfl_xor_sync(FULL, ksum, o);
-  if (lane == 0 && ksum) atomicAdd(out + 9, ksum);
 #pragma unroll
   for (int r = 0; r < 9; ++r) {
     unsigned long long m = mx[r];
@@ -436,7 +438,19 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
       const unsigned long long x = __shfl_xor_sync(FULL, m, o);
       m = x > m ? x : m;
     }
-    if (lane == 0 && m) atomicMax(out + r, m);
+    if (lane == 0) red[w][r] = m;
+  }
+  if (lane == 0) red[w][9] = ksum;
+  __syncthreads();
+  if (threadIdx.x < 10) {
+    unsigned long long m = 0;
+    for (int q = 0; q < nw; ++q) {
+      const unsigned long long x = red[q][threadIdx.x];
+      m = threadIdx.x == 9 ? m + x : (x > m ? x : m);
+    }
+    if (m) {
+      if (threadIdx.x == 9) atomicAdd(out + 9, m); else atomicMax(out + threadIdx.x, m);
+    }
   }
 }
 
@@ -1469,7 +1483,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     cudaMemsetAsync(w0.need, 0, 10 * sizeof(unsigned long long), s);
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
-    k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 65535 ? 65535 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
+    k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 2 * 148 ? 2 * 148 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
         P, n, lv, j0, j1, w0.need);
     unsigned long long need[10];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
