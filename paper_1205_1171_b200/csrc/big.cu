@@ -36,7 +36,7 @@
 
 namespace h3d {
 
-constexpr int SEG_MIN = 32;  // child events per time segment: chosen per level, >= SEG_MIN
+constexpr int SEG_MIN = 16;  // child events per time segment: chosen per level, >= SEG_MIN
 
 struct IncE {  // one incidence of a point: event index in S + links after it
   double t;
@@ -945,7 +945,12 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
     return H3D_E_CUDA;
   const long long kin = tot[0], pts_n = tot[1];
   // segment length: enough segments to give every SM a few warps
-  long long SEG = kin / (148 * 128) + 1;
+  static long long segs_per_sm = -1;
+  if (segs_per_sm < 0) {
+    segs_per_sm = 512;
+    if (const char *e = getenv("H3D_BIG_SEGS")) segs_per_sm = atoll(e);
+  }
+  long long SEG = kin / (148 * segs_per_sm) + 1;
   if (SEG < SEG_MIN) SEG = SEG_MIN;
   h3d_count_launches(1);
   k_big_segs<<<grid_of(J2 + 1), 256, 0, s>>>(J, W, static_cast<int>(SEG));
