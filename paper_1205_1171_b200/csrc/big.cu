@@ -91,6 +91,8 @@ struct BigWS {
   int *ibeg, *iend;
   int *first, *keep, *newid;
   int2 *ltmp;
+  int *pjob;   // job of each compact point
+  int *gjob;   // job of each compact child event
   // per segment
   int2 *segst;
   int *bcnt, *boff;
@@ -139,6 +141,8 @@ static bool carve_big(h3d_arena &ar, long long m, BigWS &b) {
   b.keep = ar.take<int>(EP + 1);
   b.newid = ar.take<int>(EP + 1);
   b.ltmp = ar.take<int2>(EP);
+  b.pjob = ar.take<int>(EP);
+  b.gjob = ar.take<int>(EK);
   b.segst = ar.take<int2>(NS + 1);
   b.bcnt = ar.take<int>(NS + 1);
   b.boff = ar.take<int>(NS + 1);
@@ -295,6 +299,7 @@ __global__ void k_big_seq(Pass2 P, long long n, int lv, long long j0, long long 
   const int total = W.jkinoff[J2];
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
     const int jb = find_job(W.jkinoff, J2, g);
+    W.gjob[g] = jb;
     const JobRef r = job_ref(P, jb, J, j0, lv, n);
     const int d = g - W.jkinoff[jb];
     const int kL = r.kL, kR = W.jkin[jb] - kL;
@@ -324,6 +329,15 @@ __global__ void k_big_seq(Pass2 P, long long n, int lv, long long j0, long long 
   }
 }
 
+// job of every compact point (one binary search per point, reused by the
+// fill, keep and write kernels)
+__global__ void k_big_pjob(long long J, BigWS W) {
+  const int J2 = static_cast<int>(2 * J);
+  const int total = W.jnsoff[J2];
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x)
+    W.pjob[x] = find_job(W.jnsoff, J2, x);
+}
+
 // ------------------------------------------------ K4 incidence list bounds
 __global__ void k_big_incidx(const unsigned *__restrict__ key, int E, BigWS W) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < E; k += gridDim.x * blockDim.x) {
@@ -346,7 +360,7 @@ __global__ void k_big_fill_init(Pass2 P, long long n, int lv, long long j0, long
   const int J2 = static_cast<int>(2 * J);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < E; k += gridDim.x * blockDim.x) {
     const int x = static_cast<int>(key[k]);
-    const int jb = find_job(W.jnsoff, J2, x);
+    const int jb = W.pjob[x];
     const int p = x - W.jnsoff[jb];
     const Ev e = W.seq[val[k]];
     const bool ins = (e.kind & 1) == EV_INS;
@@ -373,7 +387,7 @@ __global__ void k_big_fill_final(Pass2 P, long long n, int lv, long long j0, lon
   const int J2 = static_cast<int>(2 * J);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < E; k += gridDim.x * blockDim.x) {
     const int x = static_cast<int>(key[k]);
-    const int jb = find_job(W.jnsoff, J2, x);
+    const int jb = W.pjob[x];
     const int p = x - W.jnsoff[jb];
     const unsigned long long sv = W.sc1[k];
     int2 l = make_int2(NIL, NIL);
@@ -741,7 +755,7 @@ __global__ void k_big_emit(long long J, BigWS W, long long *err) {
   const int J2 = static_cast<int>(2 * J);
   const int total = W.jkinoff[J2];
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
-    const int jb = find_job(W.jkinoff, J2, g);
+    const int jb = W.gjob[g];
     const Ev e = W.seq[g];
     const int2 br = job_bridges(W, jb);
     const int nbf = bridges_before(W, br.x, br.y, e.t);
@@ -773,7 +787,7 @@ __global__ void k_big_out(Pass2 P, long long n, int lv, long long j0, long long 
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total + nbtot; g += stride) {
     if (g < total) {  // a kept child event
       if (!W.em[g]) continue;
-      const int jb = find_job(W.jkinoff, J2, g);
+      const int jb = W.gjob[g];
       const JobRef r = job_ref(P, jb, J, j0, lv, n);
       const Ev e = W.seq[g];
       const int2 br = job_bridges(W, jb);
@@ -836,7 +850,7 @@ __global__ void k_big_keep(Pass2 P, long long n, int lv, long long j0, long long
   const int J2 = static_cast<int>(2 * J);
   const int total = W.jnsoff[J2];
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
-    const int jb = find_job(W.jnsoff, J2, x);
+    const int jb = W.pjob[x];
     const JobRef r = job_ref(P, jb, J, j0, lv, n);
     const int p = x - W.jnsoff[jb];
     const int2 uv = W.ju0v0[jb];
@@ -872,7 +886,7 @@ __global__ void k_big_write(Pass2 P, long long n, int lv, long long j0, long lon
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < ptot + etot; x += stride) {
     if (x < ptot) {
       if (!W.keep[x]) continue;
-      const int jb = find_job(W.jnsoff, J2, x);
+      const int jb = W.pjob[x];
       const JobRef r = job_ref(P, jb, J, j0, lv, n);
       const int pb = W.jnsoff[jb], nb = W.newid[pb];
       const int p = x - pb;
@@ -965,6 +979,7 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   }
   h3d_count_launches(9);
   k_big_fill_first<<<grid_of(pts_n), 256, 0, s>>>(W, static_cast<int>(pts_n));
+  k_big_pjob<<<grid_of(pts_n), 256, 0, s>>>(J, W);
   k_big_seq<<<grid_of(kin), 256, 0, s>>>(P, n, lv, j0, J, W);
   // incidence lists: stable sort of (point, event) pairs by point
   {
