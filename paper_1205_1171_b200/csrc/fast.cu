@@ -539,6 +539,7 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
   };
   // ---- stage (cooperative, coalesced; U elements per lane in flight)
   constexpr int U = 4;
+  int js = 0;
   for (int x0 = 0; x0 < tot_pts; x0 += 32 * U) {
     int jj[U], p[U];
     long long src[U];
@@ -547,7 +548,9 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const int x = x0 + q * 32 + lane;
-      jj[q] = job_of(s_pre, x < tot_pts ? x : tot_pts - 1);
+      const int xc = x < tot_pts ? x : tot_pts - 1;
+      while (s_pre[js + 1] <= xc) ++js;  // the job index only advances
+      jj[q] = js;
       p[q] = x - s_pre[jj[q]];
       const int m_nSL = s_nSL[jj[q]];
       src[q] = p[q] < m_nSL ? s_L[jj[q]] + p[q] : s_M[jj[q]] + (p[q] - m_nSL);
@@ -647,8 +650,10 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
   // remapped in place
   bool bad = false;
   const int tot_p2 = s_pre[32], tot_ev = s_epre[32];
+  int jw = 0;
   for (int x = lane; x < tot_p2; x += 32) {
-    const int jj = job_of(s_pre, x);
+    while (s_pre[jw + 1] <= x) ++jw;  // the job index only advances
+    const int jj = jw;
     const int p = x - s_pre[jj];
     const TpjSlice<XYZ> T(smem + s_off[jj], s_pre[jj + 1] - s_pre[jj]);
     const unsigned id = T.fi[p];
@@ -661,18 +666,34 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
     out.lnk[s_L[jj] + id] = o;
     out.gid[s_L[jj] + id] = T.gd[p];
   }
-  for (int x = lane; x < tot_ev; x += 32) {
-    const int jj = job_of(s_epre, x);
-    const int e = x - s_epre[jj];
-    const TpjSlice<XYZ> T(smem + s_off[jj], s_pre[jj + 1] - s_pre[jj]);
-    Ev *evo = out.ev + 2 * s_L[jj];
-    Ev o = evo[e];
-    const unsigned na = T.fi[o.a], nb = T.fi[o.b], nc = T.fi[o.c];
-    bad |= (na == FULL) | (nb == FULL) | (nc == FULL);
-    o.a = static_cast<int>(na);
-    o.b = static_cast<int>(nb);
-    o.c = static_cast<int>(nc);
-    evo[e] = o;
+  {  // events: 4 read-backs in flight per lane; the job index only advances
+    int jj = 0;
+    for (int x0 = 0; x0 < tot_ev; x0 += 4 * 32) {
+      int jq[4];
+      Ev *ptr[4];
+      Ev o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int x = x0 + q * 32 + lane;
+        if (x < tot_ev) {
+          while (s_epre[jj + 1] <= x) ++jj;
+          jq[q] = jj;
+          ptr[q] = out.ev + 2 * s_L[jj] + (x - s_epre[jj]);
+          o[q] = *ptr[q];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (x0 + q * 32 + lane >= tot_ev) continue;
+        const TpjSlice<XYZ> T(smem + s_off[jq[q]], s_pre[jq[q] + 1] - s_pre[jq[q]]);
+        const unsigned na = T.fi[o[q].a], nb = T.fi[o[q].b], nc = T.fi[o[q].c];
+        bad |= (na == FULL) | (nb == FULL) | (nc == FULL);
+        o[q].a = static_cast<int>(na);
+        o[q].b = static_cast<int>(nb);
+        o[q].c = static_cast<int>(nc);
+        *ptr[q] = o[q];
+      }
+    }
   }
   if (__any_sync(FULL, bad) && lane == 0) raise_err(err, E_FASTPATH);
 }
