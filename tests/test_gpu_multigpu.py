@@ -54,12 +54,15 @@ def _worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_distributed_equals_single_gpu(world, large_json):
     import paper_1205_1171_b200 as H
     from paper_1205_1171_b200.generators import generate
 
-    cases = [(1000, "ball", 1), (3 * 1024 + 7, "sphere", 2), (5000, "cube", 3), (2**20, "ball", 0)]
+    # the 2^18 sphere sends its cross-rank levels through the time-split
+    # pipeline (large merged logs), the others through the mini/warp merges
+    cases = [(1000, "ball", 1), (3 * 1024 + 7, "sphere", 2), (5000, "cube", 3), (2**20, "ball", 0),
+             (2**18, "sphere", 5)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
