@@ -139,6 +139,17 @@ def orient_remap(sorted_pts: torch.Tensor, order: torch.Tensor, raw: torch.Tenso
     return verts[:h], faces
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device result -> numpy.  Large results go through a fresh pinned
+    buffer (the returned array owns it): a pageable copy of a sphere's 2M
+    faces costs ~2x more (tools/d2h_probe.py)."""
+    if t.numel() * t.element_size() < (1 << 20):
+        return t.cpu().numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+
+
 def _to_device(points, dev: torch.device) -> torch.Tensor:
     if isinstance(points, torch.Tensor):
         t = points.to(dtype=torch.float64)
@@ -258,7 +269,7 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
                                                 (lower_levels, upper_levels))
     verts, faces = orient_remap(sorted_pts, order, raw)
     if not return_device:
-        verts, faces = verts.cpu().numpy(), faces.cpu().numpy()
+        verts, faces = to_host(verts), to_host(faces)
     total_ms = (time.perf_counter() - total_t0) * 1e3
     stats = HullStats(n=n, levels=level_count(n), lower_events=int(k_lo),
                       upper_events=int(k_up), sort_ms=sort_ms, lower_ms=lo_ms,

@@ -254,7 +254,7 @@ def convex_hull_3d_distributed(points, device=None, return_device: bool = False)
     import numpy as np
     import torch.distributed as dist
 
-    from .api import HullResult, HullStats, _to_device, convex_hull_3d, orient_remap
+    from .api import HullResult, HullStats, _to_device, convex_hull_3d, orient_remap, to_host
     from .engine import level_count
 
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -276,7 +276,7 @@ def convex_hull_3d_distributed(points, device=None, return_device: bool = False)
                       sort_ms=0.0, lower_ms=0.0, upper_ms=0.0, total_ms=total_ms,
                       perturbed=perturbed, solver="parallel", workers=world)
     if not return_device:
-        verts, faces = verts.cpu().numpy(), faces.cpu().numpy()
+        verts, faces = to_host(verts), to_host(faces)
     return HullResult(vertices=verts, faces=faces, stats=stats)
 
 
