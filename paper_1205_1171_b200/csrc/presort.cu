@@ -52,25 +52,6 @@ __global__ void k_adjacent_tie(const unsigned long long *__restrict__ keys, long
 // longer than RUN_MAX sends the sort to the 64-bit path.
 constexpr int RUN_MAX = 64;
 
-__global__ void k_xminmax(const double *__restrict__ pts, long long n, unsigned long long *mm) {
-  unsigned long long lo = ~0ull, hi = 0ull;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long k = order_key(pts[3 * i]);
-    lo = k < lo ? k : lo;
-    hi = k > hi ? k : hi;
-  }
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
-    lo = a < lo ? a : lo;
-    hi = b > hi ? b : hi;
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin(mm, lo);
-    atomicMax(mm + 1, hi);
-  }
-}
-
 __device__ __forceinline__ double key_to_double(unsigned long long k) {
   const unsigned long long b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
   return __longlong_as_double(static_cast<long long>(b));
@@ -122,24 +103,47 @@ __global__ void k_tiefix(const double *__restrict__ pts, const unsigned *__restr
   }
 }
 
-// adjacent equal x in the sorted order (through the permutation)
-__global__ void k_adjacent_tie_perm(const double *__restrict__ pts, const int *__restrict__ perm,
-                                    long long n, int *flag) {
-  for (long long i = 1 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+// one pass over the input: any non-finite coordinate (api.py:192-193), the
+// x range (order keys) for the fixed-point sort keys, and max |coordinate|
+// (the degeneracy scan's scale, api.py:122; valid while no tie perturbs x)
+__global__ void k_scan_input(const double *__restrict__ pts, long long n, int *nonfinite,
+                             unsigned long long *mm, unsigned long long *absmax_bits) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  double amax = 0.0;
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    if (pts[3ll * perm[i]] == pts[3ll * perm[i - 1]]) {
-      *flag = 1;
-      return;
-    }
+    const double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+    bad |= !isfinite(x) || !isfinite(y) || !isfinite(z);
+    const unsigned long long k = order_key(x);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+    amax = fmax(amax, fmax(fabs(x), fmax(fabs(y), fabs(z))));
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o),
+                             b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+    atomicMax(absmax_bits, static_cast<unsigned long long>(__double_as_longlong(amax)));
+    if (bad) *nonfinite = 1;
   }
 }
 
 __global__ void k_gather_rows(const double *__restrict__ pts, const int *__restrict__ perm,
                               long long n, double *out, long long *order,
-                              const int *__restrict__ outer) {
+                              const int *__restrict__ outer, int *tie = nullptr) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const long long r = perm[i];
+    // adjacent equal x in the sorted order (the reference's tie test)
+    if (tie && i > 0 && pts[3 * r] == pts[3ll * perm[i - 1]]) *tie = 1;
     out[3 * i] = pts[3 * r];
     out[3 * i + 1] = pts[3 * r + 1];
     out[3 * i + 2] = pts[3 * r + 2];
@@ -253,16 +257,6 @@ __global__ void k_degenerate(const double *__restrict__ P, long long n, ScanStat
       return;
     }
   }
-}
-
-// any non-finite coordinate (api.py:192-193 rejects them before sorting)
-__global__ void k_nonfinite(const double *__restrict__ p, long long m, int *flag) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
-       i += (long long)gridDim.x * blockDim.x)
-    if (!isfinite(p[i])) {
-      *flag = 1;
-      return;
-    }
 }
 
 __global__ void k_scan_init(ScanState *st) {
@@ -424,15 +418,15 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   int *vs;
   *perturbed = 0;
 
-  // finiteness first, as the reference validates before sorting
+  // finiteness, x range and |coordinate| scale in one pass over the input
   cudaMemsetAsync(w.flag, 0, sizeof(int) * 4, s);
   h3d_count_launches(1);
-  k_nonfinite<<<G, 256, 0, s>>>(pts, 3 * n, w.flag + 1);
-  // stable argsort of x (api.py:97): 32-bit fixed-point keys + tie-run fix
+  k_scan_init<<<1, 1, 0, s>>>(w.scan);
   unsigned long long mm_init[2] = {~0ull, 0ull};
   cudaMemcpyAsync(w.mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, s);
   h3d_count_launches(4);
-  k_xminmax<<<G, 256, 0, s>>>(pts, n, w.mm);
+  k_scan_input<<<G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
+  // stable argsort of x (api.py:97): 32-bit fixed-point keys + tie-run fix
   unsigned *k32a = reinterpret_cast<unsigned *>(w.k0), *k32b = reinterpret_cast<unsigned *>(w.k1);
   k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, w.v0);
   {
@@ -445,7 +439,9 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     vs = vb.Current();
     k_tiefix<<<G, 256, 0, s>>>(pts, kb.Current(), vs, n, w.flag + 2);
   }
-  k_adjacent_tie_perm<<<G, 256, 0, s>>>(pts, vs, n, w.flag);
+  // rows in x order, with the adjacent-tie test folded in (rare ties:
+  // the rows are rebuilt by the lexsort/perturbation path below)
+  k_gather_rows<<<G, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, nullptr, w.flag);
   int hflag[3] = {0, 0, 0};
   if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
       h3d_check(cudaStreamSynchronize(s)))
@@ -460,12 +456,13 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     if (h3d_check(cudaMemcpyAsync(hflag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
+    if (!hflag[0]) {
+      h3d_count_launches(1);
+      k_gather_rows<<<G, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, nullptr);
+    }
   }
   const int tie = hflag[0];
-  if (!tie) {
-    h3d_count_launches(1);
-    k_gather_rows<<<G, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, nullptr);
-  } else {
+  if (tie) {
     // lexsort (x, y, z): stable LSD passes on z, then y, then x (api.py:86-87)
     int *perm = nullptr;
     h3d_count_launches(1);
@@ -504,12 +501,12 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     h3d_count_launches(1);
     k_adjacent_tie<<<G, 256, 0, s>>>(ks, n, w.flag);
     *perturbed = 1;
+    // the perturbation changed x: the scale is re-taken on the sorted rows
+    h3d_count_launches(2);
+    k_scan_init<<<1, 1, 0, s>>>(w.scan);
+    k_absmax<<<G, 256, 0, s>>>(sorted_pts, 3 * n, &w.scan->scale_bits);
   }
   // _scan_degenerate on the sorted rows (api.py:113-147)
-  h3d_count_launches(1);
-  k_scan_init<<<1, 1, 0, s>>>(w.scan);
-  h3d_count_launches(1);
-  k_absmax<<<G, 256, 0, s>>>(sorted_pts, 3 * n, &w.scan->scale_bits);
   // each stage scans the first 16K rows with a small grid and the rest only
   // when they hold no hit (random inputs stop in the first block, as the
   // reference's block-wise scan does)
