@@ -33,13 +33,17 @@ struct MiniSmem {
   short2 KL[MINI_N];            // rebuilt links
   int ib[MINI_N + 1];           // incidence list bounds (exclusive scan)
   int cur[MINI_N];              // scatter cursors, then first output event
-  short ei[3 * MINI_K];         // incidence: event index
+  short ei[3 * MINI_K];         // incidence: event index (each list in event order)
+  short eo[3 * MINI_K];         // incidence: scattered event index (before ordering)
   short2 el[3 * MINI_K];        // incidence: links after the event
   int cpos[MINI_K + 1];         // kept child events: flags, then exclusive scan
   int nid[MINI_N + 1];          // keep flags, then new ids (exclusive scan)
   double bt[MINI_B];            // bridge events: time
   unsigned bw[MINI_B];          //   facet a | b << 10 | c << 20 | kind << 30
   short2 buv[MINI_B];           //   feet after
+  double slt[MINI_B];           // per-segment slabs of the sweep (then compacted)
+  unsigned slw[MINI_B];
+  short2 sluv[MINI_B];
   short2 sst[MINI_S];           // segment start bridges
   int sbn[MINI_S + 1];          // bridge events per segment, then offsets
   int flag, nb;
@@ -95,7 +99,7 @@ __device__ __forceinline__ bool mturn_neg_at(const MS &m, int a, int b, int c, d
 // the sequential core of one segment (see big.cu k_big_sweep); MODE 0
 // counts, MODE 1 writes.  Returns false on an exact tie.
 template <int MODE, class MS>
-__device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int *nb_out,
+__device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int cap, int *nb_out,
                            int2 *end_uv) {
   const int pos0 = s * seg, pos1 = (pos0 + seg < kin) ? pos0 + seg : kin;
   const double tend = (s == nseg - 1) ? INF : m.st[pos1 - 1];
@@ -107,7 +111,7 @@ __device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int *nb_out
   double c2 = mevt(m, u, un, v), c3 = mevt(m, up, u, v);
   double c4 = mevt(m, u, v, vn), c5 = mevt(m, u, vp, v);
   int nb = 0;
-  const int base = (MODE == 1) ? m.sbn[s] : 0;
+  const int base = (MODE == 1) ? m.sbn[s] : s * cap;
   for (;;) {
     double tu = INF, tv = INF;
     if (cu < m.ib[u + 1] && m.ei[cu] < pos1) tu = m.st[m.ei[cu]];
@@ -170,11 +174,16 @@ __device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int *nb_out
         const short2 l = mlinks(m, v, pos, &cv);
         vp = l.x; vn = l.y;
       }
+      const unsigned bw = static_cast<unsigned>(a) | (static_cast<unsigned>(b) << 10) |
+                          (static_cast<unsigned>(c) << 20) | (static_cast<unsigned>(kind) << 30);
       if (MODE == 1 && base + nb < MS::MINI_B) {
         m.bt[base + nb] = best;
-        m.bw[base + nb] = static_cast<unsigned>(a) | (static_cast<unsigned>(b) << 10) |
-                          (static_cast<unsigned>(c) << 20) | (static_cast<unsigned>(kind) << 30);
+        m.bw[base + nb] = bw;
         m.buv[base + nb] = make_short2(static_cast<short>(u), static_cast<short>(v));
+      } else if (MODE == 0 && nb < cap) {
+        m.slt[base + nb] = best;
+        m.slw[base + nb] = bw;
+        m.sluv[base + nb] = make_short2(static_cast<short>(u), static_cast<short>(v));
       }
       ++nb;
       c2 = mevt(m, u, un, v);
@@ -243,18 +252,24 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     m.LN[p] = make_short2(static_cast<short>(l.x), static_cast<short>(l.y));
     m.cur[p] = 0;
   }
-  // ---- merged child sequence S (merge path, left first on equal times)
+  // ---- merged child sequence S (merge path, left first on equal times);
+  // the child times are staged in shared memory first (the bridge-event
+  // arrays are free until the sweeps) so the co-rank searches stay on chip
   const Ev *evL = in.ev + 2 * L, *evR = in.ev + 2 * M;
+  double *tL = m.bt, *tR = m.bt + kL;
+  for (int d = tid; d < kL; d += T) tL[d] = evL[d].t;
+  for (int d = tid; d < kR; d += T) tR[d] = evR[d].t;
+  __syncthreads();
   for (int d = tid; d < kin; d += T) {
     int lo = d - kR > 0 ? d - kR : 0, hi = d < kL ? d : kL;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (evL[mid].t <= evR[d - mid - 1].t) lo = mid + 1; else hi = mid;
+      if (tL[mid] <= tR[d - mid - 1]) lo = mid + 1; else hi = mid;
     }
     const int i = lo, jj = d - lo;
     Ev o;
     unsigned side = 0;
-    if (i < kL && (jj >= kR || evL[i].t <= evR[jj].t)) {
+    if (i < kL && (jj >= kR || tL[i] <= tR[jj])) {
       o = evL[i];
     } else {
       o = evR[jj];
@@ -298,24 +313,34 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   __syncthreads();
   for (int p = tid; p < nS; p += T) m.cur[p] = m.ib[p];
   __syncthreads();
+  // scatter (arbitrary order within a list; the owner kept alongside) ...
   for (int d = tid; d < kin; d += T) {
     const unsigned w = m.sw[d];
-    m.ei[atomicAdd(&m.cur[swa(w)], 1)] = static_cast<short>(d);
-    m.ei[atomicAdd(&m.cur[swb(w)], 1)] = static_cast<short>(d);
-    m.ei[atomicAdd(&m.cur[swc(w)], 1)] = static_cast<short>(d);
+    const int pa = swa(w), pb = swb(w), pc = swc(w);
+    int q = atomicAdd(&m.cur[pa], 1);
+    m.eo[q] = static_cast<short>(d);
+    m.el[q].x = static_cast<short>(pa);
+    q = atomicAdd(&m.cur[pb], 1);
+    m.eo[q] = static_cast<short>(d);
+    m.el[q].x = static_cast<short>(pb);
+    q = atomicAdd(&m.cur[pc], 1);
+    m.eo[q] = static_cast<short>(d);
+    m.el[q].x = static_cast<short>(pc);
+  }
+  __syncthreads();
+  // ... then every entry placed at its rank within its list (event order),
+  // all entries in parallel (a list of L entries costs L reads per entry,
+  // not a sequential L^2 sort)
+  for (int k = tid; k < 3 * kin; k += T) {
+    const int p = m.el[k].x, b0 = m.ib[p], b1 = m.ib[p + 1];
+    const short x = m.eo[k];
+    int rank = 0;
+    for (int q = b0; q < b1; ++q) rank += m.eo[q] < x;
+    m.ei[b0 + rank] = x;
   }
   __syncthreads();
   for (int p = tid; p < nS; p += T) {
     const int b0 = m.ib[p], b1 = m.ib[p + 1];
-    for (int a = b0 + 1; a < b1; ++a) {  // insertion sort by event index (lists are short)
-      const short x = m.ei[a];
-      int b = a - 1;
-      while (b >= b0 && m.ei[b] > x) {
-        m.ei[b + 1] = m.ei[b];
-        --b;
-      }
-      m.ei[b + 1] = x;
-    }
     short2 l = m.LN[p];
     for (int k = b0; k < b1; ++k) {  // links after each incidence (forward fill)
       const unsigned w = m.sw[m.ei[k]];
@@ -361,34 +386,32 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
         break;
       }
     } else {  // just after the last child event before the segment
+      // both candidate moves are evaluated every step (the v-advance wins,
+      // as in _find_bridge) so the warp's walks stay converged
       const int pos = s * seg;
       const double T0 = m.st[pos - 1];
       int dummy;
       for (;;) {
         const int vn = mlinks(m, v, pos, &dummy).y;
-        if (vn != NIL && mturn_neg_at(m, u, v, vn, T0)) {
-          v = vn;
-          if (++moves > limit) { bad = true; break; }
-          continue;
-        }
         const int up = mlinks(m, u, pos, &dummy).x;
-        if (up != NIL && mturn_neg_at(m, up, u, v, T0)) {
-          u = up;
-          if (++moves > limit) { bad = true; break; }
-          continue;
-        }
-        break;
+        const bool mv = vn != NIL && mturn_neg_at(m, u, v, vn, T0);
+        const bool mu = up != NIL && mturn_neg_at(m, up, u, v, T0);
+        if (!mv && !mu) break;
+        if (mv) v = vn; else u = up;
+        if (++moves > limit) { bad = true; break; }
       }
     }
     if (bad) m.flag = 1;
     m.sst[s] = make_short2(static_cast<short>(u), static_cast<short>(v));
   }
   __syncthreads();
-  // ---- segment sweeps: count, offsets, write
+  // ---- segment sweeps (bridge events to per-segment slabs), offsets,
+  // compaction; a segment whose slab overflowed is swept again in place
+  const int cap = MINI_B / nseg;
   if (tid < nseg) {
     int nb;
     int2 e;
-    if (!mini_sweep<0>(m, tid, nseg, seg, kin, &nb, &e)) m.flag = 1;
+    if (!mini_sweep<0>(m, tid, nseg, seg, kin, cap, &nb, &e)) m.flag = 1;
     if (tid + 1 < nseg && (m.sst[tid + 1].x != e.x || m.sst[tid + 1].y != e.y)) m.flag = 1;
     m.sbn[tid] = nb;
   }
@@ -409,10 +432,19 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     if (tid == 0) raise_err(err, E_FASTPATH);
     return;
   }
-  if (tid < nseg) {
+  for (int q = tid; q < nseg * cap; q += T) {  // slabs -> compact arrays
+    const int sg = q / cap, r = q - sg * cap;
+    const int cnt = m.sbn[sg + 1] - m.sbn[sg];
+    if (cnt <= cap && r < cnt) {
+      m.bt[m.sbn[sg] + r] = m.slt[q];
+      m.bw[m.sbn[sg] + r] = m.slw[q];
+      m.buv[m.sbn[sg] + r] = m.sluv[q];
+    }
+  }
+  if (tid < nseg && m.sbn[tid + 1] - m.sbn[tid] > cap) {
     int nb;
     int2 e;
-    mini_sweep<1>(m, tid, nseg, seg, kin, &nb, &e);
+    mini_sweep<1>(m, tid, nseg, seg, kin, cap, &nb, &e);
   }
   __syncthreads();
   const int NB = m.nb;
