@@ -480,22 +480,18 @@ __global__ void k_big_walk(Pass2 P, const double *__restrict__ pts, long long n,
       }
       W.ju0v0[jb] = make_int2(u, v);
     } else {  // just after the last child event before the segment
+      // both candidate moves are evaluated every step (the v-advance wins,
+      // as in _find_bridge): the lanes' load chains stay converged
       const int pos = s * SEG;
       const double T = W.seq[gbase + pos - 1].t;
       for (;;) {
         const int vn = links_at(r, W, pbase, v, pos).y;
-        if (vn != NIL && turn_neg_at(r, pts, u, v, vn, T)) {
-          v = vn;
-          if (++moves > limit) { bad = true; break; }
-          continue;
-        }
         const int up = links_at(r, W, pbase, u, pos).x;
-        if (up != NIL && turn_neg_at(r, pts, up, u, v, T)) {
-          u = up;
-          if (++moves > limit) { bad = true; break; }
-          continue;
-        }
-        break;
+        const bool mv = vn != NIL && turn_neg_at(r, pts, u, v, vn, T);
+        const bool mu = up != NIL && turn_neg_at(r, pts, up, u, v, T);
+        if (!mv && !mu) break;
+        if (mv) v = vn; else u = up;
+        if (++moves > limit) { bad = true; break; }
       }
     }
     if (bad) raise_err(err, E_FASTPATH);
