@@ -51,6 +51,7 @@ extern "C" {
 #define H3D_E_NOFACETS (-10)     /* DegenerateInputError (api.py:253-256)   */
 #define H3D_E_CAPACITY (-11)     /* fast-path fixed capacity exceeded       */
 #define H3D_E_NONFINITE (-12)   /* ValueError("coordinates must be finite") */
+#define H3D_E_FASTPATH (-13)     /* fast path declined: caller takes the exact route */
 #define H3D_E_ARG (-100)         /* bad argument                            */
 #define H3D_E_CUDA (-101)        /* CUDA runtime error                      */
 
@@ -144,6 +145,19 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts,
                     int64_t *order, void *workspace, size_t workspace_bytes,
                     int32_t *perturbed, void *stream);
 
+/* Sharded presort (multi-GPU): writes rows [q0, p1) of the global sorted
+ * order (sorted_pts / order, both full-size n) from the full input without
+ * sorting the rest: 32-bit keys, a radix select of the two window
+ * boundaries, exact ranking of the boundary key runs, a sort of the window.
+ * scan != 0 also runs _scan_degenerate over rows [0, p1) (rank 0, q0 = 0).
+ * Returns 0, or H3D_E_FASTPATH whenever the window cannot reproduce
+ * h3d_presort on its own (any x tie, a long run of equal keys, non-finite
+ * input, a degeneracy not decided inside the window): the caller then runs
+ * the replicated h3d_presort.  Needs n >= 2048. */
+int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1,
+                         int32_t scan, double *sorted_pts, int64_t *order,
+                         void *workspace, size_t workspace_bytes, void *stream);
+
 /* Epilogue (pkg/src/hull3d/api.py:252-266): faces_raw (F,3) i32 in sorted
  * indices (lower block then upper block) -> faces (F,3) i64 oriented outward
  * against the centroid and mapped through order; vertex_mark (n) i32 scratch;
@@ -153,6 +167,16 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n,
                          int64_t nfaces, int64_t *faces, int32_t *vertex_mark,
                          int64_t *vertices, void *workspace,
                          size_t workspace_bytes, void *stream);
+
+/* h3d_orient_remap with the centroid taken over centroid_pts (n rows, any
+ * order; nullptr = sorted_pts): the sharded multi-GPU path, whose rank 0
+ * holds only the rows its merges touched, passes the caller-order input. */
+int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n,
+                            const int64_t *order, const int32_t *faces_raw,
+                            int64_t nfaces, int64_t *faces,
+                            int32_t *vertex_mark, int64_t *vertices,
+                            const double *centroid_pts, void *workspace,
+                            size_t workspace_bytes, void *stream);
 
 /* Routing knobs of the fast path (not a reference interface; used by the
  * tests to drive every kernel route and by tuning sweeps): "big_kin"

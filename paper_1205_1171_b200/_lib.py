@@ -49,6 +49,8 @@ SIGNATURES: dict[str, tuple] = {
     "h3d_presort_workspace_bytes": (sz, [i64]),
     "h3d_presort": (i64, [vp, i64, vp, vp, vp, sz, vp, vp]),
     "h3d_orient_remap": (i64, [vp, i64, vp, vp, i64, vp, vp, vp, vp, sz, vp]),
+    "h3d_orient_remap_ex": (i64, [vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]),
+    "h3d_presort_slab": (i64, [vp, i64, i64, i64, ctypes.c_int32, vp, vp, vp, sz, vp]),
 }
 
 

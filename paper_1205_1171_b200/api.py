@@ -119,8 +119,11 @@ def presort(pts_dev: torch.Tensor):
     return sorted_pts, order, bool(pert.value)
 
 
-def orient_remap(sorted_pts: torch.Tensor, order: torch.Tensor, raw: torch.Tensor):
-    """Device api.py:252-266 -> (vertices i64, faces i64) on device."""
+def orient_remap(sorted_pts: torch.Tensor, order: torch.Tensor, raw: torch.Tensor,
+                 centroid_pts: torch.Tensor | None = None):
+    """Device api.py:252-266 -> (vertices i64, faces i64) on device.
+    centroid_pts: rows the centroid is taken over (default sorted_pts; the
+    sharded multi-GPU path passes the caller-order input)."""
     L = _lib.load()
     n = sorted_pts.shape[0]
     dev = sorted_pts.device
@@ -133,9 +136,10 @@ def orient_remap(sorted_pts: torch.Tensor, order: torch.Tensor, raw: torch.Tenso
     mark = torch.empty(n, dtype=torch.int32, device=dev)
     verts = torch.empty(n, dtype=torch.int64, device=dev)
     raw = raw.contiguous()
-    h = check_api(L.h3d_orient_remap(sorted_pts.data_ptr(), n, order.data_ptr(), raw.data_ptr(), F,
-                                     faces.data_ptr(), mark.data_ptr(), verts.data_ptr(),
-                                     ws.data_ptr(), ws.numel(), stream_ptr(dev)))
+    cen = centroid_pts.contiguous().data_ptr() if centroid_pts is not None else None
+    h = check_api(L.h3d_orient_remap_ex(sorted_pts.data_ptr(), n, order.data_ptr(), raw.data_ptr(),
+                                        F, faces.data_ptr(), mark.data_ptr(), verts.data_ptr(),
+                                        cen, ws.data_ptr(), ws.numel(), stream_ptr(dev)))
     return verts[:h], faces
 
 

@@ -57,20 +57,34 @@ __device__ __forceinline__ double key_to_double(unsigned long long k) {
   return __longlong_as_double(static_cast<long long>(b));
 }
 
+__device__ __forceinline__ unsigned fixed_key(double x, double lo, double sc) {
+  if (x == 0.0) x = 0.0;
+  double f = __dmul_rn(__dsub_rn(x, lo), sc);  // monotone in x
+  if (!(f >= 0.0)) f = 0.0;
+  if (f > 4294967295.0) f = 4294967295.0;
+  return static_cast<unsigned>(f);
+}
+
 __global__ void k_keys32(const double *__restrict__ pts, long long n,
                          const unsigned long long *__restrict__ mm, unsigned *keys, int *vals) {
   const double lo = key_to_double(mm[0]), hi = key_to_double(mm[1]);
   const double span = __dsub_rn(hi, lo);
   const double sc = span > 0.0 ? __ddiv_rn(4294967295.0, span) : 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    double x = pts[3 * i];
-    if (x == 0.0) x = 0.0;
-    double f = __dmul_rn(__dsub_rn(x, lo), sc);  // monotone in x
-    if (!(f >= 0.0)) f = 0.0;
-    if (f > 4294967295.0) f = 4294967295.0;
-    keys[i] = static_cast<unsigned>(f);
-    vals[i] = static_cast<int>(i);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {  // four loads in flight
+    double x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = pts[3 * (i + q * stride)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      keys[i + q * stride] = fixed_key(x[q], lo, sc);
+      if (vals) vals[i + q * stride] = static_cast<int>(i + q * stride);
+    }
+  }
+  for (; i < n; i += stride) {
+    keys[i] = fixed_key(pts[3 * i], lo, sc);
+    if (vals) vals[i] = static_cast<int>(i);
   }
 }
 
@@ -111,14 +125,63 @@ __global__ void k_scan_input(const double *__restrict__ pts, long long n, int *n
   unsigned long long lo = ~0ull, hi = 0ull;
   double amax = 0.0;
   bool bad = false;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
-    bad |= !isfinite(x) || !isfinite(y) || !isfinite(z);
-    const unsigned long long k = order_key(x);
-    lo = k < lo ? k : lo;
-    hi = k > hi ? k : hi;
-    amax = fmax(amax, fmax(fabs(x), fmax(fabs(y), fabs(z))));
+  // the (n,3) rows as a flat array read in 16-byte pairs; element e is an
+  // x coordinate iff e % 3 == 0
+  const long long m = 3 * n;
+  // (a row-offset view is only 8-byte aligned: one element per step then)
+  const bool vec = (reinterpret_cast<unsigned long long>(pts) & 15ull) == 0;
+  const long long pairs = vec ? (m >> 1) : 0;
+  const double2 *p2 = reinterpret_cast<const double2 *>(pts);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; !vec && e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double d = pts[e];
+    bad |= !isfinite(d);
+    amax = fmax(amax, fabs(d));
+    if (e % 3 == 0) {
+      const unsigned long long k = order_key(d);
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
+  }
+  const long long j0 = blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                  stride = (long long)gridDim.x * blockDim.x;
+  const int inc = static_cast<int>((2 * stride) % 3);
+  int r0 = static_cast<int>((2 * j0) % 3);  // phase of element 2j, kept incrementally
+  auto visit = [&](double d, int r) {
+    bad |= !isfinite(d);
+    amax = fmax(amax, fabs(d));
+    if (r == 0) {
+      const unsigned long long k = order_key(d);
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
+  };
+  auto step = [&](int &r) {
+    r += inc;
+    if (r >= 3) r -= 3;
+  };
+  long long j = j0;
+  if (vec) {
+    // four independent 16-byte loads in flight per thread
+    for (; j + 3 * stride < pairs; j += 4 * stride) {
+      double2 d[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d[q] = p2[j + q * stride];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r1 = r0 == 2 ? 0 : r0 + 1;
+        visit(d[q].x, r0);
+        visit(d[q].y, r1);
+        step(r0);
+      }
+    }
+    for (; j < pairs; j += stride) {
+      const double2 d = p2[j];
+      visit(d.x, r0);
+      visit(d.y, r0 == 2 ? 0 : r0 + 1);
+      step(r0);
+    }
+    if (j == pairs && (m & 1)) visit(pts[m - 1], r0);
   }
   for (int o = 16; o; o >>= 1) {
     const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o),
@@ -128,17 +191,38 @@ __global__ void k_scan_input(const double *__restrict__ pts, long long n, int *n
     amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   }
   bad = __any_sync(0xffffffffu, bad);
+  // block reduction, then one atomic of each kind per block
+  __shared__ unsigned long long s_lo[32], s_hi[32], s_am[32];
+  __shared__ int s_bad;
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
   if ((threadIdx.x & 31) == 0) {
-    atomicMin(mm, lo);
-    atomicMax(mm + 1, hi);
-    atomicMax(absmax_bits, static_cast<unsigned long long>(__double_as_longlong(amax)));
-    if (bad) *nonfinite = 1;
+    s_lo[w] = lo;
+    s_hi[w] = hi;
+    s_am[w] = static_cast<unsigned long long>(__double_as_longlong(amax));
+    if (bad) s_bad = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long L = s_lo[0], H = s_hi[0], A = s_am[0];
+    for (int i = 1; i < nw; ++i) {
+      L = s_lo[i] < L ? s_lo[i] : L;
+      H = s_hi[i] > H ? s_hi[i] : H;
+      A = s_am[i] > A ? s_am[i] : A;  // non-negative doubles order as bits
+    }
+    atomicMin(mm, L);
+    atomicMax(mm + 1, H);
+    atomicMax(absmax_bits, A);
+    if (s_bad) *nonfinite = 1;
   }
 }
 
 __global__ void k_gather_rows(const double *__restrict__ pts, const int *__restrict__ perm,
                               long long n, double *out, long long *order,
                               const int *__restrict__ outer, int *tie = nullptr) {
+  // random 24-byte rows: bound by DRAM efficiency of scattered reads (more
+  // rows in flight per thread measured no faster)
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const long long r = perm[i];
@@ -148,6 +232,196 @@ __global__ void k_gather_rows(const double *__restrict__ pts, const int *__restr
     out[3 * i + 1] = pts[3 * r + 1];
     out[3 * i + 2] = pts[3 * r + 2];
     if (order) order[i] = outer ? outer[r] : r;
+  }
+}
+
+// ---- sharded presort (multi-GPU): one rank's window [q0, p1) of the global
+// stable x order without sorting the other ranks' points.  The 32-bit keys of
+// every point are computed; a 3-pass radix select (11+11+10 bits) finds the
+// key K_b of the element at each window boundary b and its rank inside the
+// run of equal keys; elements strictly between the two boundary keys are
+// compacted, the (short) boundary runs are ranked by (64-bit order key,
+// index) exactly as k_tiefix orders them, and only the window is sorted.
+struct SelState {
+  unsigned pre[2];   // key prefix found so far, per boundary
+  long long rem[2];  // rank inside the prefix bucket still to skip
+  long long b[2];    // boundary positions (-1: none)
+  int count, nrun, bad, pad;
+};
+
+constexpr int kSelRunCap = 2 * RUN_MAX;
+
+__device__ __forceinline__ int sel_shift(int pass) { return pass == 0 ? 21 : (pass == 1 ? 10 : 0); }
+__device__ __forceinline__ int sel_bits(int pass) { return pass == 2 ? 10 : 11; }
+
+__global__ void k_sel_hist(const unsigned *__restrict__ k32, long long n,
+                           const SelState *__restrict__ st, int pass, unsigned *hist) {
+  __shared__ unsigned h[2][2048];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int sh = sel_shift(pass), hi = sh + sel_bits(pass);
+  const unsigned mask = (1u << sel_bits(pass)) - 1u;
+  const bool h0 = st->b[0] >= 0, h1 = st->b[1] >= 0;
+  const unsigned p0 = st->pre[0], p1 = st->pre[1];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned k = k32[i];
+    const unsigned top = hi >= 32 ? 0u : (k >> hi);
+    const unsigned d = (k >> sh) & mask;
+    if (h0 && top == p0) atomicAdd(&h[0][d], 1u);
+    if (h1 && top == p1) atomicAdd(&h[1][d], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) {
+    const unsigned v = (&h[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
+
+// one block of 256 threads, 8 bins each: the bucket holding each boundary's rank
+__global__ void k_sel_pick(unsigned *hist, SelState *st, int pass) {
+  typedef cub::BlockScan<long long, 256> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const int bins = 1 << sel_bits(pass);
+  const int t = threadIdx.x;
+  for (int b = 0; b < 2; ++b) {
+    const bool has = st->b[b] >= 0;
+    const long long rem = st->rem[b];
+    long long c[8], tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      c[q] = 8 * t + q < bins ? hist[(pass == 0 ? 0 : 2048 * b) + 8 * t + q] : 0;
+      tot += c[q];
+    }
+    long long before;
+    BS(tmp).ExclusiveSum(tot, before);
+    __syncthreads();
+    if (has && rem >= before && rem < before + tot) {
+      int d = 0;
+      while (rem >= before + c[d]) before += c[d++];
+      st->pre[b] = (st->pre[b] << sel_bits(pass)) | static_cast<unsigned>(8 * t + d);
+      st->rem[b] = rem - before;
+    }
+    __syncthreads();
+  }
+  for (int i = t; i < 4096; i += blockDim.x) hist[i] = 0;
+}
+
+// block-aggregated compaction: 8 keys per thread, one atomic per block tile
+constexpr int kSelItems = 8;
+
+__global__ void __launch_bounds__(256) k_sel_compact(const unsigned *__restrict__ k32, long long n,
+                                                     SelState *st, int *out, int *runs) {
+  typedef cub::BlockScan<int, 256> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int s_base;
+  const bool h0 = st->b[0] >= 0, h1 = st->b[1] >= 0;
+  const unsigned K0 = st->pre[0], K1 = st->pre[1];
+  const long long tile = 256ll * kSelItems;
+  for (long long base = blockIdx.x * tile; base < n; base += (long long)gridDim.x * tile) {
+    const long long i0 = base + (long long)threadIdx.x * kSelItems;
+    unsigned k[kSelItems];
+    if (i0 + kSelItems <= n) {
+      const uint4 a = *reinterpret_cast<const uint4 *>(k32 + i0);
+      const uint4 b = *reinterpret_cast<const uint4 *>(k32 + i0 + 4);
+      k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w;
+      k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSelItems; ++q) k[q] = i0 + q < n ? k32[i0 + q] : 0u;
+    }
+    int cnt = 0;
+    unsigned inm = 0;
+#pragma unroll
+    for (int q = 0; q < kSelItems; ++q) {
+      if (i0 + q >= n) continue;
+      const bool in = (!h0 || k[q] > K0) && (!h1 || k[q] < K1);
+      const bool run = (h0 && k[q] == K0) || (h1 && k[q] == K1);
+      inm |= (in ? 1u : 0u) << q;
+      cnt += in;
+      if (run) {
+        const int r = atomicAdd(&st->nrun, 1);
+        if (r < kSelRunCap) runs[r] = static_cast<int>(i0 + q);
+        else st->bad = 1;
+      }
+    }
+    int off, total;
+    BS(tmp).ExclusiveSum(cnt, off, total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(&st->count, total) : 0;
+    __syncthreads();
+    off += s_base;
+#pragma unroll
+    for (int q = 0; q < kSelItems; ++q)
+      if (inm >> q & 1u) out[off++] = static_cast<int>(i0 + q);
+    __syncthreads();
+  }
+}
+
+// k_keys32 fused with the first select pass (top 11 bits, every key)
+__global__ void k_keys32_hist(const double *__restrict__ pts, long long n,
+                              const unsigned long long *__restrict__ mm, unsigned *keys,
+                              unsigned *hist) {
+  __shared__ unsigned h[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const double lo = key_to_double(mm[0]), hi = key_to_double(mm[1]);
+  const double span = __dsub_rn(hi, lo);
+  const double sc = span > 0.0 ? __ddiv_rn(4294967295.0, span) : 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    double x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = pts[3 * (i + q * stride)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned k = fixed_key(x[q], lo, sc);  // the same key as k_keys32
+      keys[i + q * stride] = k;
+      atomicAdd(&h[k >> 21], 1u);
+    }
+  }
+  for (; i < n; i += stride) {
+    const unsigned k = fixed_key(pts[3 * i], lo, sc);
+    keys[i] = k;
+    atomicAdd(&h[k >> 21], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if (h[i]) atomicAdd(hist + i, h[i]);
+}
+
+// boundary runs: global position = (b - rem_b) + rank inside the run
+__global__ void k_sel_runs(const double *__restrict__ pts, const unsigned *__restrict__ k32,
+                           SelState *st, const int *__restrict__ runs, int *out) {
+  const int nr = min(st->nrun, kSelRunCap);
+  const long long q0 = st->b[0] >= 0 ? st->b[0] : 0;
+  for (int e = threadIdx.x; e < nr; e += blockDim.x) {
+    const int ve = runs[e];
+    const unsigned k = k32[ve];
+    const unsigned long long ke = order_key(pts[3ll * ve]);
+    long long r = 0;
+    for (int f = 0; f < nr; ++f) {
+      const int vf = runs[f];
+      if (vf == ve || k32[vf] != k) continue;
+      const unsigned long long kf = order_key(pts[3ll * vf]);
+      r += (kf < ke || (kf == ke && vf < ve));
+    }
+    const int b = (st->b[0] >= 0 && k == st->pre[0]) ? 0 : 1;
+    const long long pos = st->b[b] - st->rem[b] + r;
+    const long long p1 = st->b[1] >= 0 ? st->b[1] : 0x7fffffffffffffffll;
+    if (pos >= q0 && pos < p1) out[atomicAdd(&st->count, 1)] = ve;
+  }
+}
+
+// window keys; a count other than the window size flags the selection
+__global__ void k_sel_keys(const unsigned *__restrict__ k32, SelState *st, int *idx,
+                           unsigned *keys, long long m) {
+  const long long cnt = st->count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != m) st->bad = 1;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (i >= cnt) idx[i] = 0;
+    keys[i] = k32[idx[i]];
   }
 }
 
@@ -425,7 +699,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   unsigned long long mm_init[2] = {~0ull, 0ull};
   cudaMemcpyAsync(w.mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, s);
   h3d_count_launches(4);
-  k_scan_input<<<G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
+  k_scan_input<<<G > 1184 ? 1184 : G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
   // stable argsort of x (api.py:97): 32-bit fixed-point keys + tie-run fix
   unsigned *k32a = reinterpret_cast<unsigned *>(w.k0), *k32b = reinterpret_cast<unsigned *>(w.k1);
   k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, w.v0);
@@ -529,17 +803,94 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   return 0;
 }
 
-int64_t h3d_orient_remap(const double *sorted_pts, int64_t n, const int64_t *order,
-                         const int32_t *faces_raw, int64_t nfaces, int64_t *faces,
-                         int32_t *vertex_mark, int64_t *vertices, void *workspace,
+int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1, int32_t scan,
+                         double *sorted_pts, int64_t *order, void *workspace,
                          size_t workspace_bytes, void *stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n < 2048 || n > (1ll << 30) || q0 < 0 || p1 > n || q0 >= p1) return H3D_E_ARG;
+  h3d_arena ar(workspace, workspace_bytes);
+  PresortWS w;
+  if (!carve(ar, n, w)) return H3D_E_ARG;
+  const unsigned G = h3d_grid(n, 256) > 4096 ? 4096 : h3d_grid(n, 256);
+  const long long m = p1 - q0;
+  unsigned *k32 = reinterpret_cast<unsigned *>(w.k0);
+  unsigned *lk = reinterpret_cast<unsigned *>(w.k1), *lk_alt = lk + n;
+  int *idx = w.v0, *idx_alt = w.v1, *runs = w.v2;
+  unsigned *hist = reinterpret_cast<unsigned *>(w.head);
+  SelState *st = reinterpret_cast<SelState *>(w.partial);
+  SelState init{};
+  init.b[0] = q0 > 0 ? q0 : -1;
+  init.b[1] = p1 < n ? p1 : -1;
+  init.rem[0] = q0;
+  init.rem[1] = p1;
+  cudaMemsetAsync(w.flag, 0, sizeof(int) * 4, s);
+  cudaMemsetAsync(hist, 0, sizeof(unsigned) * 4096, s);
+  cudaMemcpyAsync(st, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+  unsigned long long mm_init[2] = {~0ull, 0ull};
+  cudaMemcpyAsync(w.mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, s);
+  h3d_count_launches(2);
+  k_scan_init<<<1, 1, 0, s>>>(w.scan);
+  k_scan_input<<<G > 1184 ? 1184 : G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
+  // keys + the first select pass's histogram (every key has the empty prefix)
+  h3d_count_launches(1);
+  k_keys32_hist<<<1184, 256, 0, s>>>(pts, n, w.mm, k32, hist);
+  if (init.b[0] >= 0 || init.b[1] >= 0) {
+    for (int pass = 0; pass < 3; ++pass) {
+      h3d_count_launches(pass ? 2 : 1);
+      if (pass) k_sel_hist<<<296, 512, 0, s>>>(k32, n, st, pass, hist);
+      k_sel_pick<<<1, 256, 0, s>>>(hist, st, pass);
+    }
+  }
+  h3d_count_launches(3);
+  k_sel_compact<<<1184, 256, 0, s>>>(k32, n, st, idx, runs);
+  k_sel_runs<<<1, 256, 0, s>>>(pts, k32, st, runs, idx);
+  const unsigned Gm = h3d_grid(m, 256) > 4096 ? 4096 : h3d_grid(m, 256);
+  k_sel_keys<<<Gm, 256, 0, s>>>(k32, st, idx, lk, m);
+  cub::DoubleBuffer<unsigned> kb(lk, lk_alt);
+  cub::DoubleBuffer<int> vb(idx, idx_alt);
+  size_t bytes = w.cub_bytes;
+  if (h3d_check(cub::DeviceRadixSort::SortPairs(w.cub_tmp, bytes, kb, vb, static_cast<int>(m), 0,
+                                                32, s)))
+    return H3D_E_CUDA;
+  h3d_count_launches(2);
+  k_tiefix<<<Gm, 256, 0, s>>>(pts, kb.Current(), vb.Current(), m, w.flag + 2);
+  k_gather_rows<<<Gm, 256, 0, s>>>(pts, vb.Current(), m, sorted_pts + 3 * q0,
+                                   reinterpret_cast<long long *>(order) + q0, nullptr, w.flag);
+  if (scan) {  // _scan_degenerate over this window (rank 0: rows [0, p1))
+    h3d_count_launches(6);
+    for (int stage = 0; stage < 3; ++stage) {
+      k_degenerate<<<64, 256, 0, s>>>(sorted_pts, p1, w.scan, stage, 1, 16384);
+      k_degenerate<<<G, 256, 0, s>>>(sorted_pts, p1, w.scan, stage, 16384, p1);
+    }
+  }
+  int hflag[3] = {0, 0, 0};
+  SelState hst;
+  ScanState hs;
+  if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+      h3d_check(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s)) ||
+      h3d_check(cudaMemcpyAsync(&hs, w.scan, sizeof(hs), cudaMemcpyDeviceToHost, s)) ||
+      h3d_check(cudaStreamSynchronize(s)))
+    return H3D_E_CUDA;
+  // ties, long key runs, a bad selection, non-finite input or a degeneracy
+  // the window cannot decide: the caller runs the replicated h3d_presort
+  if (hflag[0] || hflag[1] || hflag[2] || hst.bad) return H3D_E_FASTPATH;
+  const long long none = 0x7fffffffffffffffll;
+  if (scan && (hs.i == none || hs.j == none || hs.k == none)) return H3D_E_FASTPATH;
+  return 0;
+}
+
+int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n, const int64_t *order,
+                            const int32_t *faces_raw, int64_t nfaces, int64_t *faces,
+                            int32_t *vertex_mark, int64_t *vertices,
+                            const double *centroid_pts, void *workspace,
+                            size_t workspace_bytes, void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h3d_arena ar(workspace, workspace_bytes);
   PresortWS w;
   if (!carve(ar, n, w)) return H3D_E_ARG;
   if (nfaces == 0) return H3D_E_NOFACETS;
   h3d_count_launches(1);
-  k_colsum<<<kColsumBlocks, 256, 0, s>>>(sorted_pts, n, w.partial);
+  k_colsum<<<kColsumBlocks, 256, 0, s>>>(centroid_pts ? centroid_pts : sorted_pts, n, w.partial);
   h3d_count_launches(1);
   k_centroid<<<1, 32, 0, s>>>(w.partial, kColsumBlocks, n, w.centroid);
   cudaMemsetAsync(vertex_mark, 0, sizeof(int) * n, s);
@@ -558,6 +909,14 @@ int64_t h3d_orient_remap(const double *sorted_pts, int64_t n, const int64_t *ord
       h3d_check(cudaStreamSynchronize(s)))
     return H3D_E_CUDA;
   return cnt;
+}
+
+int64_t h3d_orient_remap(const double *sorted_pts, int64_t n, const int64_t *order,
+                         const int32_t *faces_raw, int64_t nfaces, int64_t *faces,
+                         int32_t *vertex_mark, int64_t *vertices, void *workspace,
+                         size_t workspace_bytes, void *stream) {
+  return h3d_orient_remap_ex(sorted_pts, n, order, faces_raw, nfaces, faces, vertex_mark, vertices,
+                             nullptr, workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

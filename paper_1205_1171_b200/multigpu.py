@@ -150,42 +150,124 @@ def _recv(t: torch.Tensor, src: int) -> None:
         dist.recv(t, src)
 
 
-def send_group(layouts, buf: int, level: int, g: int, dst: int) -> None:
-    """Ship group g of `level` (in buffer `buf`) of both passes to rank dst."""
+def _rows_of(gid_view: torch.Tensor, rows) -> torch.Tensor:
+    """(nS, 4) int64: the sorted row (x, y, z bits) and caller index of every
+    point of a group -- what the receiver of a sharded presort lacks."""
+    sorted_pts, order = rows
+    idx = gid_view.view(torch.int32).long()
+    return torch.cat([sorted_pts.index_select(0, idx).view(torch.int64),
+                      order.index_select(0, idx).unsqueeze(1)], dim=1)
+
+
+def _group_views(lay, buf: int, L: int, nS: int, k: int):
+    return (lay.lnk_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k))
+
+
+def send_group(layouts, buf: int, level: int, g: int, dst: int, rows=None) -> None:
+    """Ship group g of `level` (in buffer `buf`) of both passes to rank dst:
+    the header, then ONE packed payload (links, ids, events of both passes;
+    with rows = (sorted_pts, order) also the coordinates and caller indices
+    of the group's points -- under the sharded presort the receiver never
+    sorted them)."""
     hdr = group_header(layouts, buf, g)
     _send(hdr, dst)
     L = g << level
     h = hdr.cpu().tolist()
+    parts = []
     for p, lay in enumerate(layouts):
         nS, k = h[2 * p], h[2 * p + 1]
-        for view in (lay.lnk_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
-            if view.numel():
-                _send(view.contiguous(), dst)
+        parts.extend(v for v in _group_views(lay, buf, L, nS, k) if v.numel())
+        if rows is not None and nS:
+            parts.append(_rows_of(lay.gid_view(buf, L, nS), rows).view(torch.uint8).reshape(-1))
+    if parts:
+        _send(torch.cat(parts), dst)
 
 
-def recv_group(layouts, buf: int, level: int, g: int, src: int) -> None:
+def recv_group(layouts, buf: int, level: int, g: int, src: int, rows=None) -> None:
     """Receive group g of `level` of both passes from rank src into the same
-    slots of this rank's buffer `buf`."""
+    slots of this rank's buffer `buf` (and, with rows, scatter the points'
+    sorted rows and caller indices into this rank's full-size arrays)."""
     dev = layouts[0].ws.device
     hdr = torch.empty(4, dtype=torch.int32, device=dev)
     _recv(hdr, src)
     L = g << level
     h = hdr.cpu().tolist()
+    total = 0
     for p, lay in enumerate(layouts):
         nS, k = h[2 * p], h[2 * p + 1]
         lay.hdr_view(buf, g).copy_(hdr[2 * p:2 * p + 2].view(torch.uint8))
-        for view in (lay.lnk_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k)):
-            if view.numel():
-                tmp = torch.empty_like(view)
-                _recv(tmp, src)
-                view.copy_(tmp)
+        total += sum(v.numel() for v in _group_views(lay, buf, L, nS, k))
+        if rows is not None:
+            total += 32 * nS
+    if total == 0:
+        return
+    payload = torch.empty(total, dtype=torch.uint8, device=dev)
+    _recv(payload, src)
+    at = 0
+    for p, lay in enumerate(layouts):
+        nS, k = h[2 * p], h[2 * p + 1]
+        for view in _group_views(lay, buf, L, nS, k):
+            view.copy_(payload[at:at + view.numel()])
+            at += view.numel()
+        if rows is not None and nS:
+            sorted_pts, order = rows
+            tmp = payload[at:at + 32 * nS].clone().view(torch.int64).view(nS, 4)  # 8-byte aligned
+            at += 32 * nS
+            idx = lay.gid_view(buf, L, nS).view(torch.int32).long()
+            sorted_pts.index_copy_(0, idx, tmp[:, :3].contiguous().view(torch.float64))
+            order.index_copy_(0, idx, tmp[:, 3].contiguous())
+
+
+SHARD_PRESORT_MIN = 1 << 14
+SHARDED_RUNS = [0]  # hulls whose presort ran sharded (tests check it is taken)
+
+
+def sharded_presort(pts_dev: torch.Tensor, plan: "SlabPlan", rank: int):
+    """Every rank sorts only its own slab (plus the row before it, for the
+    tie test across the boundary) with h3d_presort_slab; rank 0 also runs the
+    degeneracy scan.  Returns (sorted_pts, order) -- full-size arrays of which
+    only the rank's window is filled -- or None on every rank when any rank's
+    window cannot reproduce the replicated presort (ties, long key runs,
+    non-finite input, undecided degeneracy)."""
+    import os
+
+    import torch.distributed as dist
+
+    from .api import _Workspace
+    from .engine import stream_ptr
+
+    L = _lib.load()
+    n = pts_dev.shape[0]
+    dev = pts_dev.device
+    if os.environ.get("H3D_DIST_POISON"):  # tests: unfilled rows must never be read
+        sorted_pts = torch.full((n, 3), float("nan"), dtype=torch.float64, device=dev)
+        order = torch.full((n,), -1, dtype=torch.int64, device=dev)
+    else:
+        sorted_pts = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        order = torch.empty(n, dtype=torch.int64, device=dev)
+    code = 0
+    sl = plan.slab(rank)
+    if sl is not None:
+        ws = _Workspace.get(dev, int(L.h3d_presort_workspace_bytes(n)))
+        code = int(L.h3d_presort_slab(pts_dev.data_ptr(), n, max(0, sl[0] - 1), sl[1],
+                                      1 if rank == 0 else 0, sorted_pts.data_ptr(),
+                                      order.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      stream_ptr(dev)))
+    flag = torch.tensor([1 if code != 0 else 0], dtype=torch.int64,
+                        device="cpu" if _p2p_via_host() else dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    if int(flag.item()) != 0:
+        return None
+    SHARDED_RUNS[0] += 1
+    return sorted_pts, order
 
 
 def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
     """Both passes of the hull over x-slabs.  Every rank passes the same
     input (caller order, on its own device).  Returns on rank 0 the same
-    tuple as fast.run_both plus (sorted points, order, perturbed); None on the
-    other ranks; None on rank 0 too when the exact engine must take over."""
+    tuple as fast.run_both plus (sorted points, order, perturbed, sharded);
+    None on the other ranks; None on rank 0 too when the exact engine must
+    take over."""
     import torch.distributed as dist
 
     from .api import presort
@@ -196,8 +278,14 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
     n = pts_dev.shape[0]
     dev = pts_dev.device
     s = stream_ptr(dev)
-    sorted_pts, order, perturbed = presort(pts_dev)
     plan = SlabPlan(n, world)
+    sh = sharded_presort(pts_dev, plan, rank) if n >= SHARD_PRESORT_MIN else None
+    if sh is not None:
+        (sorted_pts, order), perturbed = sh, False
+        rows = sh
+    else:
+        sorted_pts, order, perturbed = presort(pts_dev)
+        rows = None
     wsb = int(L.h3d_fast_pass_workspace_bytes(n))
     ws = [_WS.get(dev, 0, wsb), _WS.get(dev, 1, wsb)]
     lays = [GroupLayout(ws[0], n), GroupLayout(ws[1], n)]
@@ -213,10 +301,10 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
         role, peer = plan.role(lv, rank)
         prev_buf = (lv - 1) & 1
         if role == "send":
-            send_group(lays, prev_buf, lv - 1, (rank * plan.S) >> (lv - 1), peer)
+            send_group(lays, prev_buf, lv - 1, (rank * plan.S) >> (lv - 1), peer, rows)
         elif role in ("merge", "carry"):
             if role == "merge":
-                recv_group(lays, prev_buf, lv - 1, (peer * plan.S) >> (lv - 1), peer)
+                recv_group(lays, prev_buf, lv - 1, (peer * plan.S) >> (lv - 1), peer, rows)
             p0 = rank * plan.S
             p1 = min(n, p0 + (1 << lv))
             r = L.h3d_fast_passes_range(sorted_pts.data_ptr(), n, p0, p1, lv, lv,
@@ -243,7 +331,7 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
     if int(h[0]) != 0:
         return None
     k_lo, k_up = int(h[1]), int(h[2])
-    return faces[: k_lo + k_up], k_lo, k_up, sorted_pts, order, perturbed
+    return faces[: k_lo + k_up], k_lo, k_up, sorted_pts, order, perturbed, rows is not None
 
 
 def convex_hull_3d_distributed(points, device=None, return_device: bool = False):
@@ -269,8 +357,10 @@ def convex_hull_3d_distributed(points, device=None, return_device: bool = False)
         return None
     if res is None:  # exact engine, single GPU, reference semantics
         return convex_hull_3d(pts, _exact_backend(dev), return_device=return_device)
-    raw, k_lo, k_up, sorted_pts, order, perturbed = res
-    verts, faces = orient_remap(sorted_pts, order, raw)
+    raw, k_lo, k_up, sorted_pts, order, perturbed, sharded = res
+    # sharded presort: rank 0 holds only the rows its merges touched, so the
+    # centroid is taken over the caller-order input (same points)
+    verts, faces = orient_remap(sorted_pts, order, raw, pts if sharded else None)
     total_ms = (time.perf_counter() - t0) * 1e3
     stats = HullStats(n=n, levels=level_count(n), lower_events=k_lo, upper_events=k_up,
                       sort_ms=0.0, lower_ms=0.0, upper_ms=0.0, total_ms=total_ms,

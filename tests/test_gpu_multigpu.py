@@ -34,6 +34,7 @@ def _worker(rank, world, port, cases, q):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["H3D_DIST_POISON"] = "1"  # rows a rank did not sort are NaN
     import torch
     import torch.distributed as dist
 
@@ -41,6 +42,7 @@ def _worker(rank, world, port, cases, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1205_1171_b200.generators import generate
+        from paper_1205_1171_b200 import multigpu
         from paper_1205_1171_b200.multigpu import convex_hull_3d_distributed
 
         out = {}
@@ -49,6 +51,7 @@ def _worker(rank, world, port, cases, q):
             if rank == 0:
                 out[(n, dist_name, seed)] = (r.faces, r.vertices)
         if rank == 0:
+            out["sharded"] = multigpu.SHARDED_RUNS[0]
             q.put(out)
     finally:
         dist.destroy_process_group()
@@ -73,6 +76,8 @@ def test_distributed_equals_single_gpu(world, large_json):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    # the two cases >= SHARD_PRESORT_MIN points sort only their own slabs
+    assert got.pop("sharded") == 2
     for key, (faces, verts) in got.items():
         ref = H.convex_hull_3d(generate(*key))
         assert np.array_equal(faces, ref.faces), key

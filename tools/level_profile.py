@@ -26,8 +26,11 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--engine", default="fast")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--n", type=int, default=0, help="override the config's size")
     a = ap.parse_args()
     n, dist, seed, _ = bench.CONFIGS[a.config]
+    if a.n:
+        n = a.n
     pts = torch.from_numpy(generate(n, dist, seed)).cuda()
     be = H.CudaBackend(0, engine=a.engine)
     for _ in range(2):
