@@ -33,21 +33,34 @@ struct ProfRec {
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_ev_free;  // recycled events (creation is not free)
+
+cudaEvent_t ev_get() {
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (!g_ev_free.empty()) {
+      cudaEvent_t e = g_ev_free.back();
+      g_ev_free.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e;
+  return cudaEventCreate(&e) == cudaSuccess ? e : nullptr;
+}
 }  // namespace
 
 bool h3d_profiling() { return g_prof_on; }
 
 void *h3d_prof_begin(cudaStream_t s) {
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
-  cudaEventRecord(e, s);
+  cudaEvent_t e = ev_get();
+  if (e) cudaEventRecord(e, s);
   return e;
 }
 
 void h3d_prof_end(void *e0, int level, int pass, cudaStream_t s) {
   if (!e0) return;
-  cudaEvent_t e1;
-  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEvent_t e1 = ev_get();
+  if (!e1) return;
   cudaEventRecord(e1, s);
   std::lock_guard<std::mutex> g(g_prof_mu);
   g_prof.push_back({level, pass, static_cast<cudaEvent_t>(e0), e1});
@@ -71,8 +84,8 @@ extern "C" int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms,
       ms[m] = t;
       ++m;
     }
-    cudaEventDestroy(r.e0);
-    cudaEventDestroy(r.e1);
+    g_ev_free.push_back(r.e0);
+    g_ev_free.push_back(r.e1);
   }
   g_prof.clear();
   return m;

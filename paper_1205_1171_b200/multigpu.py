@@ -334,6 +334,44 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
     return faces[: k_lo + k_up], k_lo, k_up, sorted_pts, order, perturbed, rows is not None
 
 
+GATHER_INPUT_MIN = 1 << 16
+
+
+def gather_input(points, dev: torch.device, rank: int, world: int) -> torch.Tensor:
+    """Every rank's device copy of the whole cloud.  A host input is not
+    copied whole by every rank over PCIe: rank r copies only its 1/world row
+    chunk and an all-gather (NVLink under NCCL) assembles the rest."""
+    import numpy as np
+    import torch.distributed as dist
+
+    from .api import _to_device
+
+    if (isinstance(points, torch.Tensor) and points.is_cuda) or world == 1:
+        return _to_device(points, dev)
+    host = points if isinstance(points, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(points, dtype=np.float64)))
+    if host.ndim != 2 or host.shape[1] != 3:
+        raise ValueError("points must have shape (n, 3)")
+    host = host.to(dtype=torch.float64).contiguous()
+    n = host.shape[0]
+    if n < GATHER_INPUT_MIN:
+        return _to_device(host, dev)
+    C = (n + world - 1) // world
+    lo, hi = min(n, rank * C), min(n, (rank + 1) * C)
+    if _p2p_via_host():
+        mine = torch.zeros((C, 3), dtype=torch.float64)
+        mine[:hi - lo] = host[lo:hi]
+        parts = [torch.empty((C, 3), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        return torch.cat(parts)[:n].to(dev)
+    full = torch.empty((world * C, 3), dtype=torch.float64, device=dev)
+    mine = full[rank * C:(rank + 1) * C]
+    if hi > lo:
+        mine[:hi - lo].copy_(host[lo:hi], non_blocking=host.is_pinned())
+    dist.all_gather_into_tensor(full, mine)  # in place: mine is rank r's slice
+    return full[:n]
+
+
 def convex_hull_3d_distributed(points, device=None, return_device: bool = False):
     """Distributed drop-in: every rank calls it with the same points; rank 0
     gets the HullResult (identical to the single-GPU one), the others None."""
@@ -342,13 +380,13 @@ def convex_hull_3d_distributed(points, device=None, return_device: bool = False)
     import numpy as np
     import torch.distributed as dist
 
-    from .api import HullResult, HullStats, _to_device, convex_hull_3d, orient_remap, to_host
+    from .api import HullResult, HullStats, convex_hull_3d, orient_remap, to_host
     from .engine import level_count
 
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = device or torch.device("cuda", torch.cuda.current_device())
     t0 = time.perf_counter()
-    pts = _to_device(points, dev)
+    pts = gather_input(points, dev, rank, world)
     n = pts.shape[0]
     if world == 1 or n <= 3 or SlabPlan(n, world).G == 1:
         return convex_hull_3d(pts, return_device=return_device) if rank == 0 else None

@@ -119,3 +119,63 @@ def test_group_exchange_gloo():
     # everything the sender wrote arrived in the same slots; nothing else moved
     for a, b in zip(got["sent"], got["recv"]):
         assert np.array_equal(a, b)
+
+
+def _rows_worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1205_1171_b200 import _lib
+        from paper_1205_1171_b200.multigpu import gather_input
+
+        # the sharded presort's exchange: a group's points travel with their
+        # sorted rows and caller indices
+        wsb = int(_lib.load().h3d_fast_pass_workspace_bytes(n))
+        ws = [torch.zeros(wsb, dtype=torch.uint8), torch.zeros(wsb, dtype=torch.uint8)]
+        lays = [GroupLayout(ws[0], n), GroupLayout(ws[1], n)]
+        level, g, buf = 6, 1, 0
+        L = g << level
+        sizes = [(13, 21), (9, 14)]
+        sp = torch.full((n, 3), float("nan"), dtype=torch.float64)
+        od = torch.full((n,), -1, dtype=torch.int64)
+        gen = torch.Generator().manual_seed(3)
+        for p, lay in enumerate(lays):
+            nS, k = sizes[p]
+            lay.hdr_view(buf, g).copy_(torch.tensor([nS, k], dtype=torch.int32).view(torch.uint8))
+            ids = (L + torch.randperm(1 << level, generator=gen)[:nS]).to(torch.int32)
+            lay.gid_view(buf, L, nS).copy_(ids.view(torch.uint8))
+        if rank == 1:
+            sp.copy_(torch.randn((n, 3), generator=gen, dtype=torch.float64))
+            od.copy_(torch.randperm(n, generator=gen))
+            send_group(lays, buf, level, g, 0, (sp, od))
+        else:
+            recv_group(lays, buf, level, g, 1, (sp, od))
+        # chunked input gather (uneven chunks for world 2 and n odd)
+        pts = np.random.default_rng(9).uniform(-1, 1, (70001, 3))
+        full = gather_input(pts, torch.device("cpu"), rank, world)
+        q.put((rank, sp.numpy(), od.numpy(), bool(np.array_equal(full.numpy(), pts))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_group_rows_and_input_gather_gloo():
+    n = 4096
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sp1, od1, ok1 = got[1]
+    sp0, od0, ok0 = got[0]
+    assert ok0 and ok1
+    moved = od0 >= 0
+    assert 0 < moved.sum() <= 13 + 9
+    assert np.array_equal(od0[moved], od1[moved])
+    assert np.array_equal(sp0[moved], sp1[moved])
+    assert np.isnan(sp0[~moved]).all()

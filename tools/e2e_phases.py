@@ -33,4 +33,7 @@ for _ in range(3):
     verts, faces = api.orient_remap(sp, order, raw); t = tick("orient_remap", t)
     v, f = verts.cpu().numpy(), faces.cpu().numpy(); t = tick("d2h", t)
     t0 = time.perf_counter(); H.convex_hull_3d(pinned); t = tick("whole_api", t0)
+    t0 = time.perf_counter(); H.convex_hull_3d(pinned, solver="serial"); t = tick("whole_api_serial", t0)
+    t0 = time.perf_counter(); H.convex_hull_3d(pinned, return_device=True); t = tick("whole_api_dev", t0)
+    t0 = time.perf_counter(); H.convex_hull_3d(pts, return_device=True); t = tick("whole_api_devin", t0)
 print({k: round(v / 3, 2) for k, v in T.items()})
