@@ -1353,6 +1353,11 @@ bool g_env_done = false;
 int g_leaf_b = 3;  // H3D_LEAF_B: levels 1..B fused (0 = off)
 int g_mini = 1;    // H3D_MINI: few small jobs -> mini.cu (0 = warp kernel)
 long long kMiniMaxCtas = 2 * 148;  // H3D_MINI_CTAS
+// the tiny mini variant (several CTAs per SM): at most this many CTAs, and
+// over the lane-per-job kernel only when the longest merged child log is at
+// least kMiniTinyKin events (the lane kernel's serial path then dominates)
+long long kMiniTinyCtas = 8192;  // H3D_MINI_TINY_CTAS
+long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
 
 // tuning knobs from the environment (read once; h3d_tune overrides)
 void load_env_once() {
@@ -1366,6 +1371,8 @@ void load_env_once() {
   if (const char *e = getenv("H3D_BIG_TOTAL")) kBigTotal = atoll(e);
   if (const char *e = getenv("H3D_MINI")) g_mini = atoi(e);
   if (const char *e = getenv("H3D_MINI_CTAS")) kMiniMaxCtas = atoll(e);
+  if (const char *e = getenv("H3D_MINI_TINY_CTAS")) kMiniTinyCtas = atoll(e);
+  if (const char *e = getenv("H3D_MINI_TINY_KIN")) kMiniTinyKin = atoll(e);
   if (g_leaf_b > 4) g_leaf_b = 4;
 }
 
@@ -1387,6 +1394,8 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = value > 4 ? 4 : static_cast<int>(value); }
   else if (k == "mini") { old = g_mini; if (value >= 0) g_mini = value ? 1 : 0; }
   else if (k == "mini_ctas") { old = kMiniMaxCtas; if (value >= 0) kMiniMaxCtas = value; }
+  else if (k == "mini_tiny_ctas") { old = kMiniTinyCtas; if (value >= 0) kMiniTinyCtas = value; }
+  else if (k == "mini_tiny_kin") { old = kMiniTinyKin; if (value >= 0) kMiniTinyKin = value; }
   else if (k == "big_total") { old = kBigTotal; if (value >= 0) kBigTotal = value; }
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
@@ -1516,6 +1525,16 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     // at most a few CTAs per SM)
     const bool mini_small = static_cast<long long>(need[6]) <= kMiniSmallPoints &&
                             maxkin <= kMiniSmallEvents;
+    const bool mini_tiny = static_cast<long long>(need[6]) <= kMiniTinyPoints &&
+                           maxkin <= kMiniTinyEvents && 2 * jobs <= kMiniTinyCtas &&
+                           (2 * jobs < kTpjMinTotalJobs || maxkin >= kMiniTinyKin);
+    if (g_mini && mini_tiny) {
+      const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, 2);
+      if (rm < 0) return rm;
+      h3d_prof_end(e0, lv + 5000, 2, s);
+      P = Pass2{P.out0, P.out1, P.in0, P.in1};
+      continue;
+    }
     if (g_mini && 2 * jobs < kTpjMinTotalJobs &&
         ((mini_small && 2 * jobs <= 4 * kMiniMaxCtas) ||
          (2 * jobs <= kMiniMaxCtas && static_cast<long long>(need[6]) <= kMiniMaxPoints &&

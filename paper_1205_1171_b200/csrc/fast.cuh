@@ -172,5 +172,6 @@ long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, lon
                      long long j1, long long *err, cudaStream_t s, int variant);
 constexpr int kMiniMaxPoints = 1024, kMiniMaxEvents = 2048;
 constexpr int kMiniSmallPoints = 256, kMiniSmallEvents = 512;
+constexpr int kMiniTinyPoints = 192, kMiniTinyEvents = 320;
 
 }  // namespace h3d

@@ -5,7 +5,8 @@ for bit with no exact-engine fallback:
 * leaf kernel depth 0 / 3 / 4 (levels 1..B fused in shared memory);
 * the time-split pipeline (big.cu) on almost every level (big_kin=16);
 * lane-per-job on every level (tpj_min_jobs=1, pipeline off);
-* warp-per-job on every level (tpj_min_jobs huge, pipeline off).
+* warp-per-job on every level (tpj_min_jobs huge, pipeline off);
+* each mini variant (one CTA per job in shared memory) wherever its jobs fit.
 """
 
 from __future__ import annotations
@@ -26,10 +27,12 @@ ROUTES = {
     "leaf4": {"leaf_b": 4},
     "big_everywhere": {"big_kin": 16, "mini": 0},
     "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0, "mini": 0},
-    "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF},
+    "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0},
     "warp_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 0},
     "mini_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
-                        "mini_ctas": BIG_OFF},
+                        "mini_ctas": BIG_OFF, "mini_tiny_ctas": 0},
+    "mini_tiny_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
+                             "mini_ctas": 0, "mini_tiny_ctas": BIG_OFF},
 }
 CLOUDS = [("ball", 3001), ("sphere", 20000), ("cube", 65537), ("gauss", 9999), ("sphere", 4097)]
 

@@ -18,10 +18,12 @@ pytestmark = pytest.mark.gpu
 BIG_OFF = 1 << 40
 ROUTES = {
     "default": {},
-    "tpj": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "leaf_b": 0},
+    "tpj": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "leaf_b": 0, "mini_tiny_ctas": 0},
     "warp": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 0},
     "mini": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
-             "mini_ctas": BIG_OFF},
+             "mini_ctas": BIG_OFF, "mini_tiny_ctas": 0},
+    "mini_tiny": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
+                  "mini_ctas": 0, "mini_tiny_ctas": BIG_OFF},
     "big": {"big_kin": 2, "leaf_b": 0, "mini": 0},
     "leaf4": {"leaf_b": 4},
 }

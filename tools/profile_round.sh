@@ -14,7 +14,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fa
   -o $out/full_tpj_c4_l4 python tools/one_hull.py C4 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fast_leaf -c 1 \
   -o $out/full_leaf_c4 python tools/one_hull.py C4 1 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_big_sweep -s 3 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_big_sweep -s 0 -c 1 \
   -o $out/full_bigsweep_c3 python tools/one_hull.py C3 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mini -c 1 \
   -o $out/full_mini_c4 python tools/one_hull.py C4 1 > /dev/null 2>&1
