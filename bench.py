@@ -247,6 +247,7 @@ NCU_NAMES = {
     "k_fast_leaf": ("h3d::k_fast_leaf<",),
     "k_fast_init1": ("h3d::k_fast_init1",),
     "k_big_level": ("h3d::k_big_",),
+    "k_mini": ("h3d::k_mini<",),
 }
 
 
