@@ -182,7 +182,7 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n,
  * tests to drive every kernel route and by tuning sweeps): "big_kin"
  * (time-split pipeline from this merged child log size), "big_total" (or
  * half that log size with this many child events in the level), "leaf_b" (levels
- * 1..B fused, 0..4), "tpj_min_jobs", "tpj_xyz_kb", "tpj_max_level", "mini"
+ * 1..B fused: 3 or 4; 0-2 = off), "tpj_min_jobs", "tpj_xyz_kb", "tpj_max_level", "mini"
  * (0/1: the one-CTA-per-job shared-memory merges), "mini_ctas" (their CTA
  * cap), "mini_tiny_ctas" / "mini_tiny_kin" (the 6-CTA-per-SM variant: CTA
  * cap, and the merged child log size from which it replaces the lane-per-job

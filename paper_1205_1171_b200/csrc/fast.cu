@@ -1359,6 +1359,9 @@ long long kMiniMaxCtas = 2 * 148;  // H3D_MINI_CTAS
 long long kMiniTinyCtas = 8192;  // H3D_MINI_TINY_CTAS
 long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
 
+// leaf kernel depth: 3 or 4 fused levels, anything below 3 = off
+int leaf_depth(long long b) { return b >= 4 ? 4 : (b == 3 ? 3 : 0); }
+
 // tuning knobs from the environment (read once; h3d_tune overrides)
 void load_env_once() {
   if (g_env_done) return;
@@ -1373,7 +1376,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_MINI_CTAS")) kMiniMaxCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_CTAS")) kMiniTinyCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_KIN")) kMiniTinyKin = atoll(e);
-  if (g_leaf_b > 4) g_leaf_b = 4;
+  g_leaf_b = leaf_depth(g_leaf_b);
 }
 
 template <bool XYZ>
@@ -1391,7 +1394,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   const std::string k(name ? name : "");
   long long old = -1;
   if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
-  else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = value > 4 ? 4 : static_cast<int>(value); }
+  else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = leaf_depth(value); }
   else if (k == "mini") { old = g_mini; if (value >= 0) g_mini = value ? 1 : 0; }
   else if (k == "mini_ctas") { old = kMiniMaxCtas; if (value >= 0) kMiniMaxCtas = value; }
   else if (k == "mini_tiny_ctas") { old = kMiniTinyCtas; if (value >= 0) kMiniTinyCtas = value; }
@@ -1452,9 +1455,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     if (h3d_check(cudaFuncSetAttribute(k_fast_leaf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        32 * leaf_lane_bytes<3>())) ||
         h3d_check(cudaFuncSetAttribute(k_fast_leaf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       32 * leaf_lane_bytes<4>())) ||
-        h3d_check(cudaFuncSetAttribute(k_fast_leaf<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       32 * leaf_lane_bytes<5>())))
+                                       32 * leaf_lane_bytes<4>())))
       return H3D_E_CUDA;
     g_attr_done = true;
   }
@@ -1466,7 +1467,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   Pass2 P = (lv_lo & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
   int lv = lv_lo;
   const int NPB = 1 << g_leaf_b;
-  if (lv_lo == 1 && g_leaf_b >= 2 && lv_hi >= g_leaf_b && (p0 & (NPB - 1)) == 0) {
+  if (lv_lo == 1 && g_leaf_b >= 3 && lv_hi >= g_leaf_b && (p0 & (NPB - 1)) == 0) {
     // levels 1..B fused in shared memory, one lane per 2^B-point block
     const long long blocks = (p1 - p0 + NPB - 1) / NPB;
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
@@ -1474,17 +1475,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     const dim3 grid(h3d_grid(blocks, 32), 2);
     // level B's groups go to buffer B&1
     const Pass2 LP = (g_leaf_b & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
-    switch (g_leaf_b) {
-      case 3:
-        k_fast_leaf<3><<<grid, 32, 32 * leaf_lane_bytes<3>(), s>>>(LP, sorted_pts, n, p0, p1, err);
-        break;
-      case 4:
-        k_fast_leaf<4><<<grid, 32, 32 * leaf_lane_bytes<4>(), s>>>(LP, sorted_pts, n, p0, p1, err);
-        break;
-      default:
-        k_fast_leaf<5><<<grid, 32, 32 * leaf_lane_bytes<5>(), s>>>(LP, sorted_pts, n, p0, p1, err);
-        break;
-    }
+    if (g_leaf_b == 4)
+      k_fast_leaf<4><<<grid, 32, 32 * leaf_lane_bytes<4>(), s>>>(LP, sorted_pts, n, p0, p1, err);
+    else
+      k_fast_leaf<3><<<grid, 32, 32 * leaf_lane_bytes<3>(), s>>>(LP, sorted_pts, n, p0, p1, err);
     h3d_prof_end(e0, 3000 + g_leaf_b, 2, s);
     // the leaf writes level B's groups into buffer B&1
     P = (g_leaf_b & 1) ? Pass2{w0.B, w1.B, w0.A, w1.A} : Pass2{w0.A, w1.A, w0.B, w1.B};

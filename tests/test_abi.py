@@ -55,3 +55,19 @@ def test_library_is_sm100a_only():
     blob = open(build.LIB, "rb").read()
     assert b"sm_100a" in blob or b"sm_100" in blob
     ctypes.CDLL(build.LIB)
+
+
+def test_tune_leaf_depth_normalised():
+    """leaf_b accepts 3 or 4 fused levels; anything below 3 turns the leaf
+    kernel off (h3d_tune is host-only: no GPU needed)."""
+    from paper_1205_1171_b200 import fast
+
+    old = fast.tune("leaf_b", 2)
+    try:
+        assert fast.tune("leaf_b") == 0
+        fast.tune("leaf_b", 9)
+        assert fast.tune("leaf_b") == 4
+        fast.tune("leaf_b", 3)
+        assert fast.tune("leaf_b") == 3
+    finally:
+        fast.tune("leaf_b", old)

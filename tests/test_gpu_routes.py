@@ -25,6 +25,7 @@ ROUTES = {
     "default": {},
     "no_leaf_no_big": {"leaf_b": 0, "big_kin": BIG_OFF},
     "leaf4": {"leaf_b": 4},
+    "leaf_b2_is_off": {"leaf_b": 2},
     "big_everywhere": {"big_kin": 16, "mini": 0},
     "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0, "mini": 0},
     "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0},
@@ -86,3 +87,33 @@ def test_presort_clustered_x_fallback(oracle_mod):
     r = H.convex_hull_3d(pts)
     assert np.array_equal(r.faces, exp.faces)
     assert np.array_equal(r.vertices, exp.vertices)
+
+
+KNOB_CHOICES = {
+    "leaf_b": [0, 1, 2, 3, 4],
+    "big_kin": [2, 16, 300, 1000, BIG_OFF],
+    "big_total": [0, 1000, 200000],
+    "tpj_min_jobs": [1, 64, 4736, BIG_OFF],
+    "tpj_xyz_kb": [0, 16, 200],
+    "tpj_max_level": [2, 6, 40],
+    "mini": [0, 1],
+    "mini_ctas": [0, 4, 296, BIG_OFF],
+    "mini_tiny_ctas": [0, 64, 8192, BIG_OFF],
+    "mini_tiny_kin": [0, 160, BIG_OFF],
+}
+
+
+def test_random_knob_combinations(oracle_mod):
+    """Any combination of routing knobs still reproduces the oracle (each
+    level's route is chosen independently, so mixed routes must hand each
+    other valid compact groups)."""
+    rng = np.random.default_rng(2024)
+    clouds = [generate(20000, "cube", 4), generate(6000, "ball", 5), generate(3000, "sphere", 6)]
+    exp = [oracle_mod.convex_hull_3d(p) for p in clouds]
+    for trial in range(16):
+        kv = {k: int(rng.choice(v)) for k, v in KNOB_CHOICES.items()}
+        with fast.tuned(**kv):
+            for p, e in zip(clouds, exp):
+                r = H.convex_hull_3d(p)
+                assert np.array_equal(r.faces, e.faces), (trial, kv, len(p))
+                assert np.array_equal(r.vertices, e.vertices), (trial, kv, len(p))
