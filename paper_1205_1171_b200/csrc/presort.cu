@@ -533,6 +533,70 @@ __global__ void k_degenerate(const double *__restrict__ P, long long n, ScanStat
   }
 }
 
+// The three stages over rows [1, r1) in ONE CTA (random inputs hit in the
+// first rows): each stage is a block-wide first-hit reduction, so the next
+// stage starts from the exact first hit.  The full-range launches above run
+// only for a stage this head leaves undecided.
+__global__ void __launch_bounds__(1024) k_degenerate_head(const double *__restrict__ P,
+                                                          long long n, ScanState *st,
+                                                          long long r1) {
+  const double tol = 1e-9;
+  double scale = __longlong_as_double(static_cast<long long>(st->scale_bits));
+  if (scale < 1e-30) scale = 1e-30;
+  const double x0 = P[0], y0 = P[1], z0 = P[2];
+  const long long none = 0x7fffffffffffffffll;
+  if (r1 > n) r1 = n;
+  __shared__ long long s_hit;
+  double di[3] = {0, 0, 0}, nrm[3] = {0, 0, 0};
+  for (int stage = 0; stage < 3; ++stage) {
+    if (threadIdx.x == 0) s_hit = none;
+    __syncthreads();
+    double thr;
+    if (stage == 0) {
+      thr = __dmul_rn(tol, scale);
+    } else if (stage == 1) {
+      thr = __dmul_rn(__dmul_rn(tol, scale), scale);
+    } else {
+      thr = __dmul_rn(__dmul_rn(tol, scale), norm3(nrm[0], nrm[1], nrm[2]));
+    }
+    for (long long base = 1; base < r1; base += blockDim.x) {
+      const long long r = base + threadIdx.x;
+      bool hit = false;
+      if (r < r1) {
+        const double dx = __dsub_rn(P[3 * r], x0), dy = __dsub_rn(P[3 * r + 1], y0),
+                     dz = __dsub_rn(P[3 * r + 2], z0);
+        if (stage == 0) {
+          hit = norm3(dx, dy, dz) > thr;
+        } else if (stage == 1) {
+          double c[3];
+          cross3(di[0], di[1], di[2], dx, dy, dz, c);
+          hit = norm3(c[0], c[1], c[2]) > thr;
+        } else {
+          const double dot = __dadd_rn(__dadd_rn(__dmul_rn(dx, nrm[0]), __dmul_rn(dy, nrm[1])),
+                                       __dmul_rn(dz, nrm[2]));
+          hit = fabs(dot) > thr;
+        }
+      }
+      if (hit) atomicMin(reinterpret_cast<unsigned long long *>(&s_hit),
+                         static_cast<unsigned long long>(r));
+      __syncthreads();
+      if (s_hit != none) break;  // block-uniform: the first hit is in this chunk
+    }
+    const long long h = s_hit;
+    if (threadIdx.x == 0) (stage == 0 ? st->i : (stage == 1 ? st->j : st->k)) = h;
+    if (h == none) return;  // undecided here: the full-range stages take over
+    if (stage == 0) {
+      di[0] = __dsub_rn(P[3 * h], x0);
+      di[1] = __dsub_rn(P[3 * h + 1], y0);
+      di[2] = __dsub_rn(P[3 * h + 2], z0);
+    } else if (stage == 1) {
+      cross3(di[0], di[1], di[2], __dsub_rn(P[3 * h], x0), __dsub_rn(P[3 * h + 1], y0),
+             __dsub_rn(P[3 * h + 2], z0), nrm);
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_scan_init(ScanState *st) {
   st->scale_bits = 0;
   st->i = st->j = st->k = 0x7fffffffffffffffll;
@@ -666,6 +730,28 @@ bool radix(PresortWS &w, unsigned long long *kin, int *vin, unsigned long long *
   return true;
 }
 
+// _scan_degenerate on rows [0, rows) (api.py:113-147): the three stages over
+// the first 16K rows in one CTA; only a stage left undecided there scans the
+// rest (random inputs stop in the first block, as the reference's block-wise
+// scan does).  Reads back the state and the flag words (one sync, two when
+// the head is undecided).
+bool degenerate_scan(const double *sorted_pts, long long rows, PresortWS &w, unsigned G,
+                     ScanState *hs, int *hflag, int nflag, cudaStream_t s) {
+  const long long none = 0x7fffffffffffffffll;
+  h3d_count_launches(1);
+  k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, rows, w.scan, 16384);
+  if (h3d_check(cudaMemcpyAsync(hs, w.scan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) ||
+      h3d_check(cudaMemcpyAsync(hflag, w.flag, nflag * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+      h3d_check(cudaStreamSynchronize(s)))
+    return false;
+  if (hs->i != none && hs->j != none && hs->k != none) return true;
+  h3d_count_launches(3);
+  for (int stage = 0; stage < 3; ++stage)
+    k_degenerate<<<G, 256, 0, s>>>(sorted_pts, rows, w.scan, stage, 1, rows);
+  return !h3d_check(cudaMemcpyAsync(hs, w.scan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) &&
+         !h3d_check(cudaStreamSynchronize(s));
+}
+
 }  // namespace
 
 extern "C" {
@@ -781,20 +867,9 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     k_absmax<<<G, 256, 0, s>>>(sorted_pts, 3 * n, &w.scan->scale_bits);
   }
   // _scan_degenerate on the sorted rows (api.py:113-147)
-  // each stage scans the first 16K rows with a small grid and the rest only
-  // when they hold no hit (random inputs stop in the first block, as the
-  // reference's block-wise scan does)
-  h3d_count_launches(6);
-  for (int stage = 0; stage < 3; ++stage) {
-    k_degenerate<<<64, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, 16384);
-    k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 16384, n);
-  }
   ScanState hs;
   int tie2 = 0;
-  if (h3d_check(cudaMemcpyAsync(&hs, w.scan, sizeof(hs), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaMemcpyAsync(&tie2, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaStreamSynchronize(s)))
-    return H3D_E_CUDA;
+  if (!degenerate_scan(sorted_pts, n, w, G, &hs, &tie2, 1, s)) return H3D_E_CUDA;
   if (tie && tie2) return H3D_E_TIES;
   const long long none = 0x7fffffffffffffffll;
   if (hs.i == none) return H3D_E_COINCIDENT;
@@ -856,21 +931,17 @@ int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1, i
   k_tiefix<<<Gm, 256, 0, s>>>(pts, kb.Current(), vb.Current(), m, w.flag + 2);
   k_gather_rows<<<Gm, 256, 0, s>>>(pts, vb.Current(), m, sorted_pts + 3 * q0,
                                    reinterpret_cast<long long *>(order) + q0, nullptr, w.flag);
-  if (scan) {  // _scan_degenerate over this window (rank 0: rows [0, p1))
-    h3d_count_launches(6);
-    for (int stage = 0; stage < 3; ++stage) {
-      k_degenerate<<<64, 256, 0, s>>>(sorted_pts, p1, w.scan, stage, 1, 16384);
-      k_degenerate<<<G, 256, 0, s>>>(sorted_pts, p1, w.scan, stage, 16384, p1);
-    }
-  }
   int hflag[3] = {0, 0, 0};
   SelState hst;
   ScanState hs;
-  if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaMemcpyAsync(&hs, w.scan, sizeof(hs), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaStreamSynchronize(s)))
+  if (h3d_check(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s)))
     return H3D_E_CUDA;
+  if (scan) {  // _scan_degenerate over this window (rank 0: rows [0, p1))
+    if (!degenerate_scan(sorted_pts, p1, w, G, &hs, hflag, 3, s)) return H3D_E_CUDA;
+  } else if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+             h3d_check(cudaStreamSynchronize(s))) {
+    return H3D_E_CUDA;
+  }
   // ties, long key runs, a bad selection, non-finite input or a degeneracy
   // the window cannot decide: the caller runs the replicated h3d_presort
   if (hflag[0] || hflag[1] || hflag[2] || hst.bad) return H3D_E_FASTPATH;

@@ -101,3 +101,35 @@ def test_row_offset_view_input():
     v[5, 1] = float("nan")
     with pytest.raises(ValueError):
         presort(v)
+
+
+def test_degeneracy_scan_beyond_the_head(oracle_mod):
+    """The first 30000 sorted rows are collinear: the one-CTA head scan
+    (first 16K rows) cannot decide the collinearity stage, so the full-range
+    stages must run; the result (faces or exception) equals the oracle's."""
+    import paper_1205_1171_b200 as H
+
+    rng = np.random.default_rng(8)
+    t = np.sort(rng.uniform(0.0, 0.75, 30000))
+    line = np.stack([t, 2.0 * t - 0.5, -t + 0.25], axis=1)
+    rest = rng.uniform(-1.0, 1.0, (10000, 3))
+    rest[:, 0] = rng.uniform(0.75, 1.0, 10000)
+    pts = np.concatenate([line, rest])
+    rng.shuffle(pts)
+
+    def outcome(fn):
+        try:
+            r = fn(pts)
+            return ("ok", r.faces, r.vertices)
+        except Exception as exc:  # noqa: BLE001
+            return ("err", type(exc).__name__, str(exc))
+
+    got, exp = outcome(H.convex_hull_3d), outcome(oracle_mod.convex_hull_3d)
+    assert got[0] == exp[0]
+    if got[0] == "ok":
+        assert np.array_equal(got[1], exp[1]) and np.array_equal(got[2], exp[2])
+    else:
+        assert got[1:] == exp[1:]
+    # all collinear: the head and the full range both find no second direction
+    with pytest.raises(ValueError, match="collinear"):
+        H.convex_hull_3d(line)
