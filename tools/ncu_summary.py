@@ -26,7 +26,13 @@ def launches(path: str, hulls: int, out: str) -> None:
         per.setdefault((r["ID"], r["Kernel Name"]), {})[r["Metric Name"]] = float(
             r["Metric Value"].replace(",", ""))
     items = list(per.items())
-    last = items[len(items) - len(items) // hulls:]
+    # the last COMPLETE hull: between the last two presort starts when the
+    # capture holds them (a launch window need not align with hulls)
+    marks = [i for i, ((_, name), _m) in enumerate(items) if "k_scan_init" in name]
+    if len(marks) >= 2:
+        last = items[marks[-2]:marks[-1]]
+    else:
+        last = items[len(items) - len(items) // hulls:]
     agg: dict = collections.OrderedDict()
     seq = []
     for (_, name), m in last:
