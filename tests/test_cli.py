@@ -51,3 +51,27 @@ def test_degenerate_exit_3(tmp_path):
     pts_file = tmp_path / "flat.txt"
     cli.write_points(str(pts_file), np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0], [2, 3, 0]], float))
     assert cli.main(["hull", "--in", str(pts_file), "--out", str(tmp_path / "f")]) == cli.EXIT_DEGENERATE
+
+
+@pytest.mark.gpu
+def test_bench_levels_and_compare_impl(tmp_path, oracle_mod):
+    """The reference's --levels-csv (n,level,ms) and --compare-impl
+    (n,impl,...) schemas; --kernel python runs the exact engine."""
+    csv, lv = tmp_path / "b.csv", tmp_path / "l.csv"
+    assert cli.main(["bench", "--min-exp", "6", "--max-exp", "7", "--reps", "1", "--csv", str(csv),
+                     "--levels-csv", str(lv)]) == 0
+    rows = lv.read_text().splitlines()
+    assert rows[0] == cli.LEVELS_CSV_HEADER
+    assert [r.split(",")[:2] for r in rows[1:]] == \
+        [[str(n), str(l)] for n in (64, 128) for l in range(1, (n - 1).bit_length() + 1)]
+    cmp_csv = tmp_path / "c.csv"
+    assert cli.main(["bench", "--min-exp", "6", "--max-exp", "6", "--reps", "1", "--csv",
+                     str(cmp_csv), "--compare-impl"]) == 0
+    rows = cmp_csv.read_text().splitlines()
+    assert rows[0] == cli.IMPL_CSV_HEADER
+    assert sorted(r.split(",")[1] for r in rows[1:]) == ["compiled", "python"]
+    pts_file, out = tmp_path / "p.txt", tmp_path / "f.txt"
+    cli.main(["generate", "--n", "200", "--dist", "gauss", "--seed", "3", "--out", str(pts_file)])
+    assert cli.main(["--kernel", "python", "hull", "--in", str(pts_file), "--out", str(out)]) == 0
+    exp = oracle_mod.convex_hull_3d(cli.read_points(str(pts_file)))
+    assert np.array_equal(np.loadtxt(out, dtype=np.int64), exp.faces)
