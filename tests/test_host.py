@@ -87,3 +87,30 @@ def test_integer_cloud_takes_tie_path(oracle_mod):
     pts = integer_cloud(5000, 3, half_range=2**12)
     _, _, pert = oracle_mod.sort_and_perturb(pts)
     assert pert
+
+
+def test_snapshot_check_on_the_oracle_movie(oracle_mod):
+    """movie.snapshot_check (host replay) accepts the pinned oracle's final
+    movie at random probe times and rejects a chain it does not match."""
+    import numpy as np
+
+    from paper_1205_1171_b200 import movie
+    from paper_1205_1171_b200.generators import generate
+
+    pts = generate(200, "ball", 11)
+    coords = pts[np.lexsort((pts[:, 2], pts[:, 1], pts[:, 0]))]
+    final = None
+    for _lv, _k, buf, links in oracle_mod.level_logs(coords):
+        final = (buf, links)
+    buf, links = final
+    rng = np.random.default_rng(0)
+    checked = 0
+    while checked < 20:
+        try:
+            assert movie.snapshot_check(coords, links.astype(np.int64), buf, movie.random_probe_time(rng))
+            checked += 1
+        except movie.EventTimeCollision:
+            pass
+    # an empty log leaves the t = -inf chain: wrong at a late time
+    assert not movie.snapshot_check(coords, links.astype(np.int64), np.array([-1]), 1e6)
+    assert movie.lower_hull_2d([(0.0, 0.0), (1.0, -1.0), (2.0, 0.0), (3.0, 5.0)]) == [0, 1, 2, 3]
