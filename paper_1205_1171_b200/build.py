@@ -22,6 +22,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -ffp-contract=off, pkg/setup.py:51-54); fp64 division stays IEEE.
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# profiling builds only (e.g. H3D_NVCC_EXTRA=-DH3D_MINI_PROF); never set for
+# the product build
+FLAGS += os.environ.get("H3D_NVCC_EXTRA", "").split()
 
 
 def sources() -> list[str]:

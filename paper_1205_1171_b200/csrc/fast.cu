@@ -1394,6 +1394,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_MINI_CTAS")) kMiniMaxCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_CTAS")) kMiniTinyCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_KIN")) kMiniTinyKin = atoll(e);
+  if (const char *e = getenv("H3D_MINI_SEG")) g_mini_seglen = atoi(e) < 1 ? 1 : atoi(e);
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
@@ -1417,6 +1418,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "mini_ctas") { old = kMiniMaxCtas; if (value >= 0) kMiniMaxCtas = value; }
   else if (k == "mini_tiny_ctas") { old = kMiniTinyCtas; if (value >= 0) kMiniTinyCtas = value; }
   else if (k == "mini_tiny_kin") { old = kMiniTinyKin; if (value >= 0) kMiniTinyKin = value; }
+  else if (k == "mini_seg") { old = g_mini_seglen; if (value >= 1) g_mini_seglen = static_cast<int>(value); }
   else if (k == "big_total") { old = kBigTotal; if (value >= 0) kBigTotal = value; }
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }

@@ -173,5 +173,6 @@ long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, lon
 constexpr int kMiniMaxPoints = 1024, kMiniMaxEvents = 2048;
 constexpr int kMiniSmallPoints = 256, kMiniSmallEvents = 512;
 constexpr int kMiniTinyPoints = 192, kMiniTinyEvents = 320;
+extern int g_mini_seglen;  // mini.cu: child events per time segment
 
 }  // namespace h3d

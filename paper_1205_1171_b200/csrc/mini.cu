@@ -17,7 +17,16 @@
 
 namespace h3d {
 
-constexpr int MINI_S = 64;     // largest number of time segments
+#ifdef H3D_MINI_PROF
+// phase clocks of CTA (0, 0) per level (profiling builds only)
+__device__ long long g_mini_prof[64][16];
+#define MINI_TICK(i) \
+  do { if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_mini_prof[lv][i] = clock64(); } while (0)
+#else
+#define MINI_TICK(i) do {} while (0)
+#endif
+
+constexpr int MINI_S = 256;    // largest number of time segments
 constexpr int MINI_NIL = -1;
 
 // MINI_T threads per CTA (one job), MINI_K largest merged child log,
@@ -201,7 +210,7 @@ __device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int cap, in
 template <int MINI_T, int MINI_K, int MINI_N>
 __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int lv, long long j0, long long j1,
-                                                 long long *err) {
+                                                 long long *err, int seglen) {
   typedef MiniSmem<MINI_T, MINI_K, MINI_N> MS;
   constexpr int MINI_B = MS::MINI_B;
   constexpr int PER = (MINI_K + MINI_T) / MINI_T;  // blocked-scan items per thread
@@ -235,6 +244,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     return;
   }
   if (tid == 0) m.flag = 0;
+  MINI_TICK(0);
   // ---- points
   for (int p = tid; p < nS; p += T) {
     const long long src = p < nSL ? L + p : M + (p - nSL);
@@ -252,6 +262,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     m.LN[p] = make_short2(static_cast<short>(l.x), static_cast<short>(l.y));
     m.cur[p] = 0;
   }
+  MINI_TICK(1);
   // ---- merged child sequence S (merge path, left first on equal times);
   // the child times are staged in shared memory first (the bridge-event
   // arrays are free until the sweeps) so the co-rank searches stay on chip
@@ -284,6 +295,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
               (side << 31);
   }
   __syncthreads();
+  MINI_TICK(2);
   // ---- incidence lists: counts, scan, scatter, per-list sort, links after
   for (int d = tid; d < kin; d += T) {
     if (d > 0 && m.st[d] == m.st[d - 1]) m.flag = 1;  // exact tie
@@ -328,6 +340,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     m.el[q].x = static_cast<short>(pc);
   }
   __syncthreads();
+  MINI_TICK(3);
   // ... then every entry placed at its rank within its list (event order),
   // all entries in parallel (a list of L entries costs L reads per entry,
   // not a sequential L^2 sort)
@@ -357,9 +370,11 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     }
   }
   __syncthreads();
+  MINI_TICK(4);
   // ---- segments: start bridges by walks
-  int nseg = kin / 16;
+  int nseg = kin / seglen;
   if (nseg > MINI_S) nseg = MINI_S;
+  if (nseg > T) nseg = T;
   if (nseg < 1) nseg = 1;
   const int seg = (kin + nseg - 1) / nseg > 0 ? (kin + nseg - 1) / nseg : 1;
   nseg = kin > 0 ? (kin + seg - 1) / seg : 1;
@@ -388,16 +403,20 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     } else {  // just after the last child event before the segment
       // both candidate moves are evaluated every step (the v-advance wins,
       // as in _find_bridge) so the warp's walks stay converged
+      // only the foot that moved needs its links again: one incidence-list
+      // search per step, shared by both kinds of move
       const int pos = s * seg;
       const double T0 = m.st[pos - 1];
       int dummy;
+      int vn = mlinks(m, v, pos, &dummy).y;
+      int up = mlinks(m, u, pos, &dummy).x;
       for (;;) {
-        const int vn = mlinks(m, v, pos, &dummy).y;
-        const int up = mlinks(m, u, pos, &dummy).x;
         const bool mv = vn != NIL && mturn_neg_at(m, u, v, vn, T0);
         const bool mu = up != NIL && mturn_neg_at(m, up, u, v, T0);
         if (!mv && !mu) break;
         if (mv) v = vn; else u = up;
+        const short2 l = mlinks(m, mv ? v : u, pos, &dummy);
+        if (mv) vn = l.y; else up = l.x;
         if (++moves > limit) { bad = true; break; }
       }
     }
@@ -405,6 +424,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     m.sst[s] = make_short2(static_cast<short>(u), static_cast<short>(v));
   }
   __syncthreads();
+  MINI_TICK(5);
   // ---- segment sweeps (bridge events to per-segment slabs), offsets,
   // compaction; a segment whose slab overflowed is swept again in place
   const int cap = MINI_B / nseg;
@@ -416,6 +436,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     m.sbn[tid] = nb;
   }
   __syncthreads();
+  MINI_TICK(10);
   if (tid == 0) {
     int o = 0;
     for (int s = 0; s < nseg; ++s) {
@@ -447,6 +468,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     mini_sweep<1>(m, tid, nseg, seg, kin, cap, &nb, &e);
   }
   __syncthreads();
+  MINI_TICK(6);
   const int NB = m.nb;
   const int2 uv0 = make_int2(m.sst[0].x, m.sst[0].y);
   // ---- every child event kept or hidden by the bridge at its time
@@ -492,6 +514,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     if (tid == 0) raise_err(err, m.flag ? E_FASTPATH : H3D_E_OVERFLOW);
     return;
   }
+  MINI_TICK(7);
   // ---- merged log (job-local ids) straight to HBM, first event per point
   Ev *evo = out.ev + 2 * L;
   for (int d = tid; d < kin; d += T) {
@@ -528,6 +551,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     atomicMin(&m.cur[o.b], idx);
   }
   __syncthreads();
+  MINI_TICK(8);
   // ---- start-of-time links + compaction
   {
     const int per = (nS + T) / T;
@@ -587,6 +611,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     evo[e] = o;
   }
   if (bad) raise_err(err, E_FASTPATH);
+  MINI_TICK(9);
   if (tid == 0) out.hdr[j] = make_int2(m.sbn[MINI_S], kout);
 }
 
@@ -602,9 +627,12 @@ static long long launch_mini(const Pass2 &P, const double *pts, long long n, int
     attr = true;
   }
   h3d_count_launches(1);
-  k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, bytes, s>>>(P, pts, n, lv, j0, j1, err);
+  k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, bytes, s>>>(P, pts, n, lv, j0, j1,
+                                                                          err, g_mini_seglen);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
+
+int g_mini_seglen = 3;  // child events per time segment (H3D_MINI_SEG / h3d_tune)
 
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant) {
@@ -614,3 +642,9 @@ long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, lon
 }
 
 }  // namespace h3d
+
+#ifdef H3D_MINI_PROF
+extern "C" void h3d_mini_prof_read(long long *host) {
+  cudaMemcpyFromSymbol(host, h3d::g_mini_prof, sizeof(long long) * 64 * 16);
+}
+#endif
