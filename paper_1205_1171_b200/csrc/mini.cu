@@ -106,25 +106,41 @@ __device__ __forceinline__ bool mturn_neg_at(const MS &m, int a, int b, int c, d
 }
 
 // the sequential core of one segment (see big.cu k_big_sweep); MODE 0
-// counts, MODE 1 writes.  Returns false on an exact tie.
+// counts, MODE 1 writes.  Returns false on an exact tie.  Converged: every
+// step is one predicated body (touch or bridge), so the segments of a warp
+// never serialise on their event kinds; `active` lanes step, the others
+// idle through the loop until the whole warp is done.
 template <int MODE, class MS>
-__device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int cap, int *nb_out,
-                           int2 *end_uv) {
+__device__ bool mini_sweep(MS &m, bool active, int s, int nseg, int seg, int kin, int cap,
+                           int *nb_out, int2 *end_uv) {
   const int pos0 = s * seg, pos1 = (pos0 + seg < kin) ? pos0 + seg : kin;
-  const double tend = (s == nseg - 1) ? INF : m.st[pos1 - 1];
-  double tcur = (s == 0) ? -INF : m.st[pos0 - 1];
-  int u = m.sst[s].x, v = m.sst[s].y;
-  int pos = pos0, cu, cv;
-  short2 lu = mlinks(m, u, pos, &cu), lw = mlinks(m, v, pos, &cv);
-  int up = lu.x, un = lu.y, vp = lw.x, vn = lw.y;
-  double c2 = mevt(m, u, un, v), c3 = mevt(m, up, u, v);
-  double c4 = mevt(m, u, v, vn), c5 = mevt(m, u, vp, v);
+  const double tend = (!active || s == nseg - 1) ? INF : m.st[pos1 - 1];
+  double tcur = (!active || s == 0) ? -INF : m.st[pos0 - 1];
+  int u = 0, v = 0, cu = 0, cv = 0, eu = 0, ev = 0;
+  int up = MINI_NIL, un = MINI_NIL, vp = MINI_NIL, vn = MINI_NIL;
+  int pos = pos0;
+  if (active) {
+    u = m.sst[s].x;
+    v = m.sst[s].y;
+    const short2 lu = mlinks(m, u, pos, &cu), lw = mlinks(m, v, pos, &cv);
+    up = lu.x; un = lu.y; vp = lw.x; vn = lw.y;
+    eu = m.ib[u + 1];
+    ev = m.ib[v + 1];
+  }
+  double c2 = INF, c3 = INF, c4 = INF, c5 = INF;
+  if (active) {
+    c2 = mevt(m, u, un, v);
+    c3 = mevt(m, up, u, v);
+    c4 = mevt(m, u, v, vn);
+    c5 = mevt(m, u, vp, v);
+  }
   int nb = 0;
-  const int base = (MODE == 1) ? m.sbn[s] : s * cap;
-  for (;;) {
+  bool ok = true;
+  const int base = (MODE == 1) ? (active ? m.sbn[s] : 0) : s * cap;
+  while (__any_sync(0xffffffffu, active)) {
     double tu = INF, tv = INF;
-    if (cu < m.ib[u + 1] && m.ei[cu] < pos1) tu = m.st[m.ei[cu]];
-    if (cv < m.ib[v + 1] && m.ei[cv] < pos1) tv = m.st[m.ei[cv]];
+    if (active && cu < eu && m.ei[cu] < pos1) tu = m.st[m.ei[cu]];
+    if (active && cv < ev && m.ei[cv] < pos1) tv = m.st[m.ei[cv]];
     double best = INF;
     int which = -1;
     if (tu > tcur && tu < best) { best = tu; which = 0; }
@@ -133,56 +149,50 @@ __device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int cap, in
     if (c3 > tcur && c3 < best) { best = c3; which = 3; }
     if (c4 > tcur && c4 < best) { best = c4; which = 4; }
     if (c5 > tcur && c5 < best) { best = c5; which = 5; }
-    if (which < 0 || best > tend) break;
-    if ((which != 0 && tu == best) || (which != 1 && tv == best) || (which != 2 && c2 == best) ||
-        (which != 3 && c3 == best) || (which != 4 && c4 == best) || (which != 5 && c5 == best))
-      return false;
-    if (which == 0) {  // a child event naming u
-      pos = m.ei[cu] + 1;
-      up = m.el[cu].x;
-      un = m.el[cu].y;
-      ++cu;
-      c2 = mevt(m, u, un, v);
-      c3 = mevt(m, up, u, v);
-    } else if (which == 1) {  // a child event naming v
-      pos = m.ei[cv] + 1;
-      vp = m.el[cv].x;
-      vn = m.el[cv].y;
-      ++cv;
-      c4 = mevt(m, u, v, vn);
-      c5 = mevt(m, u, vp, v);
-    } else {
-      {  // the child events before this time are all applied
-        int lo = pos, hi = pos1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (m.st[mid] < best) lo = mid + 1; else hi = mid;
-        }
-        pos = lo;
+    if (which < 0 || best > tend) active = false;
+    if (active && ((which != 0 && tu == best) || (which != 1 && tv == best) ||
+                   (which != 2 && c2 == best) || (which != 3 && c3 == best) ||
+                   (which != 4 && c4 == best) || (which != 5 && c5 == best))) {
+      ok = false;
+      active = false;
+    }
+    const bool touch = active && which <= 1, bridge = active && which >= 2;
+    const bool sideU = which == 0 || which == 2 || which == 3;
+    // position after the child events before this time: the touched event
+    // itself, or a search of the segment for a bridge event
+    if (touch) pos = m.ei[sideU ? cu : cv] + 1;
+    {
+      int lo = bridge ? pos : 0, hi = bridge ? pos1 : 0;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (m.st[mid] < best) lo = mid + 1; else hi = mid;
       }
-      int a, b, c, kind;
-      // the new foot takes both links from its list (see big.cu)
-      if (which == 2) {
-        a = u; b = un; c = v; kind = EV_INS;
-        u = un;
-        const short2 l = mlinks(m, u, pos, &cu);
-        up = l.x; un = l.y;
-      } else if (which == 3) {
-        a = up; b = u; c = v; kind = EV_DEL;
-        u = up;
-        const short2 l = mlinks(m, u, pos, &cu);
-        up = l.x; un = l.y;
-      } else if (which == 4) {
-        a = u; b = v; c = vn; kind = EV_DEL;
-        v = vn;
-        const short2 l = mlinks(m, v, pos, &cv);
-        vp = l.x; vn = l.y;
-      } else {
-        a = u; b = vp; c = v; kind = EV_INS;
-        v = vp;
-        const short2 l = mlinks(m, v, pos, &cv);
-        vp = l.x; vn = l.y;
+      if (bridge) pos = lo;
+    }
+    // the facet of a bridge move and the foot that moves
+    int a = u, b = un, c = v, kind = EV_INS, nfoot = un;
+    if (which == 3) { a = up; b = u; c = v; kind = EV_DEL; nfoot = up; }
+    if (which == 4) { a = u; b = v; c = vn; kind = EV_DEL; nfoot = vn; }
+    if (which == 5) { a = u; b = vp; c = v; kind = EV_INS; nfoot = vp; }
+    // links of the point whose links change: the touched foot (the
+    // event's links) or the new foot (its list at pos) -- one lookup
+    int first = 0;
+    short2 l = make_short2(MINI_NIL, MINI_NIL);
+    if (touch) l = m.el[sideU ? cu : cv];
+    {
+      const int q = bridge ? nfoot : 0;
+      int lo = bridge ? m.ib[q] : 0, hi = bridge ? m.ib[q + 1] : 0;
+      const int b0 = lo;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (m.ei[mid] < pos) lo = mid + 1; else hi = mid;
       }
+      first = lo;
+      if (bridge) l = lo == b0 ? m.LN[q] : m.el[lo - 1];
+    }
+    if (bridge) {
+      if (sideU) { u = nfoot; cu = first; eu = m.ib[u + 1]; }
+      else { v = nfoot; cv = first; ev = m.ib[v + 1]; }
       const unsigned bw = static_cast<unsigned>(a) | (static_cast<unsigned>(b) << 10) |
                           (static_cast<unsigned>(c) << 20) | (static_cast<unsigned>(kind) << 30);
       if (MODE == 1 && base + nb < MS::MINI_B) {
@@ -195,16 +205,22 @@ __device__ bool mini_sweep(MS &m, int s, int nseg, int seg, int kin, int cap, in
         m.sluv[base + nb] = make_short2(static_cast<short>(u), static_cast<short>(v));
       }
       ++nb;
+    }
+    if (touch) {
+      if (sideU) ++cu; else ++cv;
+    }
+    if (active) {
+      if (sideU) { up = l.x; un = l.y; } else { vp = l.x; vn = l.y; }
       c2 = mevt(m, u, un, v);
       c3 = mevt(m, up, u, v);
       c4 = mevt(m, u, v, vn);
       c5 = mevt(m, u, vp, v);
+      tcur = best;
     }
-    tcur = best;
   }
   *nb_out = nb;
   *end_uv = make_int2(u, v);
-  return true;
+  return ok;
 }
 
 template <int MINI_T, int MINI_K, int MINI_N>
@@ -428,12 +444,13 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   // ---- segment sweeps (bridge events to per-segment slabs), offsets,
   // compaction; a segment whose slab overflowed is swept again in place
   const int cap = MINI_B / nseg;
-  if (tid < nseg) {
+  if (tid < ((nseg + 31) & ~31)) {  // whole warps: the sweep votes per warp
     int nb;
     int2 e;
-    if (!mini_sweep<0>(m, tid, nseg, seg, kin, cap, &nb, &e)) m.flag = 1;
-    if (tid + 1 < nseg && (m.sst[tid + 1].x != e.x || m.sst[tid + 1].y != e.y)) m.flag = 1;
-    m.sbn[tid] = nb;
+    const bool mine = tid < nseg;
+    if (!mini_sweep<0>(m, mine, tid, nseg, seg, kin, cap, &nb, &e)) m.flag = 1;
+    if (mine && tid + 1 < nseg && (m.sst[tid + 1].x != e.x || m.sst[tid + 1].y != e.y)) m.flag = 1;
+    if (mine) m.sbn[tid] = nb;
   }
   __syncthreads();
   MINI_TICK(10);
@@ -462,10 +479,11 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       m.buv[m.sbn[sg] + r] = m.sluv[q];
     }
   }
-  if (tid < nseg && m.sbn[tid + 1] - m.sbn[tid] > cap) {
+  if (tid < ((nseg + 31) & ~31)) {  // overflowed slabs: swept again in place
     int nb;
     int2 e;
-    mini_sweep<1>(m, tid, nseg, seg, kin, cap, &nb, &e);
+    const bool redo = tid < nseg && m.sbn[tid + 1] - m.sbn[tid] > cap;
+    if (__any_sync(0xffffffffu, redo)) mini_sweep<1>(m, redo, tid, nseg, seg, kin, cap, &nb, &e);
   }
   __syncthreads();
   MINI_TICK(6);
