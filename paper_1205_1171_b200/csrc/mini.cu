@@ -654,9 +654,9 @@ int g_mini_seglen = 3;  // child events per time segment (H3D_MINI_SEG / h3d_tun
 
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant) {
-  if (variant == 2) return launch_mini<64, 320, 192>(P, pts, n, lv, j0, j1, err, s);
-  if (variant == 0) return launch_mini<128, 512, 256>(P, pts, n, lv, j0, j1, err, s);
-  return launch_mini<512, 2048, 1024>(P, pts, n, lv, j0, j1, err, s);
+  if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s);
+  if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s);
+  return launch_mini<1024, 2048, 1024>(P, pts, n, lv, j0, j1, err, s);
 }
 
 }  // namespace h3d
