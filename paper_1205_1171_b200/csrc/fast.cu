@@ -1374,7 +1374,7 @@ long long kMiniMaxCtas = 2 * 148;  // H3D_MINI_CTAS
 // the tiny mini variant (several CTAs per SM): at most this many CTAs, and
 // over the lane-per-job kernel only when the longest merged child log is at
 // least kMiniTinyKin events (the lane kernel's serial path then dominates)
-long long kMiniTinyCtas = 8192;  // H3D_MINI_TINY_CTAS
+long long kMiniTinyCtas = 16384;  // H3D_MINI_TINY_CTAS
 long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
 
 // leaf kernel depth: 3 or 4 fused levels, anything below 3 = off
