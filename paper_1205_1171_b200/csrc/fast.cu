@@ -1376,6 +1376,10 @@ long long kMiniMaxCtas = 2 * 148;  // H3D_MINI_CTAS
 // least kMiniTinyKin events (the lane kernel's serial path then dominates)
 long long kMiniTinyCtas = 16384;  // H3D_MINI_TINY_CTAS
 long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
+// after a level on the large mini variant, launch the remaining levels on it
+// without measuring them (no read-back and host sync per level)
+int g_mini_spec = 1;  // H3D_MINI_SPEC
+int g_trace = 0;      // H3D_TRACE: one stderr line per routed level
 
 // leaf kernel depth: 3 or 4 fused levels, anything below 3 = off
 int leaf_depth(long long b) { return b >= 4 ? 4 : (b == 3 ? 3 : 0); }
@@ -1395,6 +1399,8 @@ void load_env_once() {
   if (const char *e = getenv("H3D_MINI_TINY_CTAS")) kMiniTinyCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_KIN")) kMiniTinyKin = atoll(e);
   if (const char *e = getenv("H3D_MINI_SEG")) g_mini_seglen = atoi(e) < 1 ? 1 : atoi(e);
+  if (const char *e = getenv("H3D_MINI_SPEC")) g_mini_spec = atoi(e) ? 1 : 0;
+  if (const char *e = getenv("H3D_TRACE")) g_trace = atoi(e);
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
@@ -1419,6 +1425,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "mini_tiny_ctas") { old = kMiniTinyCtas; if (value >= 0) kMiniTinyCtas = value; }
   else if (k == "mini_tiny_kin") { old = kMiniTinyKin; if (value >= 0) kMiniTinyKin = value; }
   else if (k == "mini_seg") { old = g_mini_seglen; if (value >= 1) g_mini_seglen = static_cast<int>(value); }
+  else if (k == "mini_spec") { old = g_mini_spec; if (value >= 0) g_mini_spec = value ? 1 : 0; }
   else if (k == "big_total") { old = kBigTotal; if (value >= 0) kBigTotal = value; }
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
@@ -1534,6 +1541,9 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
     const long long maxkin = static_cast<long long>(need[8]), sumkin = static_cast<long long>(need[9]);
+    if (g_trace)
+      fprintf(stderr, "h3d level %d: jobs %lld max nS %llu max kin %lld sum kin %lld\n", lv, jobs,
+              need[6], maxkin, sumkin);
     // few small jobs: the in-shared-memory time-split merge (mini.cu)
     // (154 KB of shared memory per CTA: one CTA per SM, so only for levels of
     // at most a few CTAs per SM)
@@ -1557,6 +1567,44 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       if (rm < 0) return rm;
       h3d_prof_end(e0, lv + 5000, 2, s);
       P = Pass2{P.out0, P.out1, P.in0, P.in1};
+      if (g_mini_spec && !mini_small && lv < lv_hi) {
+        // the remaining levels have at most half these jobs: launch them all
+        // on the large variant unmeasured; a job that does not fit records
+        // its level in `spec` (later launches then write nothing) and the
+        // loop resumes, measured, from that level
+        long long *spec = reinterpret_cast<long long *>(w0.need + 12);
+        cudaMemsetAsync(spec, 0, sizeof(long long), s);
+        for (int l2 = lv + 1; l2 <= lv_hi; ++l2) {
+          void *e2 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
+          const long long rs = mini_level(P, sorted_pts, n, l2, p0 >> l2,
+                                          (p1 + (1ll << l2) - 1) >> l2, err, s, 1, spec);
+          if (rs < 0) return rs;
+          if (g_trace) {
+            long long f = 0;
+            cudaMemcpyAsync(&f, spec, sizeof(f), cudaMemcpyDeviceToHost, s);
+            const cudaError_t ce = cudaStreamSynchronize(s);
+            fprintf(stderr, "h3d level %d speculative: flag %lld (%s)\n", l2, f,
+                    cudaGetErrorString(ce));
+          }
+          h3d_prof_end(e2, l2 + 5000, 2, s);
+          P = Pass2{P.out0, P.out1, P.in0, P.in1};
+        }
+        long long failed = 0;
+        if (h3d_check(cudaMemcpyAsync(&failed, spec, sizeof(failed), cudaMemcpyDeviceToHost, s)) ||
+            h3d_check(cudaStreamSynchronize(s)))
+          return H3D_E_CUDA;
+        if (g_trace)
+          fprintf(stderr, "h3d levels %d..%d speculative on the large mini: failed at %lld\n",
+                  lv + 1, lv_hi, failed);
+        if (failed == 0) {
+          lv = lv_hi;
+          break;
+        }
+        // redo from the failed level: it reads buffer (f-1)&1, intact
+        const int f = static_cast<int>(failed);
+        P = (f & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
+        lv = f - 1;
+      }
       continue;
     }
     // large merge jobs: the time-split pipeline (big.cu)

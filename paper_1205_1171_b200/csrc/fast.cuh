@@ -169,7 +169,8 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
 // variant 0: jobs of <= 256 points and 512 child events (~40 KB, several
 // CTAs per SM); variant 1: <= 1024 points and 2048 events (~154 KB)
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
-                     long long j1, long long *err, cudaStream_t s, int variant);
+                     long long j1, long long *err, cudaStream_t s, int variant,
+                     long long *spec = nullptr);
 constexpr int kMiniMaxPoints = 1024, kMiniMaxEvents = 2048;
 constexpr int kMiniSmallPoints = 256, kMiniSmallEvents = 512;
 constexpr int kMiniTinyPoints = 192, kMiniTinyEvents = 320;

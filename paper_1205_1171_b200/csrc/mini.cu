@@ -226,7 +226,7 @@ __device__ bool mini_sweep(MS &m, bool active, int s, int nseg, int seg, int kin
 template <int MINI_T, int MINI_K, int MINI_N>
 __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int lv, long long j0, long long j1,
-                                                 long long *err, int seglen) {
+                                                 long long *err, int seglen, long long *spec) {
   typedef MiniSmem<MINI_T, MINI_K, MINI_N> MS;
   constexpr int MINI_B = MS::MINI_B;
   constexpr int PER = (MINI_K + MINI_T) / MINI_T;  // blocked-scan items per thread
@@ -236,7 +236,17 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   const int tid = threadIdx.x, T = MINI_T;
   const long long j = j0 + blockIdx.x;
   if (j >= j1) return;
-  if (*reinterpret_cast<volatile long long *>(err) != 0) return;
+  // Stop when an earlier launch failed, or (speculative top levels) when a
+  // job of an earlier level did not fit, so this level's input is not valid:
+  // write nothing, the host redoes from there.  One thread reads the flags
+  // and the CTA decides together -- the flags can change while the CTA
+  // starts, and a split exit would leave the barriers below short.
+  __shared__ int s_stop;
+  if (threadIdx.x == 0)
+    s_stop = *reinterpret_cast<volatile long long *>(err) != 0 ||
+             (spec && *reinterpret_cast<volatile long long *>(spec) != 0);
+  __syncthreads();
+  if (s_stop) return;
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   const double zs = blockIdx.y ? -1.0 : 1.0;
@@ -255,8 +265,14 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   }
   const int2 hr = in.hdr[2 * j + 1];
   const int nSL = hl.x, nS = hl.x + hr.x, kL = hl.y, kR = hr.y, kin = kL + kR;
-  if (nS > MINI_N || kin > MINI_K) {  // the host routes only fitting levels here
-    if (tid == 0) raise_err(err, E_FASTPATH);
+  if (nS > MINI_N || kin > MINI_K) {  // the host routes only fitting levels here ...
+    if (tid == 0) {
+      if (spec)  // ... or launched it unmeasured: report the level, no fallback
+        atomicCAS(reinterpret_cast<unsigned long long *>(spec), 0ull,
+                  static_cast<unsigned long long>(lv));
+      else
+        raise_err(err, E_FASTPATH);
+    }
     return;
   }
   if (tid == 0) m.flag = 0;
@@ -635,7 +651,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
 
 template <int T, int K, int N>
 static long long launch_mini(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
-                             long long j1, long long *err, cudaStream_t s) {
+                             long long j1, long long *err, cudaStream_t s, long long *spec) {
   static bool attr = false;
   const size_t bytes = sizeof(MiniSmem<T, K, N>);
   if (!attr) {
@@ -646,17 +662,17 @@ static long long launch_mini(const Pass2 &P, const double *pts, long long n, int
   }
   h3d_count_launches(1);
   k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, bytes, s>>>(P, pts, n, lv, j0, j1,
-                                                                          err, g_mini_seglen);
+                                                                          err, g_mini_seglen, spec);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
 
 int g_mini_seglen = 3;  // child events per time segment (H3D_MINI_SEG / h3d_tune)
 
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
-                     long long j1, long long *err, cudaStream_t s, int variant) {
-  if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s);
-  if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s);
-  return launch_mini<1024, 2048, 1024>(P, pts, n, lv, j0, j1, err, s);
+                     long long j1, long long *err, cudaStream_t s, int variant, long long *spec) {
+  if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s, spec);
+  if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s, spec);
+  return launch_mini<1024, 2048, 1024>(P, pts, n, lv, j0, j1, err, s, spec);
 }
 
 }  // namespace h3d

@@ -26,6 +26,8 @@ ROUTES = {
     "no_leaf_no_big": {"leaf_b": 0, "big_kin": BIG_OFF},
     "leaf4": {"leaf_b": 4},
     "leaf_b2_is_off": {"leaf_b": 2},
+    "mini_spec_off": {"mini_spec": 0},  # top levels measured one by one
+    "mini_seg16": {"mini_seg": 16},
     "big_everywhere": {"big_kin": 16, "mini": 0},
     "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0, "mini": 0},
     "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0},
@@ -100,6 +102,8 @@ KNOB_CHOICES = {
     "mini_ctas": [0, 4, 296, BIG_OFF],
     "mini_tiny_ctas": [0, 64, 8192, BIG_OFF],
     "mini_tiny_kin": [0, 160, BIG_OFF],
+    "mini_seg": [1, 3, 16],
+    "mini_spec": [0, 1],
 }
 
 
