@@ -57,7 +57,7 @@ def _worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_distributed_equals_single_gpu(world, large_json):
     import paper_1205_1171_b200 as H
     from paper_1205_1171_b200.generators import generate
