@@ -435,6 +435,12 @@ def run_ours_distributed(args):
     for _ in range(args.warmup):
         convex_hull_3d_distributed(pinned, dev)
     e2e_ms, r = timed(lambda: convex_hull_3d_distributed(pinned, dev))
+    # one untimed call with phase events: where a rank's step goes
+    import paper_1205_1171_b200.multigpu as MG
+    MG.PHASES = []
+    convex_hull_3d_distributed(pts_dev, dev, return_device=True)
+    phases = MG.PHASES[0] if MG.PHASES else None
+    MG.PHASES = None
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -455,6 +461,9 @@ def run_ours_distributed(args):
                 "h2d_split": f"each rank copies 24n/{ws} bytes; NVLink all-gather assembles "
                              "the cloud (multigpu.gather_input)"},
         "gpu_launches": launches, "roofline": None, "cpu_baseline": None, "clocks": clk,
+        "rank0_phases_ms": phases,
+        "note": "roofline and cpu_baseline are on the N=1 line; rank0_phases_ms: one untimed "
+                "call, presort / slab levels / cross levels (device events)",
     }
     print(json.dumps(line), flush=True)
     dist.destroy_process_group()

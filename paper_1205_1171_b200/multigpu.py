@@ -279,6 +279,15 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
     dev = pts_dev.device
     s = stream_ptr(dev)
     plan = SlabPlan(n, world)
+    marks = []  # (name, event) phase boundaries, only when PHASES is set
+
+    def mark(name):
+        if PHASES is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(torch.cuda.current_stream(dev))
+            marks.append((name, e))
+
+    mark("start")
     sh = sharded_presort(pts_dev, plan, rank) if n >= SHARD_PRESORT_MIN else None
     if sh is not None:
         (sorted_pts, order), perturbed = sh, False
@@ -292,11 +301,13 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
     state = torch.zeros(4, dtype=torch.int64, device=dev)
     err = state[0:1]
     sl = plan.slab(rank)
+    mark("presort")
     if sl is not None:
         r = L.h3d_fast_passes_range(sorted_pts.data_ptr(), n, sl[0], sl[1], 1, plan.slab_level,
                                     ws[0].data_ptr(), ws[1].data_ptr(), wsb, err.data_ptr(), 0, s)
         if r < 0:
             err.fill_(int(r))
+    mark("slab_levels")
     for lv in range(plan.slab_level + 1, plan.levels + 1):
         role, peer = plan.role(lv, rank)
         prev_buf = (lv - 1) & 1
@@ -312,6 +323,10 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
                                         0, s)
             if r < 0:
                 err.fill_(int(r))
+    mark("cross_levels")
+    if PHASES is not None:
+        torch.cuda.synchronize(dev)
+        PHASES.append({b[0]: round(a[1].elapsed_time(b[1]), 4) for a, b in zip(marks, marks[1:])})
     # any error anywhere sends the whole hull to the exact engine on rank 0
     flag = (err != 0).to(torch.int64)
     if _p2p_via_host():
@@ -335,6 +350,7 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
 
 
 GATHER_INPUT_MIN = 1 << 16
+PHASES: list | None = None  # set to a list to get this rank's phase times (ms)
 
 
 def gather_input(points, dev: torch.device, rank: int, world: int) -> torch.Tensor:

@@ -50,8 +50,13 @@ def _worker(rank, world, port, cases, q):
             r = convex_hull_3d_distributed(generate(n, dist_name, seed))
             if rank == 0:
                 out[(n, dist_name, seed)] = (r.faces, r.vertices)
+        multigpu.PHASES = []  # one call with phase events (bench.py's rank0_phases_ms)
+        convex_hull_3d_distributed(generate(2**18, "ball", 4))
+        phases = multigpu.PHASES
+        multigpu.PHASES = None
         if rank == 0:
             out["sharded"] = multigpu.SHARDED_RUNS[0]
+            out["phases"] = phases
             q.put(out)
     finally:
         dist.destroy_process_group()
@@ -77,7 +82,9 @@ def test_distributed_equals_single_gpu(world, large_json):
         p.join(timeout=120)
         assert p.exitcode == 0
     # the two cases >= SHARD_PRESORT_MIN points sort only their own slabs
-    assert got.pop("sharded") == 2
+    assert got.pop("sharded") == 3  # incl. the phase-timed call
+    (ph,) = got.pop("phases")
+    assert set(ph) == {"presort", "slab_levels", "cross_levels"} and min(ph.values()) >= 0
     for key, (faces, verts) in got.items():
         ref = H.convex_hull_3d(generate(*key))
         assert np.array_equal(faces, ref.faces), key
