@@ -399,9 +399,16 @@ def run_ours_distributed(args):
     from paper_1205_1171_b200.multigpu import SlabPlan, convex_hull_3d_distributed
 
     ws, rank, local = dist_env()
+    if os.environ.get("H3D_DIST_ONE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    # H3D_DIST_BACKEND=gloo (+ H3D_DIST_ONE_GPU=1): a functional run of this
+    # multi-rank path on a one-GPU box (timings meaningless); NCCL otherwise
+    if os.environ.get("H3D_DIST_BACKEND", "nccl") == "gloo":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     n, dist_name, seed, label = CONFIGS[args.config]
     pts_host = generate(n, dist_name, seed)
     pinned = torch.from_numpy(pts_host).pin_memory()
