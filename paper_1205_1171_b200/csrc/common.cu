@@ -74,10 +74,11 @@ extern "C" void h3d_profile_enable(int32_t on) {
 extern "C" int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms, int64_t max) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   int64_t m = 0;
+  // every record is on one stream: waiting for the last end event covers all
+  if (!g_prof.empty()) cudaEventSynchronize(g_prof.back().e1);
   for (auto &r : g_prof) {
     if (m < max) {
       float t = 0.f;
-      cudaEventSynchronize(r.e1);
       cudaEventElapsedTime(&t, r.e0, r.e1);
       level[m] = r.level;
       pass[m] = r.pass;
