@@ -476,7 +476,7 @@ template <bool XYZ>
 __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int level, long long j0,
                                                  long long j1, long long *err, int pool,
-                                                 int jpc) {
+                                                 int jpc, int prefetch) {
   // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
   if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0)) return;
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
@@ -585,6 +585,13 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
 #pragma unroll
       for (int q = 0; q < U; ++q)
         if (x0 + q * 32 + lane < tot_pts) c[q] = load_pt(pts, g[q], zs);
+    } else if (prefetch) {
+      // the sweep reads these rows through the ids: start them towards L2
+      // (pays on the large, DRAM-miss-bound levels; the host decides)
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+        if (x0 + q * 32 + lane < tot_pts)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pts + 3ll * g[q]));
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
@@ -1380,6 +1387,7 @@ long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
 // without measuring them (no read-back and host sync per level)
 int g_mini_spec = 1;  // H3D_MINI_SPEC
 int g_trace = 0;      // H3D_TRACE: one stderr line per routed level
+long long kTpjPrefetchJobs = 1ll << 18;  // H3D_TPJ_PREFETCH: L2 prefetch of rows from this many jobs
 
 // leaf kernel depth: 3 or 4 fused levels, anything below 3 = off
 int leaf_depth(long long b) { return b >= 4 ? 4 : (b == 3 ? 3 : 0); }
@@ -1401,13 +1409,15 @@ void load_env_once() {
   if (const char *e = getenv("H3D_MINI_SEG")) g_mini_seglen = atoi(e) < 1 ? 1 : atoi(e);
   if (const char *e = getenv("H3D_MINI_SPEC")) g_mini_spec = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_TRACE")) g_trace = atoi(e);
+  if (const char *e = getenv("H3D_TPJ_PREFETCH")) kTpjPrefetchJobs = atoll(e);
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
 template <bool XYZ>
-void launch_tpj(dim3 grid, int pool, int jpc, cudaStream_t s, Pass2 P, const double *pts,
+void launch_tpj(dim3 grid, int pool, int jpc, int prefetch, cudaStream_t s, Pass2 P,
+                const double *pts,
                 long long n, int lv, long long j0, long long j1, long long *err) {
-  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc);
+  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch);
 }
 
 }  // namespace
@@ -1642,9 +1652,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       h3d_count_launches(1);
       const dim3 grid(h3d_grid(jobs, jpc), 2);
       if (xyz)
-        launch_tpj<true>(grid, static_cast<int>(pool), jpc, s, P, sorted_pts, n, lv, j0, j1, err);
+        launch_tpj<true>(grid, static_cast<int>(pool), jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err);
       else
-        launch_tpj<false>(grid, static_cast<int>(pool), jpc, s, P, sorted_pts, n, lv, j0, j1, err);
+        launch_tpj<false>(grid, static_cast<int>(pool), jpc, jobs >= kTpjPrefetchJobs ? 1 : 0, s, P,
+                          sorted_pts, n, lv, j0, j1, err);
       h3d_prof_end(e0, lv + 1000, 2, s);
     } else {
       long long wpool = static_cast<long long>(need[7]);
