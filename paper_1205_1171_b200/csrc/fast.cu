@@ -1341,6 +1341,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, const double 
 // facets of both passes: lower block then upper block, sorted indices
 __global__ void k_fast_extract(GroupBuf lo, GroupBuf up, int *faces, long long cap,
                                long long *counts, long long *err) {
+  // a level failed: its buffers hold nothing valid (the caller falls back)
+  if (*reinterpret_cast<volatile long long *>(err) != 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = counts[1] = 0;
+    return;
+  }
   const int kLo = lo.hdr[0].y, kUp = up.hdr[0].y;
   long long F = (long long)kLo + kUp;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1547,9 +1552,18 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 2 * 148 ? 2 * 148 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
         P, n, lv, j0, j1, w0.need);
     unsigned long long need[10];
+    long long herr = 0;
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
+        h3d_check(cudaMemcpyAsync(&herr, err, sizeof(herr), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
+    // A launch declined the input (or failed): its level wrote nothing, so
+    // the groups this level would read are stale -- stop routing; the caller
+    // sees the error word and hands the hull to the exact engine.
+    if (herr != 0) {
+      if (g_trace) fprintf(stderr, "h3d level %d: error %lld set, levels stop\n", lv, herr);
+      break;
+    }
     const long long maxkin = static_cast<long long>(need[8]), sumkin = static_cast<long long>(need[9]);
     if (g_trace)
       fprintf(stderr, "h3d level %d: jobs %lld max nS %llu max kin %lld sum kin %lld\n", lv, jobs,
@@ -1599,10 +1613,15 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           h3d_prof_end(e2, l2 + 5000, 2, s);
           P = Pass2{P.out0, P.out1, P.in0, P.in1};
         }
-        long long failed = 0;
+        long long failed = 0, serr = 0;
         if (h3d_check(cudaMemcpyAsync(&failed, spec, sizeof(failed), cudaMemcpyDeviceToHost, s)) ||
+            h3d_check(cudaMemcpyAsync(&serr, err, sizeof(serr), cudaMemcpyDeviceToHost, s)) ||
             h3d_check(cudaStreamSynchronize(s)))
           return H3D_E_CUDA;
+        if (serr != 0) {
+          lv = lv_hi;
+          break;
+        }
         if (g_trace)
           fprintf(stderr, "h3d levels %d..%d speculative on the large mini: failed at %lld\n",
                   lv + 1, lv_hi, failed);

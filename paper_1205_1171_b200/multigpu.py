@@ -163,6 +163,17 @@ def _group_views(lay, buf: int, L: int, nS: int, k: int):
     return (lay.lnk_view(buf, L, nS), lay.gid_view(buf, L, nS), lay.ev_view(buf, L, k))
 
 
+def _sizes(h, p: int, level: int):
+    """(nS, k) of pass p from a header, clamped to the group's slot capacity
+    (2^level points, twice as many event slots): after a declined level the
+    header may be stale, and both sides must still size the same views
+    inside the group (the result is discarded by the error flag)."""
+    cap = 1 << level
+    nS = min(max(int(h[2 * p]), 0), cap)
+    k = min(max(int(h[2 * p + 1]), 0), 2 * cap)
+    return nS, k
+
+
 def send_group(layouts, buf: int, level: int, g: int, dst: int, rows=None) -> None:
     """Ship group g of `level` (in buffer `buf`) of both passes to rank dst:
     the header, then ONE packed payload (links, ids, events of both passes;
@@ -175,7 +186,7 @@ def send_group(layouts, buf: int, level: int, g: int, dst: int, rows=None) -> No
     h = hdr.cpu().tolist()
     parts = []
     for p, lay in enumerate(layouts):
-        nS, k = h[2 * p], h[2 * p + 1]
+        nS, k = _sizes(h, p, level)
         parts.extend(v for v in _group_views(lay, buf, L, nS, k) if v.numel())
         if rows is not None and nS:
             parts.append(_rows_of(lay.gid_view(buf, L, nS), rows).view(torch.uint8).reshape(-1))
@@ -194,7 +205,7 @@ def recv_group(layouts, buf: int, level: int, g: int, src: int, rows=None) -> No
     h = hdr.cpu().tolist()
     total = 0
     for p, lay in enumerate(layouts):
-        nS, k = h[2 * p], h[2 * p + 1]
+        nS, k = _sizes(h, p, level)
         lay.hdr_view(buf, g).copy_(hdr[2 * p:2 * p + 2].view(torch.uint8))
         total += sum(v.numel() for v in _group_views(lay, buf, L, nS, k))
         if rows is not None:
@@ -205,7 +216,7 @@ def recv_group(layouts, buf: int, level: int, g: int, src: int, rows=None) -> No
     _recv(payload, src)
     at = 0
     for p, lay in enumerate(layouts):
-        nS, k = h[2 * p], h[2 * p + 1]
+        nS, k = _sizes(h, p, level)
         for view in _group_views(lay, buf, L, nS, k):
             view.copy_(payload[at:at + view.numel()])
             at += view.numel()

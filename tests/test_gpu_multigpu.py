@@ -28,6 +28,22 @@ def _port():
     return p
 
 
+def make(n, kind, seed):
+    """Test clouds: the generators' distributions, plus inputs the sharded
+    presort must decline on every rank -- x ties ("int": a small integer
+    range) and one long run of equal sort keys ("slab_x")."""
+    from paper_1205_1171_b200.generators import generate, integer_cloud
+
+    if kind == "int":
+        return integer_cloud(n, seed, half_range=2**12)
+    if kind == "slab_x":
+        rng = np.random.default_rng(seed)
+        p = rng.uniform(-1.0, 1.0, (n, 3))
+        p[: n - 64, 0] = rng.uniform(0.0, 1e-12, n - 64)
+        return p
+    return generate(n, kind, seed)
+
+
 def _worker(rank, world, port, cases, q):
     import sys
 
@@ -47,7 +63,7 @@ def _worker(rank, world, port, cases, q):
 
         out = {}
         for n, dist_name, seed in cases:
-            r = convex_hull_3d_distributed(generate(n, dist_name, seed))
+            r = convex_hull_3d_distributed(make(n, dist_name, seed))
             if rank == 0:
                 out[(n, dist_name, seed)] = (r.faces, r.vertices)
         multigpu.PHASES = []  # one call with phase events (bench.py's rank0_phases_ms)
@@ -70,7 +86,7 @@ def test_distributed_equals_single_gpu(world, large_json):
     # the 2^18 sphere sends its cross-rank levels through the time-split
     # pipeline (large merged logs), the others through the mini/warp merges
     cases = [(1000, "ball", 1), (3 * 1024 + 7, "sphere", 2), (5000, "cube", 3), (2**20, "ball", 0),
-             (2**18, "sphere", 5)]
+             (2**18, "sphere", 5), (70000, "int", 6), (70000, "slab_x", 7)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -81,12 +97,13 @@ def test_distributed_equals_single_gpu(world, large_json):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    # the two cases >= SHARD_PRESORT_MIN points sort only their own slabs
-    assert got.pop("sharded") == 3  # incl. the phase-timed call
+    # the two general-position cases >= SHARD_PRESORT_MIN points sort only
+    # their own slabs (+ the phase-timed call); "int" and "slab_x" decline
+    assert got.pop("sharded") == 3
     (ph,) = got.pop("phases")
     assert set(ph) == {"presort", "slab_levels", "cross_levels"} and min(ph.values()) >= 0
     for key, (faces, verts) in got.items():
-        ref = H.convex_hull_3d(generate(*key))
+        ref = H.convex_hull_3d(make(*key))
         assert np.array_equal(faces, ref.faces), key
         assert np.array_equal(verts, ref.vertices), key
     f, _ = got[(2**20, "ball", 0)]
