@@ -13,6 +13,21 @@ ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 def make(n, kind, seed):
     sys.path.insert(0, ROOT)
     from paper_1205_1171_b200.generators import generate, integer_cloud
+    rng = np.random.default_rng(seed)
+    if kind == "clusters":
+        c = rng.uniform(-1, 1, (12, 3))
+        return c[rng.integers(0, 12, n)] + rng.normal(0, 1e-7, (n, 3))
+    if kind == "near_plane":
+        p = rng.uniform(-1, 1, (n, 3))
+        p[:, 2] = 0.2 * p[:, 0] - 0.4 * p[:, 1] + rng.normal(0, 1e-10, n)
+        p[:8, 2] += 1.0
+        return p
+    if kind == "paraboloid":
+        p = rng.uniform(-1, 1, (n, 3))
+        p[:, 2] = p[:, 0] ** 2 + p[:, 1] ** 2
+        return p
+    if kind == "int_wide":
+        return integer_cloud(n, seed)
     if kind == "int":
         return integer_cloud(n, seed, half_range=2**12)
     if kind == "slab_x":
@@ -34,9 +49,16 @@ def worker(rank, world, port, cases):
     from paper_1205_1171_b200.multigpu import convex_hull_3d_distributed
     for n, kind, seed in cases:
         try:
-            r = convex_hull_3d_distributed(make(n, kind, seed))
+            pts = make(n, kind, seed)
+            r = convex_hull_3d_distributed(pts)
             if rank == 0:
-                print("rank0", n, kind, seed, "faces", len(r.faces), flush=True)
+                import paper_1205_1171_b200 as H
+                try:
+                    ref = H.convex_hull_3d(pts)
+                    same = np.array_equal(r.faces, ref.faces) and np.array_equal(r.vertices, ref.vertices)
+                except Exception as exc:  # noqa: BLE001
+                    same = f"single GPU raised {type(exc).__name__}"
+                print("rank0", n, kind, seed, "faces", len(r.faces), "same as 1 GPU:", same, flush=True)
         except Exception as exc:
             import traceback
             if rank == 0:
