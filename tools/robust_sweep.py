@@ -10,7 +10,6 @@ import numpy as np
 sys.path.insert(0, ".")
 import paper_1205_1171_b200 as H  # noqa: E402
 from paper_1205_1171_b200 import fast  # noqa: E402
-from oracle import oracle as O  # noqa: E402
 from paper_1205_1171_b200.generators import generate  # noqa: E402
 
 
@@ -53,20 +52,29 @@ def outcome(fn, pts):
 
 FAMS = ["ball", "sphere", "cube", "gauss", "int_small", "int_wide", "clusters", "near_plane",
         "thin_slab_x", "shell_ball", "paraboloid"]
-max_n = int(sys.argv[1]) if len(sys.argv) > 1 else 300_000
-rng = np.random.default_rng(20261017)
-bad = 0
-t0 = time.time()
-for n in (10_007, 65_537, 131_072, max_n):
-    for fam in FAMS:
-        pts = family(fam, n, rng)
-        got, exp = outcome(H.convex_hull_3d, pts), outcome(O.convex_hull_3d, pts)
-        same = got[0] == exp[0] and (
-            (got[0] == "ok" and np.array_equal(got[1], exp[1]) and np.array_equal(got[2], exp[2]))
-            or (got[0] == "err" and got[1:] == exp[1:]))
-        if not same:
-            bad += 1
-        print(f"n={n} {fam}: {'same' if same else 'DIFFERENT'} ({got[0]}"
-              f"{'' if got[0] == 'ok' else ' ' + got[1]}), fallbacks so far "
-              f"{fast.FALLBACKS[0]}", flush=True)
-print(f"done in {time.time() - t0:.0f}s, {bad} mismatches")
+
+
+def main():
+    max_n = int(sys.argv[1]) if len(sys.argv) > 1 else 300_000
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(20261017)
+    bad = 0
+    t0 = time.time()
+    for n in (10_007, 65_537, 131_072, max_n):
+        for fam in FAMS:
+            pts = family(fam, n, rng)
+            got, exp = outcome(H.convex_hull_3d, pts), outcome(O.convex_hull_3d, pts)
+            same = got[0] == exp[0] and (
+                (got[0] == "ok" and np.array_equal(got[1], exp[1]) and np.array_equal(got[2], exp[2]))
+                or (got[0] == "err" and got[1:] == exp[1:]))
+            if not same:
+                bad += 1
+            print(f"n={n} {fam}: {'same' if same else 'DIFFERENT'} ({got[0]}"
+                  f"{'' if got[0] == 'ok' else ' ' + got[1]}), fallbacks so far "
+                  f"{fast.FALLBACKS[0]}", flush=True)
+    print(f"done in {time.time() - t0:.0f}s, {bad} mismatches")
+
+
+if __name__ == "__main__":
+    main()
