@@ -1378,7 +1378,8 @@ long long kTpjXyzMax = 16 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the
 long long kBigKin = 1000;          // H3D_BIG_KIN: time-split pipeline from this job log size
 long long kBigTotal = 200000;     // H3D_BIG_TOTAL: ... or half that with this many child events in the level
 
-bool g_attr_done = false;
+// shared-memory attributes are per device: set once per device used
+bool g_attr_done[64] = {};
 bool g_env_done = false;
 int g_leaf_b = 3;  // H3D_LEAF_B: levels 1..B fused (0 = off)
 int g_mini = 1;    // H3D_MINI: few small jobs -> mini.cu (0 = warp kernel)
@@ -1485,7 +1486,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   const size_t bb = base_pass_bytes(n);
   void *big_ws = workspace_bytes > bb ? static_cast<char *>(ws_lower) + bb : nullptr;
   const size_t big_bytes = workspace_bytes > bb ? workspace_bytes - bb : 0;
-  if (!g_attr_done) {
+  int dev_id = 0;
+  cudaGetDevice(&dev_id);
+  if (dev_id < 0 || dev_id >= 64) return H3D_E_ARG;
+  if (!g_attr_done[dev_id]) {
     if (h3d_check(cudaFuncSetAttribute(k_fast_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kWarpPoolMax))) ||
         h3d_check(cudaFuncSetAttribute(k_fast_tpj<true>,
@@ -1499,7 +1503,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         h3d_check(cudaFuncSetAttribute(k_fast_leaf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        32 * leaf_lane_bytes<4>())))
       return H3D_E_CUDA;
-    g_attr_done = true;
+    g_attr_done[dev_id] = true;
   }
   long long *err = reinterpret_cast<long long *>(err_dev);
   int levels = 0;

@@ -652,13 +652,16 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
 template <int T, int K, int N>
 static long long launch_mini(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                              long long j1, long long *err, cudaStream_t s, long long *spec) {
-  static bool attr = false;
+  static bool attr[64] = {};  // the attribute is per device
+  int dev_id = 0;
+  cudaGetDevice(&dev_id);
+  if (dev_id < 0 || dev_id >= 64) return H3D_E_ARG;
   const size_t bytes = sizeof(MiniSmem<T, K, N>);
-  if (!attr) {
+  if (!attr[dev_id]) {
     if (h3d_check(cudaFuncSetAttribute(k_mini<T, K, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(bytes))))
       return H3D_E_CUDA;
-    attr = true;
+    attr[dev_id] = true;
   }
   h3d_count_launches(1);
   k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, bytes, s>>>(P, pts, n, lv, j0, j1,
