@@ -10,6 +10,7 @@ CUDA device or the built library this raises.
 
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -75,6 +76,15 @@ class CudaBackend:
 
     def __repr__(self):
         return f"CudaBackend(device={self.device}, engine={self.engine!r})"
+
+
+_LOCKS: dict = {}
+_LOCKS_GUARD = threading.Lock()
+
+
+def _device_lock(dev: torch.device) -> threading.Lock:
+    with _LOCKS_GUARD:
+        return _LOCKS.setdefault(str(dev), threading.Lock())
 
 
 def _device_of(points, backend) -> torch.device:
@@ -263,15 +273,18 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
             verts, faces = verts.cpu().numpy(), faces.cpu().numpy()
         return HullResult(vertices=verts, faces=faces, stats=stats)
 
-    sort_t0 = time.perf_counter()
-    sorted_pts, order, perturbed = presort(pts)
-    sort_ms = (time.perf_counter() - sort_t0) * 1e3
+    # the per-device workspaces are shared: one hull at a time per device
+    # (calls from several threads are serialised, not interleaved)
+    with _device_lock(dev):
+        sort_t0 = time.perf_counter()
+        sorted_pts, order, perturbed = presort(pts)
+        sort_ms = (time.perf_counter() - sort_t0) * 1e3
 
-    lower_levels: list[float] = []
-    upper_levels: list[float] = []
-    raw, k_lo, k_up, lo_ms, up_ms = _run_passes(sorted_pts, engine, solver,
-                                                (lower_levels, upper_levels))
-    verts, faces = orient_remap(sorted_pts, order, raw)
+        lower_levels: list[float] = []
+        upper_levels: list[float] = []
+        raw, k_lo, k_up, lo_ms, up_ms = _run_passes(sorted_pts, engine, solver,
+                                                    (lower_levels, upper_levels))
+        verts, faces = orient_remap(sorted_pts, order, raw)
     if not return_device:
         verts, faces = to_host(verts), to_host(faces)
     total_ms = (time.perf_counter() - total_t0) * 1e3

@@ -123,3 +123,29 @@ def test_every_point_inside_hull():
         dist = nrm @ pts.T - np.einsum("ij,ij->i", nrm, a)[:, None]
         assert dist.max() <= 1e-9 * scale
         assert len(res.faces) == 2 * len(res.vertices) - 4
+
+
+def test_concurrent_threads_one_device(oracle_mod):
+    """Hulls from several Python threads on one device (shared workspaces)
+    are serialised per device and all correct."""
+    import threading
+
+    import numpy as np
+
+    import paper_1205_1171_b200 as H
+    from paper_1205_1171_b200.generators import generate
+
+    clouds = [generate(30000 + 17 * i, ("ball", "sphere", "cube")[i % 3], i) for i in range(6)]
+    exp = [oracle_mod.convex_hull_3d(p).faces for p in clouds]
+    got = [None] * len(clouds)
+
+    def run(i):
+        got[i] = H.convex_hull_3d(clouds[i]).faces
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(clouds))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for g, e in zip(got, exp):
+        assert np.array_equal(g, e)
