@@ -411,7 +411,10 @@ __host__ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
 // merged child log of one job; out[9] = all merged child logs.  One warp per 32
 // jobs, coalesced header reads.
 __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1,
-                           unsigned long long *out) {
+                           unsigned long long *out, const long long *err) {
+  // out[10] = the error word, read back with the measurement (one copy)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    out[10] = static_cast<unsigned long long>(*reinterpret_cast<const volatile long long *>(err));
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const long long size = 1ll << level, half = size >> 1;
   const int lane = threadIdx.x & 31;
@@ -1554,13 +1557,12 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
     k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 2 * 148 ? 2 * 148 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
-        P, n, lv, j0, j1, w0.need);
-    unsigned long long need[10];
-    long long herr = 0;
+        P, n, lv, j0, j1, w0.need, err);
+    unsigned long long need[11];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
-        h3d_check(cudaMemcpyAsync(&herr, err, sizeof(herr), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
+    const long long herr = static_cast<long long>(need[10]);
     // A launch declined the input (or failed): its level wrote nothing, so
     // the groups this level would read are stale -- stop routing; the caller
     // sees the error word and hands the hull to the exact engine.
