@@ -193,7 +193,7 @@ int64_t h3d_tune(const char *name, int64_t value);
 /* bytes of workspace one h3d_fast_pass needs for n points (two compact
  * group buffers: headers, int2 links, ids, 24-byte events; HBM scratch of
  * the warp merge; and, in the lower pass's workspace, the scratch of the
- * time-split pipeline for large merge jobs, sized for min(n, 2^21) points
+ * time-split pipeline for large merge jobs, sized for min(n, max(2^21, n/8)) points
  * per pass -- levels beyond it fall back to the warp merge) */
 size_t h3d_fast_pass_workspace_bytes(int64_t n);
 

@@ -165,8 +165,11 @@ static bool carve_big(h3d_arena &ar, long long m, BigWS &b) {
   return ar.base == nullptr || b.tmp != nullptr;
 }
 
+// points per pass the pipeline's scratch holds (~1.3 KB each): an eighth of
+// the cloud, at least 2^21 -- the mid levels of a 2^27 mixed cloud need
+// 2^24 (C5 levels 10-12: 22-28 ms on the lane kernel, 4-15 ms here)
 long long big_capacity(long long n) {
-  long long cap = 1ll << 21;
+  long long cap = n / 8 > (1ll << 21) ? n / 8 : (1ll << 21);
   if (const char *e = getenv("H3D_BIG_CAP")) cap = atoll(e);
   return n < cap ? n : cap;
 }

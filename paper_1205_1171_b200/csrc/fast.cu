@@ -1380,6 +1380,7 @@ int kTpjMaxLevel = 40;          // H3D_TPJ_MAX_LEVEL
 long long kTpjXyzMax = 16 * 1024;  // H3D_TPJ_XYZ_KB: stage coordinates when the pool fits
 long long kBigKin = 1000;          // H3D_BIG_KIN: time-split pipeline from this job log size
 long long kBigTotal = 200000;     // H3D_BIG_TOTAL: ... or half that with this many child events in the level
+long long kBigMaxJobs = 1ll << 18;  // H3D_BIG_MAX_JOBS: ... and fewer jobs (both passes) than this
 
 // shared-memory attributes are per device: set once per device used
 bool g_attr_done[64] = {};
@@ -1411,6 +1412,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_LEAF_B")) g_leaf_b = atoi(e);
   if (const char *e = getenv("H3D_BIG_KIN")) kBigKin = atoll(e);
   if (const char *e = getenv("H3D_BIG_TOTAL")) kBigTotal = atoll(e);
+  if (const char *e = getenv("H3D_BIG_MAX_JOBS")) kBigMaxJobs = atoll(e);
   if (const char *e = getenv("H3D_MINI")) g_mini = atoi(e);
   if (const char *e = getenv("H3D_MINI_CTAS")) kMiniMaxCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_CTAS")) kMiniTinyCtas = atoll(e);
@@ -1446,6 +1448,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "mini_seg") { old = g_mini_seglen; if (value >= 1) g_mini_seglen = static_cast<int>(value); }
   else if (k == "mini_spec") { old = g_mini_spec; if (value >= 0) g_mini_spec = value ? 1 : 0; }
   else if (k == "big_total") { old = kBigTotal; if (value >= 0) kBigTotal = value; }
+  else if (k == "big_max_jobs") { old = kBigMaxJobs; if (value >= 0) kBigMaxJobs = value; }
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
   else if (k == "tpj_max_level") { old = kTpjMaxLevel; if (value >= 0) kTpjMaxLevel = static_cast<int>(value); }
@@ -1644,7 +1647,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     }
     // large merge jobs: the time-split pipeline (big.cu)
     // (its fixed cost, ~25 launches, only pays when the level has work)
-    if (big_ws && (maxkin >= kBigKin || (2 * maxkin >= kBigKin && sumkin >= kBigTotal))) {
+    // (many moderate jobs keep the lane kernel busy: the second clause only
+    // for levels of fewer jobs)
+    if (big_ws && (maxkin >= kBigKin ||
+                   (2 * maxkin >= kBigKin && sumkin >= kBigTotal && 2 * jobs < kBigMaxJobs))) {
       const long long rb = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s);
       if (rb < 0) return rb;
       if (rb == 0) {

@@ -95,6 +95,7 @@ KNOB_CHOICES = {
     "leaf_b": [0, 1, 2, 3, 4],
     "big_kin": [2, 16, 300, 1000, BIG_OFF],
     "big_total": [0, 1000, 200000],
+    "big_max_jobs": [0, 1 << 18, BIG_OFF],
     "tpj_min_jobs": [1, 64, 4736, BIG_OFF],
     "tpj_xyz_kb": [0, 16, 200],
     "tpj_max_level": [2, 6, 40],
