@@ -148,30 +148,30 @@ struct GEvOut {
   Ev *__restrict__ p;
   __device__ __forceinline__ void put(long long k, const Ev &o) const { p[k] = o; }
 };
-// ... or lane-interleaved shared memory (leaf kernel): time + one word with
-// the 8-bit ids a, b, c and the kind
+// ... or lane-interleaved shared memory (leaf kernel): time + one 16-bit
+// word with the 4-bit block-local ids a, b, c (blocks of <= 16 points) and
+// the kind -- half the bytes of a 32-bit word, so more CTAs fit an SM
 struct LEvIn {
   static constexpr bool kPrefetch = false;  // shared memory: read when consumed
   const double *t;
-  const unsigned *w;
+  const unsigned short *w;
   __device__ __forceinline__ Ev get(int i) const {
     Ev e;
     e.t = t[i * 32];
     const unsigned x = w[i * 32];
-    e.a = x & 0xff;
-    e.b = (x >> 8) & 0xff;
-    e.c = (x >> 16) & 0xff;
-    e.kind = x >> 24;
+    e.a = x & 0xf;
+    e.b = (x >> 4) & 0xf;
+    e.c = (x >> 8) & 0xf;
+    e.kind = x >> 12;
     return e;
   }
 };
 struct LEvOut {
   double *t;
-  unsigned *w;
+  unsigned short *w;
   __device__ __forceinline__ void put(long long k, const Ev &o) const {
     t[k * 32] = o.t;
-    w[k * 32] = static_cast<unsigned>(o.a) | (static_cast<unsigned>(o.b) << 8) |
-                (static_cast<unsigned>(o.c) << 16) | (static_cast<unsigned>(o.kind) << 24);
+    w[k * 32] = static_cast<unsigned short>(o.a | (o.b << 4) | (o.c << 8) | (o.kind << 12));
   }
 };
 
@@ -735,10 +735,10 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
 // Nothing touches HBM between levels; groups stay uncompacted inside the
 // block (a hidden point is never referenced again), and the level-B group
 // is compacted and written in the compact-group format the per-level
-// kernels read.  Per lane: 32 B per point + 2 x 2 x 12 B event slots.
+// kernels read.  Per lane: 32 B per point + 2 x 2 x 10 B event slots.
 template <int B>
 __host__ __device__ constexpr int leaf_lane_bytes() {
-  return (1 << B) * (24 + 4 + 4) + 2 * (2 << B) * 12 + ((1 << B) / 2) * 4;
+  return (1 << B) * (24 + 4 + 4) + 2 * (2 << B) * 10 + ((1 << B) / 2) * 4;
 }
 
 template <int B>
@@ -764,8 +764,8 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   double *ET1 = ET0 + 32 * 2 * NP;
   short2 *LK = reinterpret_cast<short2 *>(reinterpret_cast<double *>(smem) + 32 * 7 * NP) + lane;
   unsigned *FI = reinterpret_cast<unsigned *>(LK - lane + 32 * NP) + lane;
-  unsigned *EW0 = FI + 32 * NP;
-  unsigned *EW1 = EW0 + 32 * 2 * NP;
+  unsigned short *EW0 = reinterpret_cast<unsigned short *>(FI - lane + 32 * NP) + lane;
+  unsigned short *EW1 = EW0 + 32 * 2 * NP;
   int *KG = reinterpret_cast<int *>(EW1 - lane + 32 * 2 * NP);
   for (int p = 0; p < NP; ++p) {
     double x = 0.0, y = 0.0, z = 0.0;
@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   int u0 = 0, v0 = 0;
   long long kfin = 0;
   double *ETi = ET0, *ETo = ET1;
-  unsigned *EWi = EW0, *EWo = EW1;
+  unsigned short *EWi = EW0, *EWo = EW1;
 #pragma unroll 1
   for (int lv = 2; lv <= B; ++lv) {
     const int size = 1 << lv, half = size >> 1;
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
       kfin = KG[g * 32 + lane];
     }
     double *tt = ETi; ETi = ETo; ETo = tt;
-    unsigned *tw = EWi; EWi = EWo; EWo = tw;
+    unsigned short *tw = EWi; EWi = EWo; EWo = tw;
     __syncwarp();
   }
   // ---- level-B group: compact (kept = merged -inf chain U logged points)
@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
       FI[p * 32] = 1u;
       p = LK[p * 32].y;
     }
-    for (int e = 0; e < kfin; ++e) FI[((EWi[e * 32] >> 8) & 0xff) * 32] = 1u;
+    for (int e = 0; e < kfin; ++e) FI[((EWi[e * 32] >> 4) & 0xf) * 32] = 1u;
   }
   int m = 0;
   for (int p = 0; p < cnt; ++p) {
@@ -893,13 +893,13 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
     const unsigned w = EWi[e * 32];
     Ev o;
     o.t = ETi[e * 32];
-    const unsigned na = FI[(w & 0xff) * 32], nb = FI[((w >> 8) & 0xff) * 32],
-                   nc = FI[((w >> 16) & 0xff) * 32];
+    const unsigned na = FI[(w & 0xf) * 32], nb = FI[((w >> 4) & 0xf) * 32],
+                   nc = FI[((w >> 8) & 0xf) * 32];
     bad |= (na == FULL) | (nb == FULL) | (nc == FULL);
     o.a = static_cast<int>(na);
     o.b = static_cast<int>(nb);
     o.c = static_cast<int>(nc);
-    o.kind = static_cast<int>(w >> 24);
+    o.kind = static_cast<int>(w >> 12);
     evo[e] = o;
   }
   out.hdr[blk] = make_int2(m, static_cast<int>(kfin));
