@@ -90,10 +90,18 @@ struct TpjSlice {
   // memory instead of rotating a register copy: a win in the leaf kernel
   // (117 vs 140 registers, -9 %), not in the lane-per-job one (measured)
   static constexpr bool kReload = XYZ && STRIDE == 32;
+  // first-event info word: 32 bits with 15-bit ids (lane kernel), 16 bits
+  // with 7-bit ids in the leaf's lane-interleaved blocks (<= 16 points), so
+  // that 12 leaf CTAs fit an SM
+  using FiT = typename std::conditional<STRIDE == 32, unsigned short, unsigned>::type;
+  static constexpr unsigned kFiChain = STRIDE == 32 ? (1u << 15) : FI_CHAIN;
+  static constexpr unsigned kFiEv = STRIDE == 32 ? (1u << 14) : FI_EV;
+  static constexpr int kFiShift = STRIDE == 32 ? 7 : 15;
+  static constexpr unsigned kFiMask = STRIDE == 32 ? 0x7fu : 0x7fffu;
   double *x, *y, *z;
   short2 *lk;
   int *gd;
-  unsigned *fi;
+  FiT *fi;
   __device__ __forceinline__ TpjSlice() {}
   __device__ __forceinline__ TpjSlice(unsigned char *base, int nS) {
     unsigned char *p = base;
@@ -105,10 +113,10 @@ struct TpjSlice {
     }
     lk = reinterpret_cast<short2 *>(p);
     gd = reinterpret_cast<int *>(lk + nS);
-    fi = reinterpret_cast<unsigned *>(gd + nS);
+    fi = reinterpret_cast<FiT *>(gd + nS);
   }
   __device__ __forceinline__ short2 &LK(int p) const { return lk[p * STRIDE]; }
-  __device__ __forceinline__ unsigned &FI(int p) const { return fi[p * STRIDE]; }
+  __device__ __forceinline__ FiT &FI(int p) const { return fi[p * STRIDE]; }
   __device__ __forceinline__ int &GD(int p) const { return gd[p * STRIDE]; }
   __device__ __forceinline__ TpjSlice shifted(int d) const {  // ids relative to point d
     TpjSlice r = *this;
@@ -326,8 +334,9 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
       o.kind = ek;
       out.put(k, o);
       const unsigned f = S.FI(eb);
-      if (!(f & FI_EV))
-        S.FI(eb) = f | FI_EV | static_cast<unsigned>(ea) | (static_cast<unsigned>(ec) << 15);
+      if (!(f & SL::kFiEv))
+        S.FI(eb) = static_cast<typename SL::FiT>(f | SL::kFiEv | static_cast<unsigned>(ea) |
+                                                 (static_cast<unsigned>(ec) << SL::kFiShift));
     }
     k += emit;
     // advance the consumed child stream
@@ -735,10 +744,10 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
 // Nothing touches HBM between levels; groups stay uncompacted inside the
 // block (a hidden point is never referenced again), and the level-B group
 // is compacted and written in the compact-group format the per-level
-// kernels read.  Per lane: 32 B per point + 2 x 2 x 10 B event slots.
+// kernels read.  Per lane: 30 B per point + 2 x 2 x 10 B event slots.
 template <int B>
 __host__ __device__ constexpr int leaf_lane_bytes() {
-  return (1 << B) * (24 + 4 + 4) + 2 * (2 << B) * 10 + ((1 << B) / 2) * 4;
+  return (1 << B) * (24 + 4 + 2) + 2 * (2 << B) * 10 + ((1 << B) / 2) * 4;
 }
 
 template <int B>
@@ -763,7 +772,8 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   double *ET0 = Z + 32 * NP;
   double *ET1 = ET0 + 32 * 2 * NP;
   short2 *LK = reinterpret_cast<short2 *>(reinterpret_cast<double *>(smem) + 32 * 7 * NP) + lane;
-  unsigned *FI = reinterpret_cast<unsigned *>(LK - lane + 32 * NP) + lane;
+  unsigned short *FI = reinterpret_cast<unsigned short *>(LK - lane + 32 * NP) + lane;
+  constexpr unsigned FULL16 = 0xffffu;  // "not kept" in the 16-bit words
   unsigned short *EW0 = reinterpret_cast<unsigned short *>(FI - lane + 32 * NP) + lane;
   unsigned short *EW1 = EW0 + 32 * 2 * NP;
   int *KG = reinterpret_cast<int *>(EW1 - lane + 32 * 2 * NP);
@@ -815,7 +825,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
         for (int p = L; p < R; ++p) {
           const int pr = S.LK(p).x;
           const bool chain = p == L || p == M || (pr != NIL && S.LK(pr).y == p);
-          S.FI(p) = chain ? FI_CHAIN : 0u;
+          S.FI(p) = static_cast<unsigned short>(chain ? S.kFiChain : 0u);
         }
       }
       const long long k = merge_tpj2(
@@ -831,21 +841,21 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
         int last = NIL;
         for (int p = L; p < R; ++p) {
           const unsigned f = S.FI(p);
-          const bool chain = (f & FI_CHAIN) && (p < M ? p <= u0 : p >= v0);
+          const bool chain = (f & S.kFiChain) && (p < M ? p <= u0 : p >= v0);
           if (chain) {
             S.LK(p).x = static_cast<short>(last);
             if (last != NIL) S.LK(last).y = static_cast<short>(p);
             last = p;
-          } else if (f & FI_EV) {
-            S.LK(p) = make_short2(static_cast<short>(f & 0x7fff),
-                                  static_cast<short>((f >> 15) & 0x7fff));
+          } else if (f & S.kFiEv) {
+            S.LK(p) = make_short2(static_cast<short>(f & S.kFiMask),
+                                  static_cast<short>((f >> S.kFiShift) & S.kFiMask));
           } else {
             // hidden from here on: NIL links, so no later chain test can
             // take a stale link for a chain link (the compact kernels drop
             // such points instead)
             S.LK(p) = make_short2(NIL, NIL);
           }
-          if (lv == B) S.FI(p) = (chain || (f & FI_EV)) ? 1u : 0u;  // keep flag
+          if (lv == B) S.FI(p) = (chain || (f & S.kFiEv)) ? 1 : 0;  // keep flag
         }
         if (last != NIL) S.LK(last).y = NIL;
       }
@@ -874,16 +884,20 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   int m = 0;
   for (int p = 0; p < cnt; ++p) {
     const bool keep = FI[p * 32] != 0u;
-    FI[p * 32] = keep ? static_cast<unsigned>(m++) : FULL;
+    FI[p * 32] = static_cast<unsigned short>(keep ? m++ : FULL16);
   }
   bool bad = false;
+  auto new_id = [&](int q) {  // -1: not kept
+    const unsigned v = FI[q * 32];
+    return v == FULL16 ? -1 : static_cast<int>(v);
+  };
   for (int p = 0; p < cnt; ++p) {
     const unsigned id = FI[p * 32];
-    if (id == FULL) continue;
+    if (id == FULL16) continue;
     const short2 l = LK[p * 32];
     int2 o;
-    o.x = l.x == NIL ? NIL : static_cast<int>(FI[l.x * 32]);
-    o.y = l.y == NIL ? NIL : static_cast<int>(FI[l.y * 32]);
+    o.x = l.x == NIL ? NIL : new_id(l.x);
+    o.y = l.y == NIL ? NIL : new_id(l.y);
     bad |= (o.x == -1 && l.x != NIL) | (o.y == -1 && l.y != NIL);
     out.lnk[base + id] = o;
     out.gid[base + id] = static_cast<int>(base + p);
@@ -895,7 +909,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
     o.t = ETi[e * 32];
     const unsigned na = FI[(w & 0xf) * 32], nb = FI[((w >> 4) & 0xf) * 32],
                    nc = FI[((w >> 8) & 0xf) * 32];
-    bad |= (na == FULL) | (nb == FULL) | (nc == FULL);
+    bad |= (na == FULL16) | (nb == FULL16) | (nc == FULL16);
     o.a = static_cast<int>(na);
     o.b = static_cast<int>(nb);
     o.c = static_cast<int>(nc);
