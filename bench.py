@@ -48,8 +48,34 @@ CONFIGS = {
     "C3": (2**20, "sphere", 0, "2^20 sphere surface (h~n)"),
     "C4": (2**24, "cube", 0, "2^24 uniform cube [-1,1]^3"),
     "C5": (2**27, "mixed", 0, "2^27 ball + 2^20 radius-2 shell"),
+    # BASELINE.md "Integer" row: integer coordinates in [-2^30, 2^30) (tie path)
+    "INT": (2**20, "int31", 0, "2^20 integer cloud, coordinates in [-2^30, 2^30)"),
 }
-STATS_KEY = {"C2": "C2_ball_2^20", "C3": "C3_sphere_2^20", "C4": "C4_cube_2^24"}
+# full-size CPU runs per config (the reference at C5 takes ~140 s per call on
+# 8 threads: the only config whose CPU legs run a bounded sample)
+CPU_FULL_MAX = 2**24
+
+
+def make_points(cfg: str) -> np.ndarray:
+    from paper_1205_1171_b200.generators import generate, integer_cloud
+
+    n, dist, seed, _ = CONFIGS[cfg]
+    if dist == "int31":
+        return integer_cloud(n, seed)
+    return generate(n, dist, seed)
+
+
+def sample_points(cfg: str, sn: int) -> np.ndarray:
+    from paper_1205_1171_b200.generators import generate, integer_cloud
+
+    n, dist, seed, _ = CONFIGS[cfg]
+    if sn >= n:
+        return make_points(cfg)
+    if dist == "int31":
+        return integer_cloud(sn, seed)
+    return generate(sn, dist, seed)
+STATS_KEY = {"C2": "C2_ball_2^20", "C3": "C3_sphere_2^20", "C4": "C4_cube_2^24",
+             "INT": "int_2^20_R2^31"}
 
 
 def parse():
@@ -61,7 +87,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--engine", default="fast", choices=["fast", "exact"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-n", type=int, default=2**20)
+    ap.add_argument("--cpu-sample-n", type=int, default=CPU_FULL_MAX,
+                    help="largest cloud the CPU legs run (configs above it use a sample)")
     return ap.parse_args()
 
 
@@ -147,12 +174,19 @@ def reference_module():
     return ref
 
 
-def time_reference(n: int, dist: str, seed: int, reps: int, warm: int = 1):
-    """Reference convex_hull_3d with ThreadBackend(all cores): list of seconds."""
-    from paper_1205_1171_b200.generators import generate
-
+def time_reference(pts: np.ndarray, reps: int, warm: int = 1, serial: bool = False):
+    """Reference convex_hull_3d on ``pts``: ThreadBackend(all host cores), or
+    the 1-core top-down ``solver="serial"``.  Returns (seconds list, cores)."""
     ref = reference_module()
-    pts = generate(n, dist, seed)
+    if serial:
+        out = []
+        for i in range(warm + reps):
+            t0 = time.perf_counter()
+            ref.convex_hull_3d(pts, solver="serial")
+            dt = time.perf_counter() - t0
+            if i >= warm:
+                out.append(dt)
+        return out, 1
     cores = os.cpu_count() or 1
     out = []
     with ref.ThreadBackend(cores) as be:
@@ -166,35 +200,54 @@ def time_reference(n: int, dist: str, seed: int, reps: int, warm: int = 1):
 
 
 def cpu_baseline(cfg: str, sample_n: int) -> dict:
+    """The unmodified reference on this host (rank 0, N=1 only): the whole
+    config cloud (up to ``sample_n`` points), one timed call of the leveled
+    solver on every host core and one of the 1-core serial solver (the two
+    CPU numbers BASELINE.md 2 asks for), no warm-up (a call is seconds long)."""
     n, dist, seed, _ = CONFIGS[cfg]
     sn = min(n, sample_n)
-    secs, cores = time_reference(sn, dist, seed, reps=3, warm=1)
-    med = statistics.median(secs)
-    return {"value": sn / med, "unit": "points/s", "cores": cores, "kind": "reference",
-            "sample": f"reference convex_hull_3d(ThreadBackend({cores})) on generate({sn}, "
-                      f"'{dist}', {seed}) (bounded sample of {cfg}), median of {len(secs)} "
-                      f"after 1 warm-up; host CPU {cpu_model()}"}
+    pts = sample_points(cfg, sn)
+    what = "the full config cloud" if sn == n else f"a bounded sample of {cfg}"
+    secs, cores = time_reference(pts, reps=1, warm=0)
+    ser, _ = time_reference(pts, reps=1, warm=0, serial=True)
+    return {"value": sn / secs[0], "unit": "points/s", "cores": cores, "kind": "reference",
+            "sample": f"reference convex_hull_3d(ThreadBackend({cores})) on {sn} points "
+                      f"({what}: {cfg} n={n}, dist {dist!r}, seed {seed}), 1 timed call, "
+                      f"no warm-up; host CPU {cpu_model()}",
+            "seconds": secs[0],
+            "serial_1core": {"value": sn / ser[0], "unit": "points/s", "cores": 1,
+                             "seconds": ser[0],
+                             "sample": f"reference convex_hull_3d(solver='serial') on the "
+                                       f"same {sn} points, 1 timed call"}}
 
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation (unmodified, oracle/_ref) on
+    this host: ThreadBackend over all host cores, every step one full
+    convex_hull_3d of the config cloud (C5, 2^27, runs a 2^24 sample).
+    Rank 0 only; other ranks exit without work."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     n, dist, seed, label = CONFIGS[args.config]
-    sn = min(n, max(args.cpu_sample_n, 1 << 22)) if args.config in ("C4", "C5") else n
-    secs, cores = time_reference(sn, dist, seed, reps=args.steps, warm=args.warmup)
+    sn = min(n, args.cpu_sample_n)
+    pts = sample_points(args.config, sn)
+    secs, cores = time_reference(pts, reps=args.steps, warm=args.warmup)
     total = sum(secs)
     value = sn * len(secs) / total
+    cfg = {"workload": f"{args.config}: {label}", "n": n, "distribution": dist, "seed": seed}
+    if sn != n:
+        cfg["sample_n"] = sn
+    what = "the full config cloud" if sn == n else f"a {sn}-point sample"
     line = {
         "impl": "reference", "metric": "3D hull points/sec", "value": value, "unit": "points/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total / len(secs) * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, PCG64)",
-        "config": {"workload": f"{args.config}: {label}", "n": n, "sample_n": sn,
-                   "distribution": dist, "seed": seed},
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "reference",
-                         "sample": f"generate({sn}, '{dist}', {seed}) per step; host CPU "
-                                   f"{cpu_model()}"},
+                         "sample": f"{what} per step ({args.steps} timed after {args.warmup} "
+                                   f"warm-up); host CPU {cpu_model()}"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -254,12 +307,16 @@ NCU_NAMES = {
 def measured_traffic(cfg: str, name: str):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
     of the kernel, from the committed ncu launch list of this config
-    (profiles/r1_ncu_launches_<cfg>.json, made by tools/profile_round.sh +
+    (profiles/r<round>_ncu_launches_<cfg>.json, the latest round's, made by tools/profile_round.sh +
     tools/ncu_summary.py).  A big-level "launch" is the pipeline's kernels of
     one level; it is counted per level."""
-    p = os.path.join(ROOT, "profiles", f"r1_ncu_launches_{cfg.lower()}.json")
-    if not os.path.exists(p):
+    import glob
+
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_launches_{cfg.lower()}.json")),
+                   key=lambda q: int(os.path.basename(q)[1:].split("_", 1)[0]))
+    if not cands:
         return None, None
+    p = cands[-1]  # the latest round's launch list
     doc = json.load(open(p))
     pre = NCU_NAMES.get(name, (name,))
     ks = [k for k in doc["kernels"] if k["kernel"].startswith(pre)]
@@ -279,7 +336,6 @@ def run_ours(args):
 
     import paper_1205_1171_b200 as H
     from paper_1205_1171_b200 import engine as E
-    from paper_1205_1171_b200.generators import generate
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -287,10 +343,12 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n, dist, seed, label = CONFIGS[args.config]
-    pts_host = generate(n, dist, seed)
+    pts_host = make_points(args.config)
     pinned = torch.from_numpy(pts_host).pin_memory()
     pts_dev = pinned.to(dev)
     be = H.CudaBackend(local, engine=args.engine)
+    from paper_1205_1171_b200 import fast as F
+    fb0 = F.FALLBACKS[0]
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(max(args.warmup, 3)):
@@ -302,6 +360,8 @@ def run_ours(args):
     # device-resident timed region (+ per-launch kernel events)
     prof: list = []
     E.PROFILE = prof
+    E.PROFILE_DEFER = True
+    F.profile_collect(1 << 20)  # drop the warm-up's records
     l0 = E.launch_count()
     clocks = ClockSampler(local)
     clocks.start()
@@ -314,10 +374,20 @@ def run_ours(args):
     ev1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
+    for tag, p_idx, t_ms in F.profile_collect(1 << 20):
+        name, lv = F.kernel_of(tag)
+        prof.append((name, p_idx, lv, t_ms))
     E.PROFILE = None
+    E.PROFILE_DEFER = False
     launches = (E.launch_count() - l0) // args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     value = n / (ms / 1e3)
+    fallbacks = F.FALLBACKS[0] - fb0
+    # which kernels ran, per step (route evidence: fused fast path vs exact)
+    routes: dict = {}
+    for name, _p, _lv, _t in prof:
+        routes[name] = routes.get(name, 0) + 1
+    routes = {k: v / args.steps for k, v in sorted(routes.items())}
 
     # roofline of the dominant kernel
     per_kernel: dict = {}
@@ -385,7 +455,7 @@ def run_ours(args):
                    "l2": "input 24n bytes > 126 MB L2 (C4/C5); no explicit flush",
                    "faces": nfaces, "vertices": nverts},
         "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
-        "clocks": clk,
+        "clocks": clk, "fallbacks": fallbacks, "routes_per_step": routes,
     }
     print(json.dumps(line), flush=True)
 
@@ -398,7 +468,6 @@ def run_ours_distributed(args):
     import torch.distributed as dist
 
     from paper_1205_1171_b200 import engine as E
-    from paper_1205_1171_b200.generators import generate
     from paper_1205_1171_b200.multigpu import SlabPlan, convex_hull_3d_distributed
 
     ws, rank, local = dist_env()
@@ -413,7 +482,7 @@ def run_ours_distributed(args):
     else:
         dist.init_process_group("nccl", device_id=dev)
     n, dist_name, seed, label = CONFIGS[args.config]
-    pts_host = generate(n, dist_name, seed)
+    pts_host = make_points(args.config)
     pinned = torch.from_numpy(pts_host).pin_memory()
     pts_dev = pinned.to(dev)
     stream = torch.cuda.current_stream(dev)

@@ -61,9 +61,11 @@ const char *h3d_impl(void);
 const char *h3d_last_error(void);
 /* number of this library's own kernel launches so far (process-wide) */
 int64_t h3d_launch_count(void);
-/* per-level profile: when enabled, every merge level of h3d_fast_pass is
- * bracketed by CUDA events on its stream; collect returns (level, pass,
- * milliseconds) rows, synchronising on the recorded events, and clears them */
+/* per-level profile of the CALLING THREAD: when enabled (per thread), every
+ * merge level of h3d_fast_passes* run by this thread is bracketed by CUDA
+ * events on its stream (events pooled per device); collect returns this
+ * thread's (level, pass, milliseconds) rows, waiting only for its own last
+ * event, and clears them */
 void h3d_profile_enable(int32_t on);
 int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms,
                             int64_t max);

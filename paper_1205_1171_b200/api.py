@@ -10,6 +10,7 @@ CUDA device or the built library this raises.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -180,50 +181,71 @@ def _to_device(points, dev: torch.device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(coords)).to(dev)
 
 
-def _run_passes(sorted_pts, engine, solver, level_lists):
+def _level_rows_to_stats(rows, n, level_lists):
+    """Profile rows -> per-level seconds per pass (F12) and the two passes'
+    shares of the kernel time."""
+    from . import engine as E
+    from . import fast
+
+    ms = [0.0, 0.0]
+    nlev = level_count(n)
+    per = [[0.0] * nlev, [0.0] * nlev]
+    for lv, p, t in rows:
+        name, lv = fast.kernel_of(lv)
+        # pass 2 = one launch covering both passes: split evenly
+        shares = ((0, t / 2), (1, t / 2)) if p == 2 else ((p, t),)
+        for pp, tt in shares:
+            ms[pp] += tt
+            # a negative level is a fused kernel (levels 1..|lv|); its time
+            # is reported at its last level, 0.0 below it
+            per[pp][abs(lv) - 1] += tt / 1e3
+        if E.PROFILE is not None:
+            E.PROFILE.append((name, p, lv, t))
+    if level_lists is not None:
+        level_lists[0].extend(per[0])
+        level_lists[1].extend(per[1])
+    return ms
+
+
+def _run_passes(sorted_pts, engine, solver, level_lists, profile: bool):
     """Both passes; returns (raw faces int32 (F,3) on device, lower count,
-    upper count, lower ms, upper ms).  Per-level times are device events
-    (seconds, like the reference's perf_counter deltas)."""
+    upper count, lower ms, upper ms, finish).  With ``profile`` every level is
+    bracketed by device events (no synchronisation here): ``finish()`` --
+    called by the API after its one host synchronisation, so it never waits
+    -- turns them into per-level seconds (like the reference's perf_counter
+    deltas) and the two passes' shares of the time."""
     from . import engine as E
     from . import fast
 
     want_levels = solver == "parallel"
     if engine == "fast":
         t0 = time.perf_counter()
-        profiling = want_levels or E.PROFILE is not None
-        if profiling:
+        if profile:
             fast.profile_enable(True)
         try:
             res = fast.run_both(sorted_pts)
         finally:
-            if profiling:
+            if profile:
                 fast.profile_enable(False)
-        rows = fast.profile_collect() if profiling else []
         if res is not None:
             dt = (time.perf_counter() - t0) * 1e3
             raw, k_lo, k_up = res
-            ms = [0.0, 0.0]
-            nlev = level_count(sorted_pts.shape[0])
-            per = [[0.0] * nlev, [0.0] * nlev]
-            for lv, p, t in rows:
-                name, lv = fast.kernel_of(lv)
-                # pass 2 = one launch covering both passes: split evenly
-                shares = ((0, t / 2), (1, t / 2)) if p == 2 else ((p, t),)
-                for pp, tt in shares:
-                    ms[pp] += tt
-                    # a negative level is a fused kernel (levels 1..|lv|); its
-                    # time is reported at its last level, 0.0 below it
-                    per[pp][abs(lv) - 1] += tt / 1e3
-                if E.PROFILE is not None:
-                    E.PROFILE.append((name, p, lv, t))
-            if want_levels:
-                level_lists[0].extend(per[0])
-                level_lists[1].extend(per[1])
-            tot = ms[0] + ms[1]
-            lo_ms = dt * ms[0] / tot if tot > 0 else dt / 2
-            return raw, k_lo, k_up, lo_ms, dt - lo_ms
-        for lst in level_lists:
-            lst.clear()
+            split = [dt / 2, dt / 2]
+
+            def finish():
+                if not profile or E.PROFILE_DEFER:
+                    # deferred: the records stay with this thread until the
+                    # caller (bench.py) collects a whole timed loop at once
+                    return split
+                ms = _level_rows_to_stats(fast.profile_collect(), sorted_pts.shape[0],
+                                          level_lists if want_levels else None)
+                tot = ms[0] + ms[1]
+                lo = dt * ms[0] / tot if tot > 0 else dt / 2
+                return [lo, dt - lo]
+
+            return raw, k_lo, k_up, finish
+        if profile:
+            fast.profile_collect()  # drop the declined run's records
     out = []
     ms = []
     for which, zsign in ((0, 1.0), (1, -1.0)):
@@ -233,7 +255,13 @@ def _run_passes(sorted_pts, engine, solver, level_lists):
         torch.cuda.current_stream(sorted_pts.device).synchronize()
         ms.append((time.perf_counter() - t0) * 1e3)
         out.append(raw)
-    return torch.cat(out), out[0].shape[0], out[1].shape[0], ms[0], ms[1]
+    return torch.cat(out), out[0].shape[0], out[1].shape[0], (lambda: ms)
+
+
+# per-level device timing for device-resident results (return_device=True):
+# off unless asked for -- it would need a synchronisation the caller did not
+# request; host results get it for free after their one synchronisation
+LEVEL_TIMES_ON_DEVICE = os.environ.get("H3D_LEVEL_TIMES", "0") not in ("", "0")
 
 
 def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
@@ -274,19 +302,25 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
         return HullResult(vertices=verts, faces=faces, stats=stats)
 
     # the per-device workspaces are shared: one hull at a time per device
-    # (calls from several threads are serialised, not interleaved)
-    with _device_lock(dev):
+    # (calls from several threads are serialised, not interleaved); every
+    # launch goes to `dev` whatever the caller's current device is
+    from . import engine as E
+
+    profile = (solver == "parallel" and (not return_device or LEVEL_TIMES_ON_DEVICE)) \
+        or E.PROFILE is not None
+    with _device_lock(dev), torch.cuda.device(dev):
         sort_t0 = time.perf_counter()
         sorted_pts, order, perturbed = presort(pts)
         sort_ms = (time.perf_counter() - sort_t0) * 1e3
 
         lower_levels: list[float] = []
         upper_levels: list[float] = []
-        raw, k_lo, k_up, lo_ms, up_ms = _run_passes(sorted_pts, engine, solver,
-                                                    (lower_levels, upper_levels))
+        raw, k_lo, k_up, finish = _run_passes(sorted_pts, engine, solver,
+                                              (lower_levels, upper_levels), profile)
         verts, faces = orient_remap(sorted_pts, order, raw)
-    if not return_device:
-        verts, faces = to_host(verts), to_host(faces)
+        if not return_device:
+            verts, faces = to_host(verts), to_host(faces)
+        lo_ms, up_ms = finish()
     total_ms = (time.perf_counter() - total_t0) * 1e3
     stats = HullStats(n=n, levels=level_count(n), lower_events=int(k_lo),
                       upper_events=int(k_up), sort_ms=sort_ms, lower_ms=lo_ms,

@@ -22,61 +22,78 @@ extern "C" const char *h3d_last_error(void) { return g_last_error; }
 extern "C" int64_t h3d_launch_count(void) { return g_launches.load(); }
 
 // ------------------------------------------------------------ level profile
+// Per-level CUDA-event profile.  The records and the on/off switch belong to
+// the calling THREAD (a hull runs on its caller's thread; two threads driving
+// two devices never see each other's records), and recycled events are pooled
+// per DEVICE (an event may only be recorded on a stream of its own device).
+#include <map>
 #include <mutex>
 #include <vector>
 
 namespace {
 struct ProfRec {
-  int level, pass;
+  int level, pass, device;
   cudaEvent_t e0, e1;
 };
-std::mutex g_prof_mu;
-bool g_prof_on = false;
-std::vector<ProfRec> g_prof;
-std::vector<cudaEvent_t> g_ev_free;  // recycled events (creation is not free)
+thread_local bool t_prof_on = false;
+thread_local std::vector<ProfRec> t_prof;
+thread_local int t_prof_dev = -1;  // device of the pending begin event
+std::mutex g_pool_mu;
+std::map<int, std::vector<cudaEvent_t>> g_ev_free;  // per device
 
-cudaEvent_t ev_get() {
+cudaEvent_t ev_get(int dev) {
   {
-    std::lock_guard<std::mutex> g(g_prof_mu);
-    if (!g_ev_free.empty()) {
-      cudaEvent_t e = g_ev_free.back();
-      g_ev_free.pop_back();
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    auto &v = g_ev_free[dev];
+    if (!v.empty()) {
+      cudaEvent_t e = v.back();
+      v.pop_back();
       return e;
     }
   }
   cudaEvent_t e;
   return cudaEventCreate(&e) == cudaSuccess ? e : nullptr;
 }
+
+void ev_put(int dev, cudaEvent_t e) {
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  g_ev_free[dev].push_back(e);
+}
 }  // namespace
 
-bool h3d_profiling() { return g_prof_on; }
+bool h3d_profiling() { return t_prof_on; }
 
 void *h3d_prof_begin(cudaStream_t s) {
-  cudaEvent_t e = ev_get();
-  if (e) cudaEventRecord(e, s);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  cudaEvent_t e = ev_get(dev);
+  if (e) {
+    cudaEventRecord(e, s);
+    t_prof_dev = dev;
+  }
   return e;
 }
 
 void h3d_prof_end(void *e0, int level, int pass, cudaStream_t s) {
   if (!e0) return;
-  cudaEvent_t e1 = ev_get();
-  if (!e1) return;
+  const int dev = t_prof_dev;
+  cudaEvent_t e1 = ev_get(dev);
+  if (!e1) {
+    ev_put(dev, static_cast<cudaEvent_t>(e0));
+    return;
+  }
   cudaEventRecord(e1, s);
-  std::lock_guard<std::mutex> g(g_prof_mu);
-  g_prof.push_back({level, pass, static_cast<cudaEvent_t>(e0), e1});
+  t_prof.push_back({level, pass, dev, static_cast<cudaEvent_t>(e0), e1});
 }
 
-extern "C" void h3d_profile_enable(int32_t on) {
-  std::lock_guard<std::mutex> g(g_prof_mu);
-  g_prof_on = on != 0;
-}
+extern "C" void h3d_profile_enable(int32_t on) { t_prof_on = on != 0; }
 
 extern "C" int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms, int64_t max) {
-  std::lock_guard<std::mutex> g(g_prof_mu);
   int64_t m = 0;
-  // every record is on one stream: waiting for the last end event covers all
-  if (!g_prof.empty()) cudaEventSynchronize(g_prof.back().e1);
-  for (auto &r : g_prof) {
+  // the caller's records are stream-ordered on its own stream: waiting for
+  // its last end event covers all of them (nothing else is synchronised)
+  if (!t_prof.empty()) cudaEventSynchronize(t_prof.back().e1);
+  for (auto &r : t_prof) {
     if (m < max) {
       float t = 0.f;
       cudaEventElapsedTime(&t, r.e0, r.e1);
@@ -85,9 +102,9 @@ extern "C" int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms,
       ms[m] = t;
       ++m;
     }
-    g_ev_free.push_back(r.e0);
-    g_ev_free.push_back(r.e1);
+    ev_put(r.device, r.e0);
+    ev_put(r.device, r.e1);
   }
-  g_prof.clear();
+  t_prof.clear();
   return m;
 }

@@ -29,6 +29,10 @@ NIL = -1
 # bench.py instrumentation: when a list, every merge-level launch appends
 # (kernel name, pass index, level, device milliseconds)
 PROFILE: list | None = None
+# bench.py: leave the fast path's per-level device events with the calling
+# thread instead of collecting them per call (one collection per timed loop,
+# no per-call synchronisation inside the timed region)
+PROFILE_DEFER = False
 
 
 def level_count(n: int) -> int:

@@ -3,8 +3,9 @@
 The final logs equal the reference's (tests/test_gpu_fast.py checks every
 level's log against the reference's per-level buffers).  If the device
 reports that the fast path cannot reproduce the reference semantics for an
-input (degenerate inputs: a stored event time disagreeing with the links in
-verify mode, a compact-capacity overflow, a dangling link), or any merge
+input (degenerate inputs: an exact tie between event times, a child event
+whose stored facet or kind disagrees with the current links, a
+compact-capacity overflow, a dangling link), or any merge
 error, the pass is rerun on the exact seam engine, which reproduces the
 reference's behaviour (and its exceptions) step for step.
 """
@@ -17,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .engine import level_count, run_pass_exact, stream_ptr
+from .engine import stream_ptr
 
 E_FASTPATH = -13
 
@@ -102,7 +103,7 @@ def profile_collect(max_rows: int = 4096):
     return [(int(lv[i]), int(ps[i]), float(ms[i])) for i in range(m)]
 
 
-def run_both(sorted_pts: torch.Tensor, verify: bool = False):
+def run_both(sorted_pts: torch.Tensor):
     """Both passes + facet extraction.  Returns (raw faces int32 (F,3) on
     device, lower count, upper count) or None when the exact engine must
     take over."""
@@ -118,7 +119,7 @@ def run_both(sorted_pts: torch.Tensor, verify: bool = False):
     counts = state[1:3]
     fin = (ctypes.c_int64 * 2)()
     r = L.h3d_fast_passes(sorted_pts.data_ptr(), n, ws_lo.data_ptr(), ws_up.data_ptr(), wsb,
-                          err.data_ptr(), 1 if verify else 0, ctypes.addressof(fin), s)
+                          err.data_ptr(), 0, ctypes.addressof(fin), s)
     if r < 0:
         from .errors import check_merge
 
@@ -139,15 +140,6 @@ def run_both(sorted_pts: torch.Tensor, verify: bool = False):
         return None
     k_lo, k_up = int(h[1]), int(h[2])
     return faces[: k_lo + k_up], k_lo, k_up
-
-
-def run_pass(pts, zsign, level_times=None):
-    """Single pass on the exact engine (kept for API symmetry)."""
-    return run_pass_exact(pts, zsign, level_times)
-
-
-def levels_of(n: int) -> int:
-    return level_count(n)
 
 
 __all__ = ["run_both", "profile_enable", "profile_collect", "E_FASTPATH", "ctypes"]

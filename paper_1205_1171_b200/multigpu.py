@@ -417,15 +417,23 @@ def convex_hull_3d_distributed(points, device=None, return_device: bool = False)
     n = pts.shape[0]
     if world == 1 or n <= 3 or SlabPlan(n, world).G == 1:
         return convex_hull_3d(pts, return_device=return_device) if rank == 0 else None
-    res = hull_distributed(pts, rank, world)
+    from .api import _device_lock
+
+    # the per-device workspaces (presort, both passes) are shared with
+    # convex_hull_3d: hold the device's lock while they are in use, and
+    # launch on `dev` whatever the caller's current device is
+    with _device_lock(dev), torch.cuda.device(dev):
+        res = hull_distributed(pts, rank, world)
+        if rank == 0 and res is not None:
+            raw, k_lo, k_up, sorted_pts, order, perturbed, sharded = res
+            # sharded presort: rank 0 holds only the rows its merges touched,
+            # so the centroid is taken over the caller-order input (same
+            # points)
+            verts, faces = orient_remap(sorted_pts, order, raw, pts if sharded else None)
     if rank != 0:
         return None
-    if res is None:  # exact engine, single GPU, reference semantics
+    if res is None:  # exact engine, single GPU, reference semantics (takes the lock itself)
         return convex_hull_3d(pts, _exact_backend(dev), return_device=return_device)
-    raw, k_lo, k_up, sorted_pts, order, perturbed, sharded = res
-    # sharded presort: rank 0 holds only the rows its merges touched, so the
-    # centroid is taken over the caller-order input (same points)
-    verts, faces = orient_remap(sorted_pts, order, raw, pts if sharded else None)
     total_ms = (time.perf_counter() - t0) * 1e3
     stats = HullStats(n=n, levels=level_count(n), lower_events=k_lo, upper_events=k_up,
                       sort_ms=0.0, lower_ms=0.0, upper_ms=0.0, total_ms=total_ms,

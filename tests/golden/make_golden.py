@@ -184,7 +184,7 @@ def make_large(ref, with_c4: bool, only_c5: bool = False):
             "ref_seconds_threads": round(dt, 3), "ref_threads": os.cpu_count(),
         }
         print(name, large[name])
-        if not name.startswith(("int", "C5")):
+        if not name.startswith("C5"):
             sp, _, _ = O.sort_and_perturb(pts)
             up = sp.copy()
             up[:, 2] = -up[:, 2]

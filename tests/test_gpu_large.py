@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import paper_1205_1171_b200 as H
+from paper_1205_1171_b200 import fast
 from paper_1205_1171_b200.generators import generate, integer_cloud
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -32,7 +33,10 @@ def test_large_config_matches_reference_digest(name, large_json):
     exp = large_json[name]
     pts = GEN[name]()
     assert sha(pts) == exp["points_sha256"]
+    fb = fast.FALLBACKS[0]
     r = H.convex_hull_3d(pts)
+    # the fused fast path produced it (no exact-engine rerun)
+    assert fast.FALLBACKS[0] == fb, f"fast path declined the input (err {fast.LAST_ERROR[0]})"
     assert len(r.faces) == exp["nfaces"] and len(r.vertices) == exp["nvertices"]
     assert (r.stats.lower_events, r.stats.upper_events) == (exp["lower_events"], exp["upper_events"])
     assert r.stats.perturbed == exp["perturbed"]
