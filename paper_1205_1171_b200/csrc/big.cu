@@ -259,6 +259,8 @@ __global__ void k_big_jobs(Pass2 P, long long n, int lv, long long j0, long long
       kin = hl.y + hr.y;
       ns = hl.x + hr.x;
       flag = 1;
+      // stored events carry 21-bit local ids (fast.cuh kEvIdBits)
+      if (ns >= kEvIdMax) raise_err(err, E_FASTPATH);
     } else if (L < n) {  // carry (copy_log, parallel.py:107-108)
       for (int p = 0; p < hl.x; ++p) {
         out.lnk[L + p] = in.lnk[L + p];
@@ -277,7 +279,6 @@ __global__ void k_big_jobs(Pass2 P, long long n, int lv, long long j0, long long
     W.jns[J2] = 0;
     W.jseg[J2] = 0;
   }
-  (void)err;
 }
 
 // segments per job for the level's segment length
@@ -306,7 +307,7 @@ __global__ void k_big_seq(Pass2 P, long long n, int lv, long long j0, long long 
     const JobRef r = job_ref(P, jb, J, j0, lv, n);
     const int d = g - W.jkinoff[jb];
     const int kL = r.kL, kR = W.jkin[jb] - kL;
-    const Ev *evL = r.in.ev + 2 * r.L, *evR = r.in.ev + 2 * r.M;
+    const EvP *evL = r.in.ev + 2 * r.L, *evR = r.in.ev + 2 * r.M;
     int lo = d - kR > 0 ? d - kR : 0, hi = d < kL ? d : kL;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;

@@ -146,15 +146,15 @@ struct TpjSlice {
   }
 };
 
-// event streams of the sweep: HBM (24-byte Ev) ...
+// event streams of the sweep: HBM (16-byte EvP) ...
 struct GEvIn {
   static constexpr bool kPrefetch = true;  // HBM: one event of prefetch
-  const Ev *__restrict__ p;
+  const EvP *__restrict__ p;
   __device__ __forceinline__ Ev get(int i) const { return p[i]; }
 };
 struct GEvOut {
-  Ev *__restrict__ p;
-  __device__ __forceinline__ void put(long long k, const Ev &o) const { p[k] = o; }
+  EvP *__restrict__ p;
+  __device__ __forceinline__ void put(long long k, const Ev &o) const { p[k] = EvP(o); }
 };
 // ... or lane-interleaved shared memory (leaf kernel): time + one 16-bit
 // word with the 4-bit block-local ids a, b, c (blocks of <= 16 points) and
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
     int jj = 0;
     for (int x0 = 0; x0 < tot_ev; x0 += 4 * 32) {
       int jq[4];
-      Ev *ptr[4];
+      EvP *ptr[4];
       Ev o[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
         o[q].a = static_cast<int>(na);
         o[q].b = static_cast<int>(nb);
         o[q].c = static_cast<int>(nc);
-        *ptr[q] = o[q];
+        *ptr[q] = EvP(o[q]);
       }
     }
   }
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
     out.lnk[base + id] = o;
     out.gid[base + id] = static_cast<int>(base + p);
   }
-  Ev *evo = out.ev + 2 * base;
+  EvP *evo = out.ev + 2 * base;
   for (int e = 0; e < kfin; ++e) {
     const unsigned w = EWi[e * 32];
     Ev o;
@@ -914,7 +914,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
     o.b = static_cast<int>(nb);
     o.c = static_cast<int>(nc);
     o.kind = static_cast<int>(w >> 12);
-    evo[e] = o;
+    evo[e] = EvP(o);
   }
   out.hdr[blk] = make_int2(m, static_cast<int>(kfin));
   if (bad) raise_err(err, E_FASTPATH);
@@ -931,7 +931,7 @@ __device__ __forceinline__ void first_event(int *first, int b, int idx) {
 // right child's ids get +nSL and the side is kept in bit 1 of `kind`.  Each
 // lane finds its diagonal split by one binary search, then merges its
 // contiguous slice of the output sequentially.
-__device__ void merge_logs_warp(const Ev *__restrict__ evL, int kL, const Ev *__restrict__ evR,
+__device__ void merge_logs_warp(const EvP *__restrict__ evL, int kL, const EvP *__restrict__ evR,
                                 int kR, int nSL, Ev *seq) {
   const int lane = threadIdx.x & 31;
   const int K = kL + kR;
@@ -978,7 +978,7 @@ __device__ void merge_logs_warp(const Ev *__restrict__ evL, int kL, const Ev *__
 // R[0,nS): records at -inf (left [0,nSL), right [nSL,nS)); seq: merged child
 // events; out: merged events (HBM); first[p]: FIRST_FLAG if p is on its
 // child's -inf chain, low bits = index of p's first merged event.
-__device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, Ev *out,
+__device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, EvP *out,
                                 int *first, long long capRef, long long limitRef, int *pu0,
                                 int *pv0) {
   const int lane = threadIdx.x & 31;
@@ -1044,7 +1044,7 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, Ev *out
         } else {
           Ev o = my;
           o.kind = kind;
-          out[pos] = o;
+          out[pos] = EvP(o);
           first_event(first, my.b, pos);
         }
       }
@@ -1083,7 +1083,7 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, Ev *out
                   o.b = b;
                   o.c = c;
                   o.kind = kind1;
-                  out[k] = o;
+                  out[k] = EvP(o);
                   first_event(first, b, k);
                 }
               }
@@ -1126,7 +1126,7 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, Ev *out
         o.b = b;
         o.c = c;
         o.kind = kind;
-        out[k] = o;
+        out[k] = EvP(o);
         first_event(first, b, k);
       }
     }
@@ -1149,7 +1149,7 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, Ev *out
 // their first event (an insertion: a point off the -inf chain enters the
 // hull once).  These are exactly the links the reference's rewind leaves on
 // every kept point.  evo (the merged events, local ids) is out.ev + 2L.
-__device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R, Ev *evo,
+__device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R, EvP *evo,
                                  int *first, long long L, long long M, int nSL, int nS, int k,
                                  int u0, int v0, long long gidx, long long *err) {
   const int lane = threadIdx.x & 31;
@@ -1169,8 +1169,8 @@ __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R
       if (p == u0) nxt = v0;
       if (p == v0) prv = u0;
     } else if (hasev) {
-      prv = evo[fe].a;
-      nxt = evo[fe].c;
+      prv = evo[fe].a();
+      nxt = evo[fe].c();
     }
     R[p].prev = prv;
     R[p].next = nxt;
@@ -1194,7 +1194,7 @@ __device__ void rebuild_writeout(const GroupBuf &in, const GroupBuf &out, Rec *R
     o.b = first[o.b];
     o.c = first[o.c];
     bad |= (o.a < 0) | (o.b < 0) | (o.c < 0);
-    evo[e] = o;
+    evo[e] = EvP(o);
   }
   // D: links remapped in place
   for (int p = lane; p < nS; p += 32) {
@@ -1285,6 +1285,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, const double 
     }
   }
   const int nS = nSL + nSR, kin = kL + kR;
+  if (merge && nS >= kEvIdMax) {  // stored events carry 21-bit local ids
+    if (lane == 0) raise_err(err, E_FASTPATH);
+    merge = false;
+  }
   const long long need = merge ? warp_job_bytes(nS, kin) : 0;
   const bool global_mode = merge && need > pool;
   bool pending = merge && !global_mode;
@@ -1313,7 +1317,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, const double 
     }
     __syncwarp();
     int u0, v0;
-    Ev *evo = out.ev + 2 * L;
+    EvP *evo = out.ev + 2 * L;
     const long long k = merge_warp(Rr, nSL, seq, kin, evo, first, 2 * (R_ - L), R_ - L, &u0, &v0);
     __syncwarp();
     if (k < 0) {
@@ -1374,7 +1378,7 @@ __global__ void k_fast_extract(GroupBuf lo, GroupBuf up, int *faces, long long c
   for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < F;
        f += (long long)gridDim.x * blockDim.x) {
     const GroupBuf &g = (f < kLo) ? lo : up;
-    const Ev e = g.ev[f < kLo ? f : f - kLo];
+    const Ev e = g.ev[f < kLo ? f : f - kLo];  // unpacked
     faces[3 * f] = g.gid[e.a];
     faces[3 * f + 1] = g.gid[e.b];
     faces[3 * f + 2] = g.gid[e.c];

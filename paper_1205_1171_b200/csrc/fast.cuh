@@ -8,9 +8,10 @@
 //   gid[L .. L+nS)      global sorted index of each kept point: its
 //                       coordinates are read from the sorted point array
 //                       (never copied between levels)
-//   ev[2L .. 2L+k)      Ev: event time t (f64), the facet (a, b, c) of the
-//                       event in group-local ids, and its kind (insertion /
-//                       deletion); b is the reference's log entry
+//   ev[2L .. 2L+k)      EvP (16 B): event time t (f64), the facet (a, b, c)
+//                       of the event in group-local ids (21 bits each) and
+//                       its kind (insertion / deletion); b is the
+//                       reference's log entry
 // A group [L, R) keeps only the points that matter above it: its chain at
 // t = -inf plus every point its log mentions.  Local ids preserve x order, so
 // the reference's x comparisons become integer comparisons (x is strictly
@@ -35,11 +36,50 @@ struct __align__(8) Ev {
 static_assert(sizeof(Rec) == 32, "Rec must be one 32-byte sector");
 static_assert(sizeof(Ev) == 24, "Ev is 24 bytes");
 
+// Group-local ids in the stored events are < 2^21: a merge whose two children
+// keep 2^21 points or more declines (E_FASTPATH, the exact engine takes the
+// hull) -- far above every configured cloud's top groups (<= 1.03M kept).
+constexpr int kEvIdBits = 21;
+constexpr int kEvIdMax = 1 << kEvIdBits;
+
+// An event as stored in the group buffers (HBM): 16 bytes, the time and one
+// word with the facet's three local ids (21 bits each) and the kind (bit 63).
+// Converts to and from the unpacked Ev the kernels compute with.
+struct __align__(16) EvP {
+  double t;
+  unsigned long long w;
+  EvP() = default;
+  __host__ __device__ __forceinline__ EvP(const Ev &e)
+      : t(e.t),
+        w(static_cast<unsigned long long>(static_cast<unsigned>(e.a)) |
+          (static_cast<unsigned long long>(static_cast<unsigned>(e.b)) << kEvIdBits) |
+          (static_cast<unsigned long long>(static_cast<unsigned>(e.c)) << (2 * kEvIdBits)) |
+          (static_cast<unsigned long long>(e.kind & 1) << 63)) {}
+  __host__ __device__ __forceinline__ int a() const { return static_cast<int>(w & (kEvIdMax - 1)); }
+  __host__ __device__ __forceinline__ int b() const {
+    return static_cast<int>((w >> kEvIdBits) & (kEvIdMax - 1));
+  }
+  __host__ __device__ __forceinline__ int c() const {
+    return static_cast<int>((w >> (2 * kEvIdBits)) & (kEvIdMax - 1));
+  }
+  __host__ __device__ __forceinline__ int kind() const { return static_cast<int>(w >> 63); }
+  __host__ __device__ __forceinline__ operator Ev() const {
+    Ev e;
+    e.t = t;
+    e.a = a();
+    e.b = b();
+    e.c = c();
+    e.kind = kind();
+    return e;
+  }
+};
+static_assert(sizeof(EvP) == 16, "EvP is 16 bytes");
+
 struct GroupBuf {
   int2 *hdr;  // (nS, k) per group
   int2 *lnk;  // start-of-time links (group-local ids) per kept point
   int *gid;   // global sorted index per kept point
-  Ev *ev;     // events, 2 slots per point
+  EvP *ev;    // events, 2 slots per point
 };
 
 // both passes of a level in one launch: blockIdx.y = 0 lower, 1 upper
@@ -143,7 +183,7 @@ inline bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
     g->hdr = ar.take<int2>(n);
     g->lnk = ar.take<int2>(n);
     g->gid = ar.take<int>(n);
-    g->ev = ar.take<Ev>(2 * n);
+    g->ev = ar.take<EvP>(2 * n);
   }
   w.seq = ar.take<Ev>(2 * n);
   w.rec = ar.take<Rec>(n);

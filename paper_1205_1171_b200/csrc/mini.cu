@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   // ---- merged child sequence S (merge path, left first on equal times);
   // the child times are staged in shared memory first (the bridge-event
   // arrays are free until the sweeps) so the co-rank searches stay on chip
-  const Ev *evL = in.ev + 2 * L, *evR = in.ev + 2 * M;
+  const EvP *evL = in.ev + 2 * L, *evR = in.ev + 2 * M;
   double *tL = m.bt, *tR = m.bt + kL;
   for (int d = tid; d < kL; d += T) tL[d] = evL[d].t;
   for (int d = tid; d < kR; d += T) tR[d] = evR[d].t;
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   }
   MINI_TICK(7);
   // ---- merged log (job-local ids) straight to HBM, first event per point
-  Ev *evo = out.ev + 2 * L;
+  EvP *evo = out.ev + 2 * L;
   for (int d = tid; d < kin; d += T) {
     const int cp = m.cpos[d];
     if (!(cp & (1 << 30))) continue;

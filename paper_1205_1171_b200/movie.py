@@ -131,11 +131,13 @@ def final_movie(points, engine: str = "fast", device=None):
     nS, k = (int(v) for v in lay.hdr_view(buf, 0).view(torch.int32).cpu().tolist())
     lnk = lay.lnk_view(buf, 0, nS).view(torch.int32).view(nS, 2).cpu().numpy().astype(np.int64)
     gid = lay.gid_view(buf, 0, nS).view(torch.int32).cpu().numpy().astype(np.int64)
-    ev = lay.ev_view(buf, 0, k).cpu().numpy().view(np.int32).reshape(k, 6)
+    # EvP (16 B): t f64, then a | b << 21 | c << 42 | kind << 63
+    w = lay.ev_view(buf, 0, k).cpu().numpy().view(np.uint64).reshape(k, 2)[:, 1]
+    b = ((w >> np.uint64(21)) & np.uint64((1 << 21) - 1)).astype(np.int64)
     links = np.full((n, 2), NIL, dtype=np.int64)
     glob = np.where(lnk == NIL, NIL, gid[np.clip(lnk, 0, None)])
     links[gid] = glob
-    log = np.append(gid[ev[:, 3]], NIL) if k else np.array([NIL])
+    log = np.append(gid[b], NIL) if k else np.array([NIL])
     return coords, links, log
 
 

@@ -91,7 +91,7 @@ class GroupLayout:
     h3d_fast_layout in include/hull3d_b200.h)."""
 
     LNK = 8
-    EV = 24
+    EV = 16  # EvP: t f64 + one word with the 21-bit local ids and the kind
 
     def __init__(self, ws: torch.Tensor, n: int):
         offs = (ctypes.c_int64 * 9)()
