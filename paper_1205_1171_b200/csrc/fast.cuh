@@ -164,6 +164,17 @@ __device__ __forceinline__ int bridge_rec(const Rec *R, int *pu, int *pv, long l
   }
 }
 
+// lane-per-job merge (lane.cu): a job's shared-memory slice is
+//   [XYZ: x, y, z f64 per point] lk short2, gd int, fi u32 per point,
+//   then ot f64 + ow u64 per staged output event (16-byte aligned pieces)
+__host__ __device__ __forceinline__ int lane_pt_bytes(bool xyz) { return xyz ? 36 : 12; }
+// staged output capacity of a job: its child events plus a margin (a merged
+// log is rarely much longer than its children's; the rest spills to HBM)
+__host__ __device__ __forceinline__ int lane_ocap(int nS, int kin) { return kin + (nS >> 2) + 4; }
+__host__ __device__ __forceinline__ int lane_slice_bytes(int nS, int ocap, bool xyz) {
+  return static_cast<int>(align16((long long)lane_pt_bytes(xyz) * nS) + 16ll * ocap);
+}
+
 }  // namespace h3d
 
 // ---------------------------------------------------------------- host side
@@ -187,7 +198,7 @@ inline bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
   }
   w.seq = ar.take<Ev>(2 * n);
   w.rec = ar.take<Rec>(n);
-  w.need = ar.take<unsigned long long>(16);
+  w.need = ar.take<unsigned long long>(32);
   return ar.base == nullptr || w.need != nullptr;
 }
 
@@ -208,6 +219,12 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
 // (mini.cu): jobs of at most MINI_N points and MINI_K merged child events
 // variant 0: jobs of <= 256 points and 512 child events (~40 KB, several
 // CTAs per SM); variant 1: <= 1024 points and 2048 events (~154 KB)
+// one level of both passes, one lane per job (lane.cu); need = the level's
+// measurement (k_tpj_need); returns 0, 1 (does not fit) or a negative code
+long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
+                     long long j1, long long *err, const unsigned long long *need,
+                     long long xyz_max, cudaStream_t s);
+
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant,
                      long long *spec = nullptr);
