@@ -430,14 +430,16 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long chunks = (j1 - j0 + 31) >> 5;
   unsigned long long mx[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  // lane kernel pools (lane.cu): per jobs-per-CTA choice, without / with
-  // staged coordinates
-  unsigned long long lb[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  // lane kernel pools (lane.cu): per jobs-per-CTA choice r and variant
+  // v = 2 * xyz + staged events
+  unsigned long long lb[24];
+#pragma unroll
+  for (int q = 0; q < 24; ++q) lb[q] = 0;
   unsigned long long ksum = 0;
   for (long long c = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
     const long long j = j0 + c * 32 + lane;
-    unsigned long long nS = 0, wb = 0, kin = 0, b0 = 0, b1 = 0;
+    unsigned long long nS = 0, wb = 0, kin = 0, b[4] = {0, 0, 0, 0};
     if (j < j1) {
       const long long L = j << level;
       const long long R_ = (L + size < n) ? L + size : n;
@@ -448,21 +450,24 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
         wb = warp_job_bytes(static_cast<int>(nS), hl.y + hr.y);
         if (nS < 0x7fff) {
           const int oc = lane_ocap(static_cast<int>(nS), static_cast<int>(kin));
-          b0 = lane_slice_bytes(static_cast<int>(nS), oc, false);
-          b1 = lane_slice_bytes(static_cast<int>(nS), oc, true);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            b[v] = lane_slice_bytes(static_cast<int>(nS), (v & 1) ? oc : 0, v >= 2);
         } else {
-          b0 = b1 = 1ull << 40;  // never fits a lane pool
+#pragma unroll
+          for (int v = 0; v < 4; ++v) b[v] = 1ull << 40;  // never fits a lane pool
         }
       }
     }
-    lb[5] = b0 > lb[5] ? b0 : lb[5];
-    lb[11] = b1 > lb[11] ? b1 : lb[11];
 #pragma unroll
-    for (int r = 4; r >= 0; --r) {  // 2, 4, 8, 16, 32 jobs per CTA
-      b0 += __shfl_xor_sync(FULL, b0, 1 << (4 - r));
-      b1 += __shfl_xor_sync(FULL, b1, 1 << (4 - r));
-      lb[r] = b0 > lb[r] ? b0 : lb[r];
-      lb[6 + r] = b1 > lb[6 + r] ? b1 : lb[6 + r];
+    for (int v = 0; v < 4; ++v) {
+      unsigned long long t = b[v];
+      lb[6 * v + 5] = t > lb[6 * v + 5] ? t : lb[6 * v + 5];
+#pragma unroll
+      for (int r = 4; r >= 0; --r) {  // 2, 4, 8, 16, 32 jobs per CTA
+        t += __shfl_xor_sync(FULL, t, 1 << (4 - r));
+        lb[6 * v + r] = t > lb[6 * v + r] ? t : lb[6 * v + r];
+      }
     }
     mx[6] = nS > mx[6] ? nS : mx[6];
     mx[7] = wb > mx[7] ? wb : mx[7];
@@ -477,7 +482,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
     }
   }
   // warp, then block reduction; one atomic per value per block
-  __shared__ unsigned long long red[32][22];
+  __shared__ unsigned long long red[32][34];
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int o = 16; o; o >>= 1) ksum += __shfl_xor_sync(FULL, ksum, o);
 #pragma unroll
@@ -491,7 +496,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
   }
   if (lane == 0) red[w][9] = ksum;
 #pragma unroll
-  for (int r = 0; r < 12; ++r) {
+  for (int r = 0; r < 24; ++r) {
     unsigned long long m = lb[r];
     for (int o = 16; o; o >>= 1) {
       const unsigned long long x = __shfl_xor_sync(FULL, m, o);
@@ -500,13 +505,13 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
     if (lane == 0) red[w][10 + r] = m;
   }
   __syncthreads();
-  if (threadIdx.x < 22) {
+  if (threadIdx.x < 34) {
     unsigned long long m = 0;
     for (int q = 0; q < nw; ++q) {
       const unsigned long long x = red[q][threadIdx.x];
       m = threadIdx.x == 9 ? m + x : (x > m ? x : m);
     }
-    // out[16 + r] / out[22 + r]: lane pools without / with coordinates
+    // out[16 + 6 v + r]: lane pools of variant v (2 * xyz + staged events)
     const int slot = threadIdx.x < 10 ? threadIdx.x : 6 + threadIdx.x;
     if (m) {
       if (threadIdx.x == 9) atomicAdd(out + 9, m); else atomicMax(out + slot, m);
@@ -1470,6 +1475,8 @@ void load_env_once() {
   if (const char *e = getenv("H3D_MINI_SPEC")) g_mini_spec = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_TRACE")) g_trace = atoi(e);
   if (const char *e = getenv("H3D_LANE")) g_lane = atoi(e);
+  if (const char *e = getenv("H3D_LANE_XYZ_KB")) g_lane_xyz_max = atoll(e) * 1024;
+  if (const char *e = getenv("H3D_LANE_STAGE")) g_lane_stage = atoi(e);
   if (const char *e = getenv("H3D_TPJ_PREFETCH")) kTpjPrefetchJobs = atoll(e);
   g_leaf_b = leaf_depth(g_leaf_b);
 }
@@ -1502,6 +1509,8 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
   else if (k == "lane") { old = g_lane; if (value >= 0) g_lane = value ? 1 : 0; }
+  else if (k == "lane_xyz_kb") { old = g_lane_xyz_max / 1024; if (value >= 0) g_lane_xyz_max = value * 1024; }
+  else if (k == "lane_stage") { old = g_lane_stage; if (value >= 0) g_lane_stage = value ? 1 : 0; }
   else if (k == "tpj_max_level") { old = kTpjMaxLevel; if (value >= 0) kTpjMaxLevel = static_cast<int>(value); }
   return old;
 }
@@ -1607,12 +1616,12 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     // they fit a shared-memory slice (int16 local ids); one warp per job
     // (1-warp CTAs, pool = the largest job's need, HBM mode above it) for
     // the few-job levels.
-    cudaMemsetAsync(w0.need, 0, 28 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(w0.need, 0, 40 * sizeof(unsigned long long), s);
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
     k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 2 * 148 ? 2 * 148 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
         P, n, lv, j0, j1, w0.need, err);
-    unsigned long long need[28];
+    unsigned long long need[40];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
       return H3D_E_CUDA;
@@ -1731,7 +1740,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       }
     }
     if (tpj && g_lane) {
-      const long long rl = lane_level(P, sorted_pts, n, lv, j0, j1, err, need, kTpjXyzMax, s);
+      const long long rl = lane_level(P, sorted_pts, n, lv, j0, j1, err, need, s);
       if (rl < 0) return rl;
       if (rl == 0) {
         h3d_prof_end(e0, lv + 1000, 2, s);

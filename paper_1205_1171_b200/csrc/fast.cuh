@@ -198,7 +198,7 @@ inline bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
   }
   w.seq = ar.take<Ev>(2 * n);
   w.rec = ar.take<Rec>(n);
-  w.need = ar.take<unsigned long long>(32);
+  w.need = ar.take<unsigned long long>(48);
   return ar.base == nullptr || w.need != nullptr;
 }
 
@@ -223,7 +223,9 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
 // measurement (k_tpj_need); returns 0, 1 (does not fit) or a negative code
 long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, const unsigned long long *need,
-                     long long xyz_max, cudaStream_t s);
+                     cudaStream_t s);
+extern long long g_lane_xyz_max;  // lane.cu knobs
+extern int g_lane_stage;
 
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant,

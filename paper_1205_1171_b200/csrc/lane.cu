@@ -157,23 +157,45 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
   double tcur = -INF;
   while (__any_sync(FULL, active)) {
     // ---- recompute the candidates whose inputs changed
-    while (dirty) {
-      const int d = __ffs(dirty) - 1;
-      dirty &= dirty - 1;
-      const int o = d == 0 ? un : (d == 1 ? up : (d == 2 ? vn : vp));
-      double t = INF;
-      if (o != NIL) {
-        const P3 O = S.pt(o, pts, zs);
-        // c2 = (u, un, v)  c3 = (up, u, v)  c4 = (u, v, vn)  c5 = (u, vp, v)
-        const P3 A = d == 1 ? O : U;
-        const P3 B = (d == 0 || d == 3) ? O : (d == 1 ? U : V);
-        const P3 C = d == 2 ? O : V;
-        t = evtime_xyz(A.x, A.y, A.z, B.x, B.y, B.z, C.x, C.y, C.z);
+    // c2 = (u, un, v)  c3 = (up, u, v)  c4 = (u, v, vn)  c5 = (u, vp, v)
+    if (XYZ) {
+      // coordinates in shared memory: one loop, a warp pays for the largest
+      // dirty mask of its lanes
+      while (dirty) {
+        const int d = __ffs(dirty) - 1;
+        dirty &= dirty - 1;
+        const int o = d == 0 ? un : (d == 1 ? up : (d == 2 ? vn : vp));
+        double t = INF;
+        if (o != NIL) {
+          const P3 O = S.pt(o, pts, zs);
+          const P3 A = d == 1 ? O : U;
+          const P3 B = (d == 0 || d == 3) ? O : (d == 1 ? U : V);
+          const P3 C = d == 2 ? O : V;
+          t = evtime_xyz(A.x, A.y, A.z, B.x, B.y, B.z, C.x, C.y, C.z);
+        }
+        c2 = d == 0 ? t : c2;
+        c3 = d == 1 ? t : c3;
+        c4 = d == 2 ? t : c4;
+        c5 = d == 3 ? t : c5;
       }
-      c2 = d == 0 ? t : c2;
-      c3 = d == 1 ? t : c3;
-      c4 = d == 2 ? t : c4;
-      c5 = d == 3 ? t : c5;
+    } else if (__any_sync(FULL, dirty != 0)) {
+      // coordinates in HBM/L2: issue every needed row first (one latency),
+      // then compute
+      const bool d0 = (dirty & 1u) && un != NIL, d1 = (dirty & 2u) && up != NIL;
+      const bool d2 = (dirty & 4u) && vn != NIL, d3 = (dirty & 8u) && vp != NIL;
+      P3 O0, O1, O2, O3;
+      O0.x = O0.y = O0.z = O1.x = O1.y = O1.z = 0.0;
+      O2 = O0;
+      O3 = O0;
+      if (d0) O0 = S.pt(un, pts, zs);
+      if (d1) O1 = S.pt(up, pts, zs);
+      if (d2) O2 = S.pt(vn, pts, zs);
+      if (d3) O3 = S.pt(vp, pts, zs);
+      if (dirty & 1u) c2 = d0 ? evtime_xyz(U.x, U.y, U.z, O0.x, O0.y, O0.z, V.x, V.y, V.z) : INF;
+      if (dirty & 2u) c3 = d1 ? evtime_xyz(O1.x, O1.y, O1.z, U.x, U.y, U.z, V.x, V.y, V.z) : INF;
+      if (dirty & 4u) c4 = d2 ? evtime_xyz(U.x, U.y, U.z, V.x, V.y, V.z, O2.x, O2.y, O2.z) : INF;
+      if (dirty & 8u) c5 = d3 ? evtime_xyz(U.x, U.y, U.z, O3.x, O3.y, O3.z, V.x, V.y, V.z) : INF;
+      dirty = 0;
     }
     // ---- next event: earliest time strictly after tcur, lowest case on ties
     double best = INF;
@@ -295,7 +317,7 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
 template <bool XYZ>
 __global__ void __launch_bounds__(32) k_lane(Pass2 P, const double *__restrict__ pts, long long n,
                                              int level, long long j0, long long j1,
-                                             long long *err, int pool, int jpc) {
+                                             long long *err, int pool, int jpc, int stage) {
   // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
   if (__any_sync(FULL, *reinterpret_cast<volatile long long *>(err) != 0)) return;
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
@@ -332,7 +354,7 @@ __global__ void __launch_bounds__(32) k_lane(Pass2 P, const double *__restrict__
     raise_err(err, E_FASTPATH);
     merge = false;
   }
-  const int ocap = merge ? lane_ocap(nS, kL + kR) : 0;
+  const int ocap = (merge && stage) ? lane_ocap(nS, kL + kR) : 0;
   // pack the slices: warp exclusive prefix sum of the slice sizes
   const int bytes = merge ? lane_slice_bytes(nS, ocap, XYZ) : 0;
   int off = bytes;
@@ -528,14 +550,18 @@ namespace {
 bool g_lane_attr[64] = {};
 }
 
-// Host side: choose jobs per CTA and coordinate staging from the level's
-// measured shared-memory need (k_tpj_need: need[16 + r] / need[22 + r] =
-// largest CTA pool without / with coordinates for 32 >> r jobs per CTA) and
-// launch.  Returns 0, 1 (does not fit: the caller routes the level
-// elsewhere) or a negative code.
+// lane-kernel variant knobs (h3d_tune / environment, fast.cu)
+long long g_lane_xyz_max = 200 * 1024;  // H3D_LANE_XYZ_KB: stage coordinates up to this pool
+int g_lane_stage = 1;                   // H3D_LANE_STAGE: stage merged events (0 = never)
+
+// Host side: choose the variant (coordinates / merged events staged in
+// shared memory) and jobs per CTA from the level's measured shared-memory
+// need (k_tpj_need: need[16 + 6 v + r] = largest CTA pool of variant
+// v = 2 * xyz + staged for 32 >> r jobs per CTA), and launch.  Returns 0,
+// 1 (does not fit: the caller routes the level elsewhere) or a negative code.
 long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, const unsigned long long *need,
-                     long long xyz_max, cudaStream_t s) {
+                     cudaStream_t s) {
   constexpr int kPool = 200 * 1024;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -547,23 +573,39 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
     g_lane_attr[dev] = true;
   }
   const long long jobs = j1 - j0;
-  int r = 0;
-  while (r < 5 && static_cast<long long>(need[16 + r]) > kPool) ++r;
-  if (static_cast<long long>(need[16 + r]) > kPool) return 1;
+  auto pick = [&](int v, int *jr) {  // fewest-lanes-idle jobs per CTA that fits
+    int r = 0;
+    while (r < 5 && static_cast<long long>(need[16 + 6 * v + r]) > kPool) ++r;
+    *jr = r;
+    return static_cast<long long>(need[16 + 6 * v + r]);
+  };
+  int r = 0, v = -1;
+  long long pool = 0;
+  for (int xyz = 1; xyz >= 0 && v < 0; --xyz) {
+    for (int st = g_lane_stage ? 1 : 0; st >= 0 && v < 0; --st) {
+      int rr;
+      const long long p = pick(2 * xyz + st, &rr);
+      if (p > kPool || (xyz && p > g_lane_xyz_max)) continue;
+      // staged events only while they cost no jobs per CTA
+      if (st) {
+        int r0;
+        pick(2 * xyz, &r0);
+        if (rr != r0) continue;
+      }
+      v = 2 * xyz + st;
+      r = rr;
+      pool = p;
+    }
+  }
+  if (v < 0) return 1;
   const int jpc = 32 >> r;
-  const long long ctas = 2 * ((jobs + jpc - 1) / jpc);
-  // stage coordinates when the pool stays small, or when there are too few
-  // CTAs for shared memory to limit occupancy
-  const long long pxyz = static_cast<long long>(need[22 + r]);
-  const bool xyz = pxyz <= xyz_max || (ctas <= 4 * 148 && pxyz <= kPool);
-  long long pool = xyz ? pxyz : static_cast<long long>(need[16 + r]);
   if (pool < 1024) pool = 1024;
   h3d_count_launches(1);
   const dim3 grid(h3d_grid(jobs, jpc), 2);
-  if (xyz)
-    k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc);
+  if (v >= 2)
+    k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1);
   else
-    k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc);
+    k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1);
   return 0;
 }
 
