@@ -52,6 +52,7 @@ extern "C" {
 #define H3D_E_CAPACITY (-11)     /* fast-path fixed capacity exceeded       */
 #define H3D_E_NONFINITE (-12)   /* ValueError("coordinates must be finite") */
 #define H3D_E_FASTPATH (-13)     /* fast path declined: caller takes the exact route */
+#define H3D_E_VERIFY (-14)       /* verify mode: a level wrote an inconsistent group */
 #define H3D_E_ARG (-100)         /* bad argument                            */
 #define H3D_E_CUDA (-101)        /* CUDA runtime error                      */
 
@@ -193,7 +194,7 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n,
 int64_t h3d_tune(const char *name, int64_t value);
 
 /* bytes of workspace one h3d_fast_pass needs for n points (two compact
- * group buffers: headers, int2 links, ids, 24-byte events; HBM scratch of
+ * group buffers: headers, int2 links, ids, 16-byte events; HBM scratch of
  * the warp merge; and, in the lower pass's workspace, the scratch of the
  * time-split pipeline for large merge jobs, sized for min(n, max(2^21, n/8)) points
  * per pass -- levels beyond it fall back to the warp merge) */
@@ -227,8 +228,9 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0,
  * A.hdr, A.lnk, A.gid, A.ev, B.hdr, B.lnk, B.gid, B.ev, seq (host int64[9]).
  * hdr = int2 (nS, k) per group; lnk = int2 (prev, next) group-local ids of
  * each kept point at t = -inf; gid = i32 sorted index of each kept point
- * (coordinates are read from sorted_pts); ev = 24-byte events (t f64, a, b,
- * c, kind i32); a group [L, R) at level l has header l, links/ids at
+ * (coordinates are read from sorted_pts); ev = 16-byte events (t f64, then
+ * one u64 word: local ids a | b << 21 | c << 42, kind in bit 63); a group
+ * [L, R) at level l has header l, links/ids at
  * [L, L+nS) and events at [2L, 2L+k).  Used to ship groups between GPUs. */
 int64_t h3d_fast_layout(int64_t n, int64_t *offsets);
 
@@ -240,6 +242,29 @@ int64_t h3d_fast_extract(void *ws_lower, void *ws_upper, int64_t n,
                          int64_t final_lower, int64_t final_upper,
                          int32_t *faces, int64_t cap, int64_t *counts_dev,
                          int64_t *err_dev, void *stream);
+
+/* ---- device-wide primitives (csrc/prims.cuh), hand-written for sm_100a;
+ * exported so the parity tests can check them against numpy on their own.
+ * All pointers are device pointers; tmp is caller-owned scratch of
+ * h3d_prim_temp_bytes(n) bytes. */
+size_t h3d_prim_temp_bytes(int64_t n);
+/* Stable LSD radix sort of (key, i32 value) pairs by key bits
+ * [begin_bit, end_bit) (numpy argsort(kind="stable") semantics, the sort
+ * under api.py:97 and :86-87); key_bytes 4 or 8; iota_vals: the input values
+ * are 0..n-1 (vals is not read).  The data ping-pong between (keys, vals)
+ * and (keys_alt, vals_alt); returns 0 (result in keys/vals), 1 (result in
+ * the _alt buffers) or a negative code. */
+int64_t h3d_radix_sort_pairs(void *keys, void *keys_alt, int32_t *vals, int32_t *vals_alt, int64_t n,
+                             int32_t key_bytes, int32_t begin_bit, int32_t end_bit, int32_t iota_vals,
+                             void *tmp, size_t tmp_bytes, void *stream);
+/* Inclusive or exclusive scan of int64 with + or max (np.cumsum /
+ * np.maximum.accumulate); in == out allowed. */
+int64_t h3d_scan_i64(const int64_t *in, int64_t *out, int64_t n, int32_t op_max, int32_t exclusive,
+                     void *tmp, size_t tmp_bytes, void *stream);
+/* Indices of the nonzero flags in ascending order (np.flatnonzero);
+ * *count_dev (device int64) receives how many. */
+int64_t h3d_select_flagged(const int32_t *flags, int64_t n, int64_t *out, int64_t *count_dev, void *tmp,
+                           size_t tmp_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -30,9 +30,8 @@
 //
 // All arrays are compact over the level's jobs of both passes (pass-major),
 // so a level costs O(sum of group sizes), not O(n).
-#include <cub/cub.cuh>
-
 #include "fast.cuh"
+#include "prims.cuh"
 
 namespace h3d {
 
@@ -149,16 +148,10 @@ static bool carve_big(h3d_arena &ar, long long m, BigWS &b) {
   b.slab = ar.take<BEv>(2 * EK);  // shared by the level's segments
   b.bev = ar.take<BEv>(EK);
   b.tot = ar.take<int>(16);
-  // cub temp: the largest of the sort and the scans
-  size_t a = 0, c = 0;
-  cub::DoubleBuffer<unsigned> kb(nullptr, nullptr), vb(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, static_cast<int>(3 * EK));
-  cub::DeviceScan::ExclusiveSum(nullptr, c, static_cast<int *>(nullptr),
-                                static_cast<int *>(nullptr), static_cast<int>(EK + 1));
-  size_t d = 0;
-  cub::DeviceScan::InclusiveScan(nullptr, d, static_cast<unsigned long long *>(nullptr),
-                                 static_cast<unsigned long long *>(nullptr), LinkScanOp(),
-                                 static_cast<int>(3 * EK));
+  // primitives' temp (prims.cuh): the largest of the sort and the scans
+  size_t a = prim::rs_temp_bytes<unsigned>(3 * EK);
+  const size_t c = prim::scan_temp_bytes<int>(EK + 1 > 2 * EP ? EK + 1 : 2 * EP);
+  const size_t d = prim::scan_temp_bytes<unsigned long long>(3 * EK);
   if (d > a) a = d;
   b.tmp_bytes = (a > c ? a : c) + 256;
   b.tmp = ar.take<unsigned char>(b.tmp_bytes);
@@ -945,8 +938,8 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   const long long J2 = 2 * J;
   if (J2 + 1 > W.m + 64) return 1;
   auto scan = [&](int *in, int *out, long long items) -> bool {
-    size_t tb = W.tmp_bytes;
-    return h3d_check(cub::DeviceScan::ExclusiveSum(W.tmp, tb, in, out, static_cast<int>(items), s));
+    h3d_count_launches(3);
+    return h3d_check(prim::scan<true, int>(W.tmp, W.tmp_bytes, in, out, items, prim::OpSum(), 0, 0, s));
   };
   h3d_count_launches(1);
   k_big_jobs<<<grid_of(J2), 256, 0, s>>>(P, n, lv, j0, J, W, err);
@@ -983,21 +976,23 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   k_big_seq<<<grid_of(kin), 256, 0, s>>>(P, n, lv, j0, J, W);
   // incidence lists: stable sort of (point, event) pairs by point
   {
-    cub::DoubleBuffer<unsigned> kb(W.k0, W.k1), vb(W.v0, W.v1);
     int bits = 1;
     while ((1ll << bits) < pts_n + 1) ++bits;
-    size_t tb = W.tmp_bytes;
-    if (h3d_check(cub::DeviceRadixSort::SortPairs(W.tmp, tb, kb, vb, static_cast<int>(3 * kin), 0,
-                                                  bits, s)))
+    bool alt = false;
+    h3d_count_launches((bits + 7) / 8 + 1);
+    if (h3d_check(prim::rs_sort_pairs<unsigned>(W.tmp, W.tmp_bytes, W.k0, reinterpret_cast<int *>(W.v0), W.k1,
+                                                reinterpret_cast<int *>(W.v1), 3 * kin, 0, bits, &alt, s)))
       return H3D_E_CUDA;
-    k_big_incidx<<<grid_of(3 * kin), 256, 0, s>>>(kb.Current(), static_cast<int>(3 * kin), W);
-    k_big_fill_init<<<grid_of(3 * kin), 256, 0, s>>>(P, n, lv, j0, J, W, kb.Current(), vb.Current(),
+    const unsigned *kcur = alt ? W.k1 : W.k0;
+    const unsigned *vcur = alt ? W.v1 : W.v0;
+    k_big_incidx<<<grid_of(3 * kin), 256, 0, s>>>(kcur, static_cast<int>(3 * kin), W);
+    k_big_fill_init<<<grid_of(3 * kin), 256, 0, s>>>(P, n, lv, j0, J, W, kcur, vcur,
                                                     static_cast<int>(3 * kin));
-    size_t tb2 = W.tmp_bytes;
-    if (h3d_check(cub::DeviceScan::InclusiveScan(W.tmp, tb2, W.sc0, W.sc1, LinkScanOp(),
-                                                 static_cast<int>(3 * kin), s)))
+    h3d_count_launches(3);
+    if (h3d_check(prim::scan<false, unsigned long long>(W.tmp, W.tmp_bytes, W.sc0, W.sc1, 3 * kin,
+                                                        LinkScanOp(), 0ull, 0ull, s)))
       return H3D_E_CUDA;
-    k_big_fill_final<<<grid_of(3 * kin), 256, 0, s>>>(P, n, lv, j0, J, W, kb.Current(), vb.Current(),
+    k_big_fill_final<<<grid_of(3 * kin), 256, 0, s>>>(P, n, lv, j0, J, W, kcur, vcur,
                                                      static_cast<int>(3 * kin));
   }
   k_big_walk<<<grid_of(nseg), 256, 0, s>>>(P, pts, n, lv, j0, J, W, static_cast<int>(SEG), err);

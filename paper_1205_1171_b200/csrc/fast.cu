@@ -147,10 +147,28 @@ struct TpjSlice {
 };
 
 // event streams of the sweep: HBM (16-byte EvP) ...
+// The prefetched event stays PACKED (Raw) in registers and is unpacked only
+// when it becomes the stream head one consumption later: unpacking at the
+// load would put the load's full latency on the step that issued it (47 % of
+// the stall samples at C4 level 8, profiles/r2_ncu_lines_tpj.txt).
 struct GEvIn {
   static constexpr bool kPrefetch = true;  // HBM: one event of prefetch
+  using Raw = EvP;
   const EvP *__restrict__ p;
+  __device__ __forceinline__ EvP raw(int i) const {
+    EvP r;  // two 64-bit loads: a 128-bit one needs an aligned register quad,
+    r.t = __ldg(&p[i].t);  // which the loop-carried prefetch does not get
+    r.w = __ldg(&p[i].w);
+    return r;
+  }
   __device__ __forceinline__ Ev get(int i) const { return p[i]; }
+  __device__ __forceinline__ static Ev unpack(const EvP &r) { return r; }
+  __device__ __forceinline__ static EvP none() {
+    EvP r;
+    r.t = INF;
+    r.w = 0;
+    return r;
+  }
 };
 struct GEvOut {
   EvP *__restrict__ p;
@@ -161,6 +179,15 @@ struct GEvOut {
 // the kind -- half the bytes of a 32-bit word, so more CTAs fit an SM
 struct LEvIn {
   static constexpr bool kPrefetch = false;  // shared memory: read when consumed
+  using Raw = Ev;
+  __device__ __forceinline__ Ev raw(int i) const { return get(i); }
+  __device__ __forceinline__ static Ev unpack(const Ev &r) { return r; }
+  __device__ __forceinline__ static Ev none() {
+    Ev r;
+    r.t = INF;
+    r.a = r.b = r.c = r.kind = 0;
+    return r;
+  }
   const double *t;
   const unsigned short *w;
   __device__ __forceinline__ Ev get(int i) const {
@@ -254,16 +281,18 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
   double c5 = evt3(u, vp, v, U, VP, V);
   // child event streams with one event of prefetch
   int i = 0, j = 0;
-  Ev cL, cR, nL, nR;
-  cL.t = cR.t = nL.t = nR.t = INF;
+  Ev cL, cR;
+  typename EIN::Raw nL = EIN::none(), nR = EIN::none();
+  cL.t = cR.t = INF;
   if (active) {
     if (kL > 0) cL = evL.get(0);
     if (kR > 0) cR = evR.get(0);
-    if (EIN::kPrefetch) {  // HBM streams: one event of prefetch
-      if (kL > 1) nL = evL.get(1);
-      if (kR > 1) nR = evR.get(1);
+    if (EIN::kPrefetch) {  // HBM streams: one event of prefetch (packed)
+      nL = evL.raw(1);
+      nR = evR.raw(1);
     }
   }
+  (void)nL;
   long long k = 0;
   double tcur = -INF;
   // Branch-free step: all 32 lanes (32 different jobs) iterate together until
@@ -343,8 +372,11 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
     if (left) {
       ++i;
       if (EIN::kPrefetch) {
-        cL = nL;
-        if (i + 1 < kL) nL = evL.get(i + 1); else nL.t = INF;
+        // unconditional load straight into the loop-carried register (a
+        // predicated one compiles to a register move that waits for the
+        // load); slot i + 1 <= k of the child is inside its slot range
+        cL = i < kL ? EIN::unpack(nL) : EIN::unpack(EIN::none());
+        nL = evL.raw(i + 1);
       } else {
         if (i < kL) cL = evL.get(i); else cL.t = INF;
       }
@@ -352,8 +384,8 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
     if (right) {
       ++j;
       if (EIN::kPrefetch) {
-        cR = nR;
-        if (j + 1 < kR) nR = evR.get(j + 1); else nR.t = INF;
+        cR = j < kR ? EIN::unpack(nR) : EIN::unpack(EIN::none());
+        nR = evR.raw(j + 1);
       } else {
         if (j < kR) cR = evR.get(j); else cR.t = INF;
       }
@@ -1394,6 +1426,66 @@ __global__ void __launch_bounds__(WARPS * 32) k_fast_warp(Pass2 P, const double 
   }
 }
 
+// verify mode (h3d_fast_passes*(verify = 1)): an independent check of every
+// group a level wrote, one warp per group -- the header is in range, the
+// kept points' ids are strictly increasing inside the group's point range
+// (x order), every link is NIL or a local id, every event's facet is an
+// x-ordered triple (a < b < c) of local ids, its stored time equals the
+// event time RE-DERIVED from the facet's coordinates (evtime of the x-sorted
+// triple, _ckernels.pyx:34-46, bit for bit) and the times strictly increase
+// along the log.  A violation records H3D_E_VERIFY.
+__global__ void k_verify_level(Pass2 P, const double *__restrict__ pts, long long n, int level,
+                               long long j0, long long j1, long long *err, long long *diag,
+                               const long long *spec) {
+  // a speculative top-level chain (mini.cu) whose level (or an earlier one)
+  // did not fit wrote nothing: the loop redoes it, measured, and checks then
+  if (spec && *reinterpret_cast<const volatile long long *>(spec) != 0) return;
+  const GroupBuf g = blockIdx.y ? P.in1 : P.in0;  // the groups the level wrote
+  const double zs = blockIdx.y ? -1.0 : 1.0;
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long j = j0 + blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); j < j1;
+       j += warps) {
+    const long long L = j << level;
+    const long long R_ = (L + (1ll << level) < n) ? L + (1ll << level) : n;
+    const int2 h = g.hdr[j];
+    const int nS = h.x, k = h.y;
+    int why = (nS < 1 || nS > R_ - L || k < 0 || k > 2 * (R_ - L) - 1) ? 1 : 0;
+    long long at = 0;
+    if (!why) {
+      for (int p = lane; p < nS; p += 32) {
+        const int gp = g.gid[L + p];
+        const int2 l = g.lnk[L + p];
+        if (gp < L || gp >= R_ || (p > 0 && g.gid[L + p - 1] >= gp)) why = 2, at = p;
+        if (l.x < NIL || l.x >= nS || l.y < NIL || l.y >= nS) why = 3, at = p;
+      }
+      for (int e = lane; e < k; e += 32) {
+        const Ev ev = g.ev[2 * L + e];
+        if (ev.a < 0 || ev.a >= ev.b || ev.b >= ev.c || ev.c >= nS) {
+          why = 4, at = e;
+          continue;
+        }
+        const P3 A = load_pt(pts, g.gid[L + ev.a], zs), B = load_pt(pts, g.gid[L + ev.b], zs),
+                 C = load_pt(pts, g.gid[L + ev.c], zs);
+        const double t = evtime_xyz(A.x, A.y, A.z, B.x, B.y, B.z, C.x, C.y, C.z);
+        if (__double_as_longlong(t) != __double_as_longlong(ev.t)) why = 5, at = e;
+        if (e > 0 && !(g.ev[2 * L + e - 1].t < ev.t)) why = 6, at = e;
+      }
+    }
+    if (why) {
+      raise_err(err, H3D_E_VERIFY);
+      // first violation: kind | level | pass | group | index (debug aid)
+      if (diag)
+        atomicCAS(reinterpret_cast<unsigned long long *>(diag), 0ull,
+                  (static_cast<unsigned long long>(why) << 60) |
+                      (static_cast<unsigned long long>(level) << 54) |
+                      (static_cast<unsigned long long>(blockIdx.y) << 53) |
+                      (static_cast<unsigned long long>(j & 0xffffffffll) << 20) |
+                      static_cast<unsigned long long>(at & 0xfffff));
+    }
+  }
+}
+
 // facets of both passes: lower block then upper block, sorted indices
 __global__ void k_fast_extract(GroupBuf lo, GroupBuf up, int *faces, long long cap,
                                long long *counts, long long *err) {
@@ -1451,6 +1543,10 @@ long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
 int g_mini_spec = 1;  // H3D_MINI_SPEC
 int g_trace = 0;      // H3D_TRACE: one stderr line per routed level
 int g_lane = 1;       // H3D_LANE: lane-per-job levels on lane.cu (0 = k_fast_tpj)
+// highest level routed to lane.cu; k_fast_tpj above (measured per level, C4:
+// lane.cu 2.33 / 1.90 ms at levels 4 / 5 vs 2.60 / 2.13; k_fast_tpj ahead
+// from level 6 on, profiles/r2_levels_c4.jsonl)
+int g_lane_max_level = 5;  // H3D_LANE_MAX_LEVEL
 long long kTpjPrefetchJobs = 1ll << 18;  // H3D_TPJ_PREFETCH: L2 prefetch of rows from this many jobs
 
 // leaf kernel depth: 3 or 4 fused levels, anything below 3 = off
@@ -1475,6 +1571,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_MINI_SPEC")) g_mini_spec = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_TRACE")) g_trace = atoi(e);
   if (const char *e = getenv("H3D_LANE")) g_lane = atoi(e);
+  if (const char *e = getenv("H3D_LANE_MAX_LEVEL")) g_lane_max_level = atoi(e);
   if (const char *e = getenv("H3D_LANE_XYZ_KB")) g_lane_xyz_max = atoll(e) * 1024;
   if (const char *e = getenv("H3D_LANE_STAGE")) g_lane_stage = atoi(e);
   if (const char *e = getenv("H3D_TPJ_PREFETCH")) kTpjPrefetchJobs = atoll(e);
@@ -1509,6 +1606,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "tpj_min_jobs") { old = kTpjMinTotalJobs; if (value >= 0) kTpjMinTotalJobs = value; }
   else if (k == "tpj_xyz_kb") { old = kTpjXyzMax / 1024; if (value >= 0) kTpjXyzMax = value * 1024; }
   else if (k == "lane") { old = g_lane; if (value >= 0) g_lane = value ? 1 : 0; }
+  else if (k == "lane_max_level") { old = g_lane_max_level; if (value >= 0) g_lane_max_level = static_cast<int>(value); }
   else if (k == "lane_xyz_kb") { old = g_lane_xyz_max / 1024; if (value >= 0) g_lane_xyz_max = value * 1024; }
   else if (k == "lane_stage") { old = g_lane_stage; if (value >= 0) g_lane_stage = value ? 1 : 0; }
   else if (k == "tpj_max_level") { old = kTpjMaxLevel; if (value >= 0) kTpjMaxLevel = static_cast<int>(value); }
@@ -1543,7 +1641,6 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
                               size_t workspace_bytes, int64_t *err_dev, int32_t verify,
                               void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  (void)verify;
   if (n < 2 || n > (1ll << 30) || p0 < 0 || p1 > n || p0 >= p1 || lv_lo < 1) return H3D_E_ARG;
   h3d_arena a0(ws_lower, workspace_bytes), a1(ws_upper, workspace_bytes);
   PassWS w0, w1;
@@ -1572,6 +1669,16 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     g_attr_done[dev_id] = true;
   }
   long long *err = reinterpret_cast<long long *>(err_dev);
+  // verify mode: check the groups level l wrote (they are Q.in0/Q.in1)
+  auto check = [&](const Pass2 &Q, int l, const long long *spec = nullptr) {
+    if (!verify) return;
+    const long long a = p0 >> l, b = (p1 + (1ll << l) - 1) >> l;
+    h3d_count_launches(1);
+    const unsigned gv = h3d_grid(b - a, 8) > 4096 ? 4096 : h3d_grid(b - a, 8);
+    // verify >= 2: err_dev has 4 words, the first violation goes to err_dev[3]
+    k_verify_level<<<dim3(gv, 2), 256, 0, s>>>(Q, sorted_pts, n, l, a, b, err, verify >= 2 ? err + 3 : nullptr,
+                                               spec);
+  };
   int levels = 0;
   while ((1ll << levels) < n) ++levels;
   if (lv_hi > levels) lv_hi = levels;
@@ -1606,6 +1713,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     lv = 2;
   }
   for (; lv <= lv_hi; ++lv) {
+    if (lv > lv_lo) check(P, lv - 1);  // the previous level's groups
     // the jobs of this level inside the point range [p0, p1)
     const long long j0 = p0 >> lv;
     const long long j1 = (p1 + (1ll << lv) - 1) >> lv;
@@ -1681,6 +1789,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           }
           h3d_prof_end(e2, l2 + 5000, 2, s);
           P = Pass2{P.out0, P.out1, P.in0, P.in1};
+          check(P, l2, spec);
         }
         long long failed = 0, serr = 0;
         if (h3d_check(cudaMemcpyAsync(&failed, spec, sizeof(failed), cudaMemcpyDeviceToHost, s)) ||
@@ -1739,7 +1848,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         if (pool < 1024) pool = 1024;
       }
     }
-    if (tpj && g_lane) {
+    if (tpj && g_lane && lv <= g_lane_max_level) {
       const long long rl = lane_level(P, sorted_pts, n, lv, j0, j1, err, need, s);
       if (rl < 0) return rl;
       if (rl == 0) {
@@ -1770,6 +1879,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     }
     P = Pass2{P.out0, P.out1, P.in0, P.in1};
   }
+  if (lv > lv_hi && lv - 1 >= lv_lo) check(P, lv - 1);  // the last level (when the loop ran it)
   if (h3d_check(cudaGetLastError())) return H3D_E_CUDA;
   return lv_hi & 1;  // buffer holding the last level's groups
 }

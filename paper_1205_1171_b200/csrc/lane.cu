@@ -79,6 +79,16 @@ struct LSlice {
   }
 };
 
+// two 64-bit loads straight into the loop-carried prefetch registers (a
+// 128-bit load needs an aligned register quad, and the copy into the
+// loop-carried registers then waits for the load)
+__device__ __forceinline__ EvP ld_ev(const EvP *__restrict__ p) {
+  EvP r;
+  r.t = __ldg(&p->t);
+  r.w = __ldg(&p->w);
+  return r;
+}
+
 __device__ __forceinline__ EvP ev_inf() {
   EvP e;
   e.t = INF;
@@ -150,8 +160,9 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
   if (active) {
     if (kL > 0) hL = evL[0];
     if (kR > 0) hR = evR[0];
-    if (kL > 1) nL = evL[1];
-    if (kR > 1) nR = evR[1];
+    // slot 1 (and later slot i + 1 <= k) is inside the child's slot range
+    nL = ld_ev(evL + 1);
+    nR = ld_ev(evR + 1);
   }
   int i = 0, j = 0, k = 0;
   double tcur = -INF;
@@ -241,12 +252,12 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
         if (q == v) { vp = del ? p : e; dirty |= 8u; }
         if (left) {
           ++i;
-          hL = nL;
-          nL = i + 1 < kL ? evL[i + 1] : ev_inf();
+          hL = i < kL ? nL : ev_inf();
+          nL = ld_ev(evL + i + 1);
         } else {
           ++j;
-          hR = nR;
-          nR = j + 1 < kR ? evR[j + 1] : ev_inf();
+          hR = j < kR ? nR : ev_inf();
+          nR = ld_ev(evR + j + 1);
         }
       }
     } else if (active) {
@@ -551,8 +562,10 @@ bool g_lane_attr[64] = {};
 }
 
 // lane-kernel variant knobs (h3d_tune / environment, fast.cu)
-long long g_lane_xyz_max = 200 * 1024;  // H3D_LANE_XYZ_KB: stage coordinates up to this pool
-int g_lane_stage = 1;                   // H3D_LANE_STAGE: stage merged events (0 = never)
+// (defaults measured on C4/C2/C3: staging either costs more occupancy than
+// it saves, profiles/r2_levels_c4.jsonl)
+long long g_lane_xyz_max = 0;  // H3D_LANE_XYZ_KB: stage coordinates up to this pool
+int g_lane_stage = 0;          // H3D_LANE_STAGE: stage merged events (0 = never)
 
 // Host side: choose the variant (coordinates / merged events staged in
 // shared memory) and jobs per CTA from the level's measured shared-memory

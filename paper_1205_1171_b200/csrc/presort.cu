@@ -5,15 +5,18 @@
 //   _scan_degenerate                               pkg/src/hull3d/api.py:113-147
 //   orientation, remap, np.unique                  pkg/src/hull3d/api.py:252-266
 //
-// Sorting: stable LSD radix sort (CUB onesweep) of order-preserving u64 keys
+// Sorting: stable LSD radix sort (prims.cuh, hand-written onesweep) of
+// order-preserving u64 keys
 // of the fp64 coordinates with the row index as payload.  -0.0 is folded
 // onto +0.0 first so that the two compare equal, as they do under numpy's
 // comparisons.  Stability + index payload reproduces argsort(kind="stable")
 // and np.lexsort((z, y, x)) exactly (three stable passes z, y, x).
-#include <cub/cub.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "h3d_device.cuh"
 #include "h3d_host.h"
+#include "prims.cuh"
 
 namespace h3d {
 
@@ -681,19 +684,13 @@ struct PresortWS {
 
 constexpr int kColsumBlocks = 296;
 
+// temporary bytes of the device-wide primitives (prims.cuh) over n items
 size_t cub_bytes_for(long long n) {
-  size_t a = 0, b = 0, c = 0, d = 0;
-  cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
-  cub::DoubleBuffer<int> vb(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, static_cast<int>(n));
-  cub::DeviceScan::InclusiveScan(nullptr, b, static_cast<long long *>(nullptr),
-                                 static_cast<long long *>(nullptr), cub::Max(),
-                                 static_cast<int>(n));
-  cub::DeviceSelect::Flagged(nullptr, c, cub::CountingInputIterator<long long>(0),
-                             static_cast<int *>(nullptr), static_cast<long long *>(nullptr),
-                             static_cast<long long *>(nullptr), static_cast<int>(n));
-  (void)d;
-  size_t m = a > b ? a : b;
+  size_t m = prim::rs_temp_bytes<unsigned long long>(n);
+  const size_t a = prim::rs_temp_bytes<unsigned>(n), b = prim::scan_temp_bytes<long long>(n),
+               c = prim::select_temp_bytes(n);
+  if (a > m) m = a;
+  if (b > m) m = b;
   return m > c ? m : c;
 }
 
@@ -719,14 +716,13 @@ bool carve(h3d_arena &ar, long long n, PresortWS &w) {
 // stable sort of (keys, vals) pairs; result in (*ko, *vo)
 bool radix(PresortWS &w, unsigned long long *kin, int *vin, unsigned long long *kalt, int *valt,
            long long n, unsigned long long **ko, int **vo, cudaStream_t s) {
-  cub::DoubleBuffer<unsigned long long> kb(kin, kalt);
-  cub::DoubleBuffer<int> vb(vin, valt);
-  size_t bytes = w.cub_bytes;
-  if (h3d_check(cub::DeviceRadixSort::SortPairs(w.cub_tmp, bytes, kb, vb, static_cast<int>(n),
-                                                0, 64, s)))
+  bool alt = false;
+  h3d_count_launches(9);
+  if (h3d_check(prim::rs_sort_pairs<unsigned long long>(w.cub_tmp, w.cub_bytes, kin, vin, kalt, valt, n, 0,
+                                                        64, &alt, s)))
     return false;
-  *ko = kb.Current();
-  *vo = vb.Current();
+  *ko = alt ? kalt : kin;
+  *vo = alt ? valt : vin;
   return true;
 }
 
@@ -788,16 +784,16 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   k_scan_input<<<G > 1184 ? 1184 : G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
   // stable argsort of x (api.py:97): 32-bit fixed-point keys + tie-run fix
   unsigned *k32a = reinterpret_cast<unsigned *>(w.k0), *k32b = reinterpret_cast<unsigned *>(w.k1);
-  k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, w.v0);
+  k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, nullptr);
   {
-    cub::DoubleBuffer<unsigned> kb(k32a, k32b);
-    cub::DoubleBuffer<int> vb(w.v0, w.v1);
-    size_t bytes = w.cub_bytes;
-    if (h3d_check(cub::DeviceRadixSort::SortPairs(w.cub_tmp, bytes, kb, vb, static_cast<int>(n),
-                                                  0, 32, s)))
+    // values = the row positions, generated by the first digit pass
+    bool alt = false;
+    h3d_count_launches(5);
+    if (h3d_check(prim::rs_sort_pairs<unsigned>(w.cub_tmp, w.cub_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32,
+                                                &alt, s, true)))
       return H3D_E_CUDA;
-    vs = vb.Current();
-    k_tiefix<<<G, 256, 0, s>>>(pts, kb.Current(), vs, n, w.flag + 2);
+    vs = alt ? w.v1 : w.v0;
+    k_tiefix<<<G, 256, 0, s>>>(pts, alt ? k32b : k32a, vs, n, w.flag + 2);
   }
   // rows in x order, with the adjacent-tie test folded in (rare ties:
   // the rows are rebuilt by the lexsort/perturbation path below)
@@ -845,9 +841,9 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     // perturb_ties: run heads by max-scan, then base + rank*step
     h3d_count_launches(1);
     k_run_heads<<<G, 256, 0, s>>>(w.work, n, w.head);
-    size_t bytes = w.cub_bytes;
-    if (h3d_check(cub::DeviceScan::InclusiveScan(w.cub_tmp, bytes, w.head, w.head, cub::Max(),
-                                                 static_cast<int>(n), s)))
+    h3d_count_launches(3);
+    if (h3d_check(prim::scan<false, long long>(w.cub_tmp, w.cub_bytes, w.head, w.head, n, prim::OpMax(),
+                                               -1ll, -1ll, s)))
       return H3D_E_CUDA;
     h3d_count_launches(1);
     k_perturb<<<G, 256, 0, s>>>(w.work, w.head, n);
@@ -921,15 +917,16 @@ int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1, i
   k_sel_runs<<<1, 256, 0, s>>>(pts, k32, st, runs, idx);
   const unsigned Gm = h3d_grid(m, 256) > 4096 ? 4096 : h3d_grid(m, 256);
   k_sel_keys<<<Gm, 256, 0, s>>>(k32, st, idx, lk, m);
-  cub::DoubleBuffer<unsigned> kb(lk, lk_alt);
-  cub::DoubleBuffer<int> vb(idx, idx_alt);
-  size_t bytes = w.cub_bytes;
-  if (h3d_check(cub::DeviceRadixSort::SortPairs(w.cub_tmp, bytes, kb, vb, static_cast<int>(m), 0,
-                                                32, s)))
+  bool alt = false;
+  h3d_count_launches(5);
+  if (h3d_check(prim::rs_sort_pairs<unsigned>(w.cub_tmp, w.cub_bytes, lk, idx, lk_alt, idx_alt, m, 0, 32,
+                                              &alt, s)))
     return H3D_E_CUDA;
+  unsigned *kcur = alt ? lk_alt : lk;
+  int *vcur = alt ? idx_alt : idx;
   h3d_count_launches(2);
-  k_tiefix<<<Gm, 256, 0, s>>>(pts, kb.Current(), vb.Current(), m, w.flag + 2);
-  k_gather_rows<<<Gm, 256, 0, s>>>(pts, vb.Current(), m, sorted_pts + 3 * q0,
+  k_tiefix<<<Gm, 256, 0, s>>>(pts, kcur, vcur, m, w.flag + 2);
+  k_gather_rows<<<Gm, 256, 0, s>>>(pts, vcur, m, sorted_pts + 3 * q0,
                                    reinterpret_cast<long long *>(order) + q0, nullptr, w.flag);
   int hflag[3] = {0, 0, 0};
   SelState hst;
@@ -970,10 +967,9 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n, const int64_t *
   k_orient<<<G, 256, 0, s>>>(sorted_pts, w.centroid, reinterpret_cast<const long long *>(order),
                              faces_raw, nfaces, reinterpret_cast<long long *>(faces),
                              vertex_mark);
-  size_t bytes = w.cub_bytes;
-  if (h3d_check(cub::DeviceSelect::Flagged(w.cub_tmp, bytes, cub::CountingInputIterator<long long>(0),
-                                           vertex_mark, reinterpret_cast<long long *>(vertices),
-                                           w.count, static_cast<int>(n), s)))
+  h3d_count_launches(3);
+  if (h3d_check(prim::select_flagged(w.cub_tmp, w.cub_bytes, vertex_mark, n,
+                                     reinterpret_cast<long long *>(vertices), w.count, s)))
     return H3D_E_CUDA;
   long long cnt = 0;
   if (h3d_check(cudaMemcpyAsync(&cnt, w.count, sizeof(cnt), cudaMemcpyDeviceToHost, s)) ||

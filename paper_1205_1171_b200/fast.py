@@ -21,6 +21,28 @@ from . import _lib
 from .engine import stream_ptr
 
 E_FASTPATH = -13
+E_VERIFY = -14
+
+# verify mode (tests): every level's groups are checked on the device
+# (csrc/fast.cu k_verify_level); a violation raises VerifyError
+VERIFY = [0]
+
+
+class VerifyError(AssertionError):
+    """A level of the fast path wrote a group that fails the device checks."""
+
+
+class verifying:
+    """Context manager: run the fast path in verify mode."""
+
+    def __enter__(self):
+        self.old = VERIFY[0]
+        VERIFY[0] = 1
+        return self
+
+    def __exit__(self, *exc):
+        VERIFY[0] = self.old
+        return False
 
 # how many pass pairs the exact engine had to redo (tests assert 0 on
 # general-position inputs: the fast path must be the one that runs)
@@ -119,7 +141,7 @@ def run_both(sorted_pts: torch.Tensor):
     counts = state[1:3]
     fin = (ctypes.c_int64 * 2)()
     r = L.h3d_fast_passes(sorted_pts.data_ptr(), n, ws_lo.data_ptr(), ws_up.data_ptr(), wsb,
-                          err.data_ptr(), 0, ctypes.addressof(fin), s)
+                          err.data_ptr(), 2 if VERIFY[0] else 0, ctypes.addressof(fin), s)
     if r < 0:
         from .errors import check_merge
 
@@ -134,6 +156,11 @@ def run_both(sorted_pts: torch.Tensor):
 
         check_merge(int(r))
     h = state.cpu()  # the one host sync of the pass pair
+    if int(h[0]) == E_VERIFY:
+        d = int(h[3]) & ((1 << 64) - 1)
+        raise VerifyError("fast path: a level wrote a group that fails the device checks "
+                          f"(check {d >> 60}, level {(d >> 54) & 63}, pass {(d >> 53) & 1}, "
+                          f"group {(d >> 20) & 0xffffffff}, item {d & 0xfffff})")
     if int(h[0]) != 0:
         FALLBACKS[0] += 1
         LAST_ERROR[0] = int(h[0])
@@ -142,4 +169,5 @@ def run_both(sorted_pts: torch.Tensor):
     return faces[: k_lo + k_up], k_lo, k_up
 
 
-__all__ = ["run_both", "profile_enable", "profile_collect", "E_FASTPATH", "ctypes"]
+__all__ = ["run_both", "profile_enable", "profile_collect", "E_FASTPATH", "E_VERIFY", "VERIFY",
+           "VerifyError", "verifying", "ctypes"]

@@ -25,7 +25,8 @@ def test_fast_vs_oracle(dist, n, oracle_mod):
     pts = generate(n, dist, n + 1)
     sp, order, _ = presort(torch.from_numpy(pts).cuda())
     before = fast.FALLBACKS[0]
-    res = fast.run_both(sp)
+    with fast.verifying():  # every level's groups checked on the device
+        res = fast.run_both(sp)
     assert res is not None, f"fast path fell back (err {fast.LAST_ERROR[0]})"
     raw, klo, kup = res
     exp = oracle_mod.convex_hull_3d(pts)

@@ -4,7 +4,8 @@ for bit with no exact-engine fallback:
 
 * leaf kernel depth 0 / 3 / 4 (levels 1..B fused in shared memory);
 * the time-split pipeline (big.cu) on almost every level (big_kin=16);
-* lane-per-job on every level (tpj_min_jobs=1, pipeline off);
+* lane-per-job on every level (tpj_min_jobs=1, pipeline off), on k_fast_tpj
+  and on lane.cu (coordinates / merged events staged in shared memory or not);
 * warp-per-job on every level (tpj_min_jobs huge, pipeline off);
 * each mini variant (one CTA per job in shared memory) wherever its jobs fit.
 """
@@ -30,7 +31,13 @@ ROUTES = {
     "mini_seg16": {"mini_seg": 16},
     "big_everywhere": {"big_kin": 16, "mini": 0},
     "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0, "mini": 0},
-    "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0},
+    "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0, "lane": 0},
+    "lane_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
+                        "lane_max_level": 40},
+    "lane_staged_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
+                               "lane_max_level": 40, "lane_xyz_kb": 200, "lane_stage": 1},
+    "lane_events_staged": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
+                           "lane_max_level": 40, "lane_stage": 1},
     "warp_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 0},
     "mini_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
                         "mini_ctas": BIG_OFF, "mini_tiny_ctas": 0},
