@@ -295,7 +295,8 @@ def level_bytes(cfg: str):
 
 # bench kernel names -> the ncu kernel names they cover
 NCU_NAMES = {
-    "k_fast_tpj": ("h3d::k_fast_tpj<",),
+    # the lane-per-job route: lane.cu (levels <= 5) and k_fast_tpj above
+    "k_fast_tpj": ("h3d::k_fast_tpj<", "h3d::k_lane<"),
     "k_fast_warp": ("h3d::k_fast_warp<",),
     "k_fast_leaf": ("h3d::k_fast_leaf<",),
     "k_fast_init1": ("h3d::k_fast_init1",),
@@ -357,10 +358,11 @@ def run_ours(args):
     nfaces = int(res.faces.shape[0])
     nverts = int(res.vertices.shape[0])
 
-    # device-resident timed region (+ per-launch kernel events)
+    # device-resident timed region: per-level times come from the level
+    # kernels' own device time stamps (no event records); CUDA events bracket
+    # only the lane-per-job kernel launches (the dominant kernel: roofline)
     prof: list = []
-    E.PROFILE = prof
-    E.PROFILE_DEFER = True
+    E.KERNEL_EVENTS = True
     F.profile_collect(1 << 20)  # drop the warm-up's records
     l0 = E.launch_count()
     clocks = ClockSampler(local)
@@ -377,17 +379,20 @@ def run_ours(args):
     for tag, p_idx, t_ms in F.profile_collect(1 << 20):
         name, lv = F.kernel_of(tag)
         prof.append((name, p_idx, lv, t_ms))
-    E.PROFILE = None
-    E.PROFILE_DEFER = False
+    E.KERNEL_EVENTS = False
     launches = (E.launch_count() - l0) // args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     value = n / (ms / 1e3)
     fallbacks = F.FALLBACKS[0] - fb0
-    # which kernels ran, per step (route evidence: fused fast path vs exact)
+    # which route each level took in the last timed step (fused fast path
+    # vs exact engine), from the device level stamps
     routes: dict = {}
-    for name, _p, _lv, _t in prof:
+    level_ms: dict = {}
+    for tag, _p, t_ms in F.LAST_LEVEL_ROWS:
+        name, lv = F.kernel_of(tag)
         routes[name] = routes.get(name, 0) + 1
-    routes = {k: v / args.steps for k, v in sorted(routes.items())}
+        level_ms[str(lv)] = round(t_ms, 4)
+    routes = dict(sorted(routes.items()))
 
     # roofline of the dominant kernel
     per_kernel: dict = {}
@@ -409,7 +414,8 @@ def run_ours(args):
         ach = d["bytes"] / d["time"] / 1e9 if d["known"] and d["time"] > 0 else None
         nl = max(d["launches"], 1)
         traffic, tsrc = measured_traffic(args.config, name)
-        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+        label = "lane-per-job (k_lane, k_fast_tpj)" if name == "k_fast_tpj" else name
+        roof = {"bound": "hbm", "kernel": label, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None,
                 "traffic": traffic,
                 "traffic_source": tsrc,
@@ -456,6 +462,7 @@ def run_ours(args):
                    "faces": nfaces, "vertices": nverts},
         "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
         "clocks": clk, "fallbacks": fallbacks, "routes_per_step": routes,
+        "level_ms_last_step": level_ms,
     }
     print(json.dumps(line), flush=True)
 

@@ -62,12 +62,23 @@ const char *h3d_impl(void);
 const char *h3d_last_error(void);
 /* number of this library's own kernel launches so far (process-wide) */
 int64_t h3d_launch_count(void);
-/* per-level profile of the CALLING THREAD: when enabled (per thread), every
- * merge level of h3d_fast_passes* run by this thread is bracketed by CUDA
- * events on its stream (events pooled per device); collect returns this
- * thread's (level, pass, milliseconds) rows, waiting only for its own last
- * event, and clears them */
+/* per-level profile of the CALLING THREAD: when enabled (per thread; on = 1),
+ * every merge level of h3d_fast_passes* run by this thread is bracketed by
+ * CUDA events on its stream (events pooled per device); on = 2 brackets only
+ * the lane-per-job kernel launches themselves (the dominant kernel's
+ * duration for bench.py's roofline); collect returns this thread's (level,
+ * pass, milliseconds) rows, waiting only for its own last event, and clears
+ * them */
 void h3d_profile_enable(int32_t on);
+/* per-level DEVICE time stamps for the calling thread's next
+ * h3d_fast_passes* calls: dev_buf = 64 device int64 (or NULL = off).  The
+ * level kernels write %globaltimer (ns) at the start of level l into slot l
+ * and the end of the last level into slot 40 -- no event records, no host
+ * work (HullStats' per-level seconds, api.py:28-44).  routes: the route tag
+ * of each stamped slot (1000+l lane-per-job, 3000+B fused leaf levels 1..B,
+ * 4000+l time-split pipeline, 5000+l one CTA per job, l warp per job, -1 none). */
+void h3d_profile_stamps(int64_t *dev_buf);
+int64_t h3d_profile_routes(int32_t *routes, int64_t max);
 int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms,
                             int64_t max);
 

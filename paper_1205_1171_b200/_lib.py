@@ -28,6 +28,8 @@ SIGNATURES: dict[str, tuple] = {
     "h3d_launch_count": (i64, []),
     "h3d_profile_enable": (None, [ctypes.c_int32]),
     "h3d_profile_collect": (i64, [vp, vp, vp, i64]),
+    "h3d_profile_stamps": (None, [vp]),
+    "h3d_profile_routes": (i64, [vp, i64]),
     "h3d_fast_pass_workspace_bytes": (sz, [i64]),
     "h3d_fast_passes": (i64, [vp, i64, vp, vp, sz, vp, ctypes.c_int32, vp, vp]),
     "h3d_fast_passes_range": (i64, [vp, i64, i64, i64, ctypes.c_int32, ctypes.c_int32, vp, vp,

@@ -207,44 +207,54 @@ def _level_rows_to_stats(rows, n, level_lists):
     return ms
 
 
-def _run_passes(sorted_pts, engine, solver, level_lists, profile: bool):
+def _run_passes(sorted_pts, engine, solver, level_lists):
     """Both passes; returns (raw faces int32 (F,3) on device, lower count,
-    upper count, lower ms, upper ms, finish).  With ``profile`` every level is
-    bracketed by device events (no synchronisation here): ``finish()`` --
-    called by the API after its one host synchronisation, so it never waits
-    -- turns them into per-level seconds (like the reference's perf_counter
-    deltas) and the two passes' shares of the time."""
+    upper count, finish).  Per-level times (solver="parallel") come from
+    device time stamps written by the level kernels themselves and read back
+    with the facet counts (no event records, no extra synchronisation);
+    ``finish()`` turns them into per-level seconds (like the reference's
+    perf_counter deltas) and the two passes' shares.  Tools
+    that set engine.PROFILE get per-level CUDA events instead; bench.py's
+    engine.KERNEL_EVENTS brackets only the lane-per-job kernel launches."""
     from . import engine as E
     from . import fast
 
     want_levels = solver == "parallel"
     if engine == "fast":
         t0 = time.perf_counter()
-        if profile:
-            fast.profile_enable(True)
+        ev_mode = 1 if E.PROFILE is not None else (2 if E.KERNEL_EVENTS else 0)
+        if ev_mode:
+            fast.profile_enable(ev_mode)
         try:
-            res = fast.run_both(sorted_pts)
+            res = fast.run_both(sorted_pts, stamps=want_levels and ev_mode != 1)
         finally:
-            if profile:
-                fast.profile_enable(False)
+            if ev_mode:
+                fast.profile_enable(0)
         if res is not None:
             dt = (time.perf_counter() - t0) * 1e3
             raw, k_lo, k_up = res
             split = [dt / 2, dt / 2]
+            rows = list(fast.LAST_LEVEL_ROWS) if want_levels and ev_mode != 1 else None
 
             def finish():
-                if not profile or E.PROFILE_DEFER:
-                    # deferred: the records stay with this thread until the
-                    # caller (bench.py) collects a whole timed loop at once
+                if ev_mode == 1:
+                    if E.PROFILE_DEFER:
+                        # deferred: the records stay with this thread until the
+                        # caller collects a whole timed loop at once
+                        return split
+                    lrows = fast.profile_collect()
+                else:
+                    lrows = rows
+                if not lrows:
                     return split
-                ms = _level_rows_to_stats(fast.profile_collect(), sorted_pts.shape[0],
+                ms = _level_rows_to_stats(lrows, sorted_pts.shape[0],
                                           level_lists if want_levels else None)
                 tot = ms[0] + ms[1]
                 lo = dt * ms[0] / tot if tot > 0 else dt / 2
                 return [lo, dt - lo]
 
             return raw, k_lo, k_up, finish
-        if profile:
+        if ev_mode:
             fast.profile_collect()  # drop the declined run's records
     out = []
     ms = []
@@ -256,12 +266,6 @@ def _run_passes(sorted_pts, engine, solver, level_lists, profile: bool):
         ms.append((time.perf_counter() - t0) * 1e3)
         out.append(raw)
     return torch.cat(out), out[0].shape[0], out[1].shape[0], (lambda: ms)
-
-
-# per-level device timing for device-resident results (return_device=True):
-# off unless asked for -- it would need a synchronisation the caller did not
-# request; host results get it for free after their one synchronisation
-LEVEL_TIMES_ON_DEVICE = os.environ.get("H3D_LEVEL_TIMES", "0") not in ("", "0")
 
 
 def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
@@ -304,10 +308,6 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
     # the per-device workspaces are shared: one hull at a time per device
     # (calls from several threads are serialised, not interleaved); every
     # launch goes to `dev` whatever the caller's current device is
-    from . import engine as E
-
-    profile = (solver == "parallel" and (not return_device or LEVEL_TIMES_ON_DEVICE)) \
-        or E.PROFILE is not None
     with _device_lock(dev), torch.cuda.device(dev):
         sort_t0 = time.perf_counter()
         sorted_pts, order, perturbed = presort(pts)
@@ -316,7 +316,7 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
         lower_levels: list[float] = []
         upper_levels: list[float] = []
         raw, k_lo, k_up, finish = _run_passes(sorted_pts, engine, solver,
-                                              (lower_levels, upper_levels), profile)
+                                              (lower_levels, upper_levels))
         verts, faces = orient_remap(sorted_pts, order, raw)
         if not return_device:
             verts, faces = to_host(verts), to_host(faces)

@@ -61,7 +61,37 @@ void ev_put(int dev, cudaEvent_t e) {
 }
 }  // namespace
 
-bool h3d_profiling() { return t_prof_on; }
+thread_local int t_prof_mode = 0;
+thread_local long long *t_stamps = nullptr;
+thread_local int t_routes[H3D_STAMPS];
+
+bool h3d_profiling() { return t_prof_mode == 1; }
+bool h3d_prof_kernels() { return t_prof_mode == 2; }
+long long *h3d_stamp_buf() { return t_stamps; }
+void h3d_stamp_route(int level, int tag) {
+  if (t_stamps && level >= 0 && level < H3D_STAMPS) t_routes[level] = tag;
+}
+
+__global__ void k_stamp(long long *buf, int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  buf[slot] = static_cast<long long>(t);
+}
+void h3d_stamp_now(cudaStream_t s, int slot) {
+  if (!t_stamps) return;
+  h3d_count_launches(1);
+  k_stamp<<<1, 1, 0, s>>>(t_stamps, slot);
+}
+
+extern "C" void h3d_profile_stamps(int64_t *dev_buf) {
+  t_stamps = reinterpret_cast<long long *>(dev_buf);
+  for (int &r : t_routes) r = -1;
+}
+extern "C" int64_t h3d_profile_routes(int32_t *out, int64_t max) {
+  int64_t m = 0;
+  for (; m < max && m < H3D_STAMPS; ++m) out[m] = t_routes[m];
+  return m;
+}
 
 void *h3d_prof_begin(cudaStream_t s) {
   int dev = 0;
@@ -86,7 +116,15 @@ void h3d_prof_end(void *e0, int level, int pass, cudaStream_t s) {
   t_prof.push_back({level, pass, dev, static_cast<cudaEvent_t>(e0), e1});
 }
 
-extern "C" void h3d_profile_enable(int32_t on) { t_prof_on = on != 0; }
+// an interval that turned out empty (the route declined): back to the pool
+void h3d_prof_drop(void *e0) {
+  if (e0) ev_put(t_prof_dev, static_cast<cudaEvent_t>(e0));
+}
+
+extern "C" void h3d_profile_enable(int32_t on) {
+  t_prof_on = on != 0;
+  t_prof_mode = on < 0 ? 0 : (on > 2 ? 1 : on);
+}
 
 extern "C" int64_t h3d_profile_collect(int32_t *level, int32_t *pass, float *ms, int64_t max) {
   int64_t m = 0;

@@ -288,11 +288,10 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
     if (kL > 0) cL = evL.get(0);
     if (kR > 0) cR = evR.get(0);
     if (EIN::kPrefetch) {  // HBM streams: one event of prefetch (packed)
-      nL = evL.raw(1);
-      nR = evR.raw(1);
+      if (kL > 0) nL = evL.raw(kL > 1 ? 1 : 0);
+      if (kR > 0) nR = evR.raw(kR > 1 ? 1 : 0);
     }
   }
-  (void)nL;
   long long k = 0;
   double tcur = -INF;
   // Branch-free step: all 32 lanes (32 different jobs) iterate together until
@@ -374,9 +373,9 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
       if (EIN::kPrefetch) {
         // unconditional load straight into the loop-carried register (a
         // predicated one compiles to a register move that waits for the
-        // load); slot i + 1 <= k of the child is inside its slot range
+        // load)
         cL = i < kL ? EIN::unpack(nL) : EIN::unpack(EIN::none());
-        nL = evL.raw(i + 1);
+        nL = evL.raw(min(i + 1, kL - 1));  // clamped: never reads a slot no level wrote
       } else {
         if (i < kL) cL = evL.get(i); else cL.t = INF;
       }
@@ -385,7 +384,7 @@ __device__ long long merge_tpj2(const SL &S, bool active, int u_init, int roff,
       ++j;
       if (EIN::kPrefetch) {
         cR = j < kR ? EIN::unpack(nR) : EIN::unpack(EIN::none());
-        nR = evR.raw(j + 1);
+        nR = evR.raw(min(j + 1, kR - 1));
       } else {
         if (j < kR) cR = evR.get(j); else cR.t = INF;
       }
@@ -452,7 +451,12 @@ __host__ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
 // merged child log of one job; out[9] = all merged child logs.  One warp per 32
 // jobs, coalesced header reads.
 __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long long j1,
-                           unsigned long long *out, const long long *err) {
+                           unsigned long long *out, const long long *err, long long *stamp) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *stamp = static_cast<long long>(t);
+  }
   // out[10] = the error word, read back with the measurement (one copy)
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
     out[10] = static_cast<unsigned long long>(*reinterpret_cast<const volatile long long *>(err));
@@ -1052,6 +1056,9 @@ __device__ long long merge_warp(Rec *R, int nSL, const Ev *seq, int kin, EvP *ou
   const unsigned ltmask = (1u << lane) - 1;
   int u = nSL - 1, v = nSL, st = 0;
   if (lane == 0) st = bridge_rec(R, &u, &v, limitRef);
+  // lane 0's walk reads R; the window retire below writes it (WAR across
+  // lanes): a memory barrier for the warp, not just the shuffle's rendezvous
+  __syncwarp();
   st = __shfl_sync(FULL, st, 0);
   if (st < 0) return H3D_E_BRIDGE;
   u = __shfl_sync(FULL, u, 0);
@@ -1689,6 +1696,8 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
   if (lv_lo == 1 && g_leaf_b >= 3 && lv_hi >= g_leaf_b && (p0 & (NPB - 1)) == 0) {
     // levels 1..B fused in shared memory, one lane per 2^B-point block
     const long long blocks = (p1 - p0 + NPB - 1) / NPB;
+    h3d_stamp_now(s, 1);
+    h3d_stamp_route(1, 3000 + g_leaf_b);
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
     h3d_count_launches(1);
     const dim3 grid(h3d_grid(blocks, 32), 2);
@@ -1704,6 +1713,8 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     lv = g_leaf_b + 1;
   } else if (lv_lo == 1) {  // level 1 written directly (no coordinates needed)
     const long long j0 = p0 >> 1, j1 = (p1 + 1) >> 1;
+    h3d_stamp_now(s, 1);
+    h3d_stamp_route(1, 2001);
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
     h3d_count_launches(1);
     const unsigned gi = h3d_grid(j1 - j0, 256) > 8192 ? 8192 : h3d_grid(j1 - j0, 256);
@@ -1728,7 +1739,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
     k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 2 * 148 ? 2 * 148 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
-        P, n, lv, j0, j1, w0.need, err);
+        P, n, lv, j0, j1, w0.need, err, h3d_stamp_buf() ? h3d_stamp_buf() + lv : nullptr);
     unsigned long long need[40];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(cudaStreamSynchronize(s)))
@@ -1757,6 +1768,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, 2);
       if (rm < 0) return rm;
       h3d_prof_end(e0, lv + 5000, 2, s);
+      h3d_stamp_route(lv, lv + 5000);
       P = Pass2{P.out0, P.out1, P.in0, P.in1};
       continue;
     }
@@ -1767,6 +1779,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, mini_small ? 0 : 1);
       if (rm < 0) return rm;
       h3d_prof_end(e0, lv + 5000, 2, s);
+      h3d_stamp_route(lv, lv + 5000);
       P = Pass2{P.out0, P.out1, P.in0, P.in1};
       if (g_mini_spec && !mini_small && lv < lv_hi) {
         // the remaining levels have at most half these jobs: launch them all
@@ -1778,7 +1791,8 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         for (int l2 = lv + 1; l2 <= lv_hi; ++l2) {
           void *e2 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
           const long long rs = mini_level(P, sorted_pts, n, l2, p0 >> l2,
-                                          (p1 + (1ll << l2) - 1) >> l2, err, s, 1, spec);
+                                          (p1 + (1ll << l2) - 1) >> l2, err, s, 1, spec,
+                                          h3d_stamp_buf() ? h3d_stamp_buf() + l2 : nullptr);
           if (rs < 0) return rs;
           if (g_trace) {
             long long f = 0;
@@ -1788,6 +1802,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
                     cudaGetErrorString(ce));
           }
           h3d_prof_end(e2, l2 + 5000, 2, s);
+          h3d_stamp_route(l2, l2 + 5000);
           P = Pass2{P.out0, P.out1, P.in0, P.in1};
           check(P, l2, spec);
         }
@@ -1824,6 +1839,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       if (rb < 0) return rb;
       if (rb == 0) {
         h3d_prof_end(e0, lv + 4000, 2, s);
+      h3d_stamp_route(lv, lv + 4000);
         P = Pass2{P.out0, P.out1, P.in0, P.in1};
         continue;
       }
@@ -1849,10 +1865,13 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       }
     }
     if (tpj && g_lane && lv <= g_lane_max_level) {
+      void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
       const long long rl = lane_level(P, sorted_pts, n, lv, j0, j1, err, need, s);
       if (rl < 0) return rl;
+      if (rl == 0) h3d_prof_end(ek, lv + 1000, 2, s); else h3d_prof_drop(ek);
       if (rl == 0) {
         h3d_prof_end(e0, lv + 1000, 2, s);
+      h3d_stamp_route(lv, lv + 1000);
         P = Pass2{P.out0, P.out1, P.in0, P.in1};
         continue;
       }
@@ -1860,13 +1879,16 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     }
     if (tpj) {
       h3d_count_launches(1);
+      void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
       const dim3 grid(h3d_grid(jobs, jpc), 2);
       if (xyz)
         launch_tpj<true>(grid, static_cast<int>(pool), jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err);
       else
         launch_tpj<false>(grid, static_cast<int>(pool), jpc, jobs >= kTpjPrefetchJobs ? 1 : 0, s, P,
                           sorted_pts, n, lv, j0, j1, err);
+      h3d_prof_end(ek, lv + 1000, 2, s);
       h3d_prof_end(e0, lv + 1000, 2, s);
+      h3d_stamp_route(lv, lv + 1000);
     } else {
       long long wpool = static_cast<long long>(need[7]);
       if (wpool > kWarpPoolMax) wpool = kWarpPoolMax;
@@ -1876,10 +1898,12 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           P, sorted_pts, n, lv, j0, j1, err, static_cast<int>(wpool), w0.seq, w1.seq, w0.rec,
           w1.rec);
       h3d_prof_end(e0, lv, 2, s);
+      h3d_stamp_route(lv, lv);
     }
     P = Pass2{P.out0, P.out1, P.in0, P.in1};
   }
   if (lv > lv_hi && lv - 1 >= lv_lo) check(P, lv - 1);  // the last level (when the loop ran it)
+  h3d_stamp_now(s, H3D_STAMP_END);
   if (h3d_check(cudaGetLastError())) return H3D_E_CUDA;
   return lv_hi & 1;  // buffer holding the last level's groups
 }

@@ -229,7 +229,7 @@ extern int g_lane_stage;
 
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant,
-                     long long *spec = nullptr);
+                     long long *spec = nullptr, long long *stamp = nullptr);
 constexpr int kMiniMaxPoints = 1024, kMiniMaxEvents = 2048;
 constexpr int kMiniSmallPoints = 256, kMiniSmallEvents = 512;
 constexpr int kMiniTinyPoints = 192, kMiniTinyEvents = 320;

@@ -9,10 +9,25 @@
 bool h3d_check(cudaError_t e);
 // counts this library's own kernel launches (bench.py reports gpu_launches)
 void h3d_count_launches(int k);
-// per-level CUDA-event profile (h3d_profile_enable); no-ops when disabled
+// per-level CUDA-event profile (h3d_profile_enable); no-ops when disabled.
+// Mode 1: every level bracketed (measurement + routing + kernels); mode 2:
+// only the lane-per-job kernel launches (h3d_prof_kernels()), for bench.py's
+// roofline of the dominant kernel.
 bool h3d_profiling();
+bool h3d_prof_kernels();
 void *h3d_prof_begin(cudaStream_t s);
 void h3d_prof_end(void *e0, int level, int pass, cudaStream_t s);
+void h3d_prof_drop(void *e0);
+// per-level DEVICE time stamps (h3d_profile_stamps): the calling thread's
+// device buffer of H3D_STAMPS int64 (ns, %globaltimer) or nullptr; slot l =
+// start of level l's work, slot H3D_STAMP_END = end of the last level.  The
+// level kernels write them (no host work, no event records); the route of
+// each level is kept host-side (h3d_stamp_route).
+constexpr int H3D_STAMPS = 64;
+constexpr int H3D_STAMP_END = 40;
+long long *h3d_stamp_buf();
+void h3d_stamp_route(int level, int tag);
+void h3d_stamp_now(cudaStream_t s, int slot);  // one tiny kernel
 
 inline unsigned h3d_grid(long long work, int block) {
   long long g = (work + block - 1) / block;

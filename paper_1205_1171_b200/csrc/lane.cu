@@ -160,9 +160,10 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
   if (active) {
     if (kL > 0) hL = evL[0];
     if (kR > 0) hR = evR[0];
-    // slot 1 (and later slot i + 1 <= k) is inside the child's slot range
-    nL = ld_ev(evL + 1);
-    nR = ld_ev(evR + 1);
+    // the prefetch index is clamped to the log (k - 1): reading the stale
+    // slot k would be harmless but reads memory no level wrote (initcheck)
+    if (kL > 0) nL = ld_ev(evL + (kL > 1 ? 1 : 0));
+    if (kR > 0) nR = ld_ev(evR + (kR > 1 ? 1 : 0));
   }
   int i = 0, j = 0, k = 0;
   double tcur = -INF;
@@ -253,11 +254,11 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
         if (left) {
           ++i;
           hL = i < kL ? nL : ev_inf();
-          nL = ld_ev(evL + i + 1);
+          nL = ld_ev(evL + min(i + 1, kL - 1));
         } else {
           ++j;
           hR = j < kR ? nR : ev_inf();
-          nR = ld_ev(evR + j + 1);
+          nR = ld_ev(evR + min(j + 1, kR - 1));
         }
       }
     } else if (active) {

@@ -226,7 +226,13 @@ __device__ bool mini_sweep(MS &m, bool active, int s, int nseg, int seg, int kin
 template <int MINI_T, int MINI_K, int MINI_N>
 __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int lv, long long j0, long long j1,
-                                                 long long *err, int seglen, long long *spec) {
+                                                 long long *err, int seglen, long long *spec,
+                                                 long long *stamp) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *stamp = static_cast<long long>(t);
+  }
   typedef MiniSmem<MINI_T, MINI_K, MINI_N> MS;
   constexpr int MINI_B = MS::MINI_B;
   constexpr int PER = (MINI_K + MINI_T) / MINI_T;  // blocked-scan items per thread
@@ -651,7 +657,8 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
 
 template <int T, int K, int N>
 static long long launch_mini(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
-                             long long j1, long long *err, cudaStream_t s, long long *spec) {
+                             long long j1, long long *err, cudaStream_t s, long long *spec,
+                             long long *stamp) {
   static bool attr[64] = {};  // the attribute is per device
   int dev_id = 0;
   cudaGetDevice(&dev_id);
@@ -665,17 +672,18 @@ static long long launch_mini(const Pass2 &P, const double *pts, long long n, int
   }
   h3d_count_launches(1);
   k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, bytes, s>>>(P, pts, n, lv, j0, j1,
-                                                                          err, g_mini_seglen, spec);
+                                                                          err, g_mini_seglen, spec, stamp);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
 
 int g_mini_seglen = 3;  // child events per time segment (H3D_MINI_SEG / h3d_tune)
 
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
-                     long long j1, long long *err, cudaStream_t s, int variant, long long *spec) {
-  if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s, spec);
-  if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s, spec);
-  return launch_mini<1024, 2048, 1024>(P, pts, n, lv, j0, j1, err, s, spec);
+                     long long j1, long long *err, cudaStream_t s, int variant, long long *spec,
+                     long long *stamp) {
+  if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
+  if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
+  return launch_mini<1024, 2048, 1024>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
 }
 
 }  // namespace h3d

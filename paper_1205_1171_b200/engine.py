@@ -33,6 +33,9 @@ PROFILE: list | None = None
 # thread instead of collecting them per call (one collection per timed loop,
 # no per-call synchronisation inside the timed region)
 PROFILE_DEFER = False
+# bench.py: CUDA events around the lane-per-job kernel launches only (the
+# dominant kernel's duration for the roofline), collected by the caller
+KERNEL_EVENTS = False
 
 
 def level_count(n: int) -> int:

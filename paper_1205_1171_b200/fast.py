@@ -125,10 +125,30 @@ def profile_collect(max_rows: int = 4096):
     return [(int(lv[i]), int(ps[i]), float(ms[i])) for i in range(m)]
 
 
-def run_both(sorted_pts: torch.Tensor):
+STAMP_SLOTS = 64
+STAMP_END = 40
+# the level rows (tag, pass, ms) of the last run_both(stamps=True) of this
+# thread's caller: device time stamps, no event records (csrc/common.cu)
+LAST_LEVEL_ROWS: list = []
+
+
+def stamp_rows(stamps, routes) -> list:
+    """Device level stamps (ns) + host route tags -> [(tag, 2, ms)]: each
+    stamped level lasts until the next stamped one (the last until the end
+    stamp); 2 = one launch covering both passes."""
+    slots = [lv for lv in range(1, STAMP_END) if routes[lv] >= 0 and stamps[lv] > 0]
+    rows = []
+    for i, lv in enumerate(slots):
+        t1 = stamps[slots[i + 1]] if i + 1 < len(slots) else stamps[STAMP_END]
+        rows.append((int(routes[lv]), 2, max(0.0, (int(t1) - int(stamps[lv])) / 1e6)))
+    return rows
+
+
+def run_both(sorted_pts: torch.Tensor, stamps: bool = False):
     """Both passes + facet extraction.  Returns (raw faces int32 (F,3) on
     device, lower count, upper count) or None when the exact engine must
-    take over."""
+    take over.  stamps: record per-level device time stamps (read back with
+    the counts in the one synchronisation) into LAST_LEVEL_ROWS."""
     L = _lib.load()
     n = sorted_pts.shape[0]
     dev = sorted_pts.device
@@ -136,12 +156,21 @@ def run_both(sorted_pts: torch.Tensor):
     wsb = int(L.h3d_fast_pass_workspace_bytes(n))
     ws_lo = _WS.get(dev, 0, wsb)
     ws_up = _WS.get(dev, 1, wsb)
-    state = torch.zeros(4, dtype=torch.int64, device=dev)  # err, kLo, kUp, pad
+    # err, kLo, kUp, verify diagnostics, then the level stamps
+    state = torch.zeros(4 + (STAMP_SLOTS if stamps else 0), dtype=torch.int64, device=dev)
     err = state[0:1]
     counts = state[1:3]
     fin = (ctypes.c_int64 * 2)()
-    r = L.h3d_fast_passes(sorted_pts.data_ptr(), n, ws_lo.data_ptr(), ws_up.data_ptr(), wsb,
-                          err.data_ptr(), 2 if VERIFY[0] else 0, ctypes.addressof(fin), s)
+    if stamps:
+        L.h3d_profile_stamps(state[4:].data_ptr())
+    try:
+        r = L.h3d_fast_passes(sorted_pts.data_ptr(), n, ws_lo.data_ptr(), ws_up.data_ptr(), wsb,
+                              err.data_ptr(), 2 if VERIFY[0] else 0, ctypes.addressof(fin), s)
+    finally:
+        if stamps:
+            routes = np.zeros(STAMP_SLOTS, dtype=np.int32)
+            L.h3d_profile_routes(routes.ctypes.data, STAMP_SLOTS)
+            L.h3d_profile_stamps(None)
     if r < 0:
         from .errors import check_merge
 
@@ -166,6 +195,8 @@ def run_both(sorted_pts: torch.Tensor):
         LAST_ERROR[0] = int(h[0])
         return None
     k_lo, k_up = int(h[1]), int(h[2])
+    if stamps:
+        LAST_LEVEL_ROWS[:] = stamp_rows(h[4:].numpy(), routes)
     return faces[: k_lo + k_up], k_lo, k_up
 
 
