@@ -1545,6 +1545,10 @@ long long kMiniMaxCtas = 2 * 148;  // H3D_MINI_CTAS
 // least kMiniTinyKin events (the lane kernel's serial path then dominates)
 long long kMiniTinyCtas = 16384;  // H3D_MINI_TINY_CTAS
 long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
+// the huge mini variant (global-memory slots): at most this many CTAs, and
+// only from this merged child log size (below it the shared-memory ones)
+long long kMiniHugeCtas = 296;   // H3D_MINI_HUGE_CTAS
+long long kMiniHugeKin = 1000;   // H3D_MINI_HUGE_KIN
 // after a level on the large mini variant, launch the remaining levels on it
 // without measuring them (no read-back and host sync per level)
 int g_mini_spec = 1;  // H3D_MINI_SPEC
@@ -1574,6 +1578,8 @@ void load_env_once() {
   if (const char *e = getenv("H3D_MINI_CTAS")) kMiniMaxCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_CTAS")) kMiniTinyCtas = atoll(e);
   if (const char *e = getenv("H3D_MINI_TINY_KIN")) kMiniTinyKin = atoll(e);
+  if (const char *e = getenv("H3D_MINI_HUGE_CTAS")) kMiniHugeCtas = atoll(e);
+  if (const char *e = getenv("H3D_MINI_HUGE_KIN")) kMiniHugeKin = atoll(e);
   if (const char *e = getenv("H3D_MINI_SEG")) g_mini_seglen = atoi(e) < 1 ? 1 : atoi(e);
   if (const char *e = getenv("H3D_MINI_SPEC")) g_mini_spec = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_TRACE")) g_trace = atoi(e);
@@ -1606,6 +1612,8 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "mini_ctas") { old = kMiniMaxCtas; if (value >= 0) kMiniMaxCtas = value; }
   else if (k == "mini_tiny_ctas") { old = kMiniTinyCtas; if (value >= 0) kMiniTinyCtas = value; }
   else if (k == "mini_tiny_kin") { old = kMiniTinyKin; if (value >= 0) kMiniTinyKin = value; }
+  else if (k == "mini_huge_ctas") { old = kMiniHugeCtas; if (value >= 0) kMiniHugeCtas = value; }
+  else if (k == "mini_huge_kin") { old = kMiniHugeKin; if (value >= 0) kMiniHugeKin = value; }
   else if (k == "mini_seg") { old = g_mini_seglen; if (value >= 1) g_mini_seglen = static_cast<int>(value); }
   else if (k == "mini_spec") { old = g_mini_spec; if (value >= 0) g_mini_spec = value ? 1 : 0; }
   else if (k == "big_total") { old = kBigTotal; if (value >= 0) kBigTotal = value; }
@@ -1828,6 +1836,21 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         lv = f - 1;
       }
       continue;
+    }
+    // few large jobs (the top levels of ball clouds, the mid levels of
+    // spheres): one CTA per job with its arrays in global memory (L1/L2)
+    if (g_mini && big_ws && 2 * jobs <= kMiniHugeCtas &&
+        static_cast<long long>(need[6]) <= kMiniHugePoints && maxkin <= kMiniHugeEvents &&
+        maxkin >= kMiniHugeKin) {
+      const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, 3, nullptr, nullptr,
+                                      big_ws, big_bytes);
+      if (rm < 0) return rm;
+      if (rm == 0) {
+        h3d_prof_end(e0, lv + 5000, 2, s);
+        h3d_stamp_route(lv, lv + 5000);
+        P = Pass2{P.out0, P.out1, P.in0, P.in1};
+        continue;
+      }
     }
     // large merge jobs: the time-split pipeline (big.cu)
     // (its fixed cost, ~25 launches, only pays when the level has work)

@@ -227,10 +227,14 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
 extern long long g_lane_xyz_max;  // lane.cu knobs
 extern int g_lane_stage;
 
+// variant 3 (huge): <= kMiniHugePoints / kMiniHugeEvents per job, the job's
+// arrays in global-memory slots of gscratch (returns 1 when they do not fit)
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant,
-                     long long *spec = nullptr, long long *stamp = nullptr);
+                     long long *spec = nullptr, long long *stamp = nullptr,
+                     void *gscratch = nullptr, size_t gbytes = 0);
 constexpr int kMiniMaxPoints = 1024, kMiniMaxEvents = 2048;
+constexpr int kMiniHugePoints = 8192, kMiniHugeEvents = 16384;
 constexpr int kMiniSmallPoints = 256, kMiniSmallEvents = 512;
 constexpr int kMiniTinyPoints = 192, kMiniTinyEvents = 320;
 extern int g_mini_seglen;  // mini.cu: child events per time segment

@@ -11,6 +11,8 @@
 // classification of every child event by the bridge at its time, and the
 // start-of-time link rebuild + compaction -- with shared-memory latencies
 // instead of HBM ones, and one launch per level.
+#include <type_traits>
+
 #include <cub/cub.cuh>
 
 #include "fast.cuh"
@@ -31,11 +33,29 @@ constexpr int MINI_NIL = -1;
 
 // MINI_T threads per CTA (one job), MINI_K largest merged child log,
 // MINI_N largest job (points), MINI_B largest number of bridge events
+// facet words: a | b << S | c << 2S | kind << 3S | side << 3S+1, with
+// S = 10 in 32-bit words (jobs of <= 1024 points) and S = 16 in 64-bit words
+// (the huge variant in global memory)
+template <int MINI_N>
+using MiniWord = typename std::conditional<(MINI_N <= 1024), unsigned, unsigned long long>::type;
+
+template <class W>
+__device__ __forceinline__ constexpr int wsh() {
+  return sizeof(W) == 4 ? 10 : 16;
+}
+template <class W>
+__device__ __forceinline__ W wpack(int a, int b, int c, int kind, int side) {
+  constexpr int S = wsh<W>();
+  return static_cast<W>(a) | (static_cast<W>(b) << S) | (static_cast<W>(c) << (2 * S)) |
+         (static_cast<W>(kind & 1) << (3 * S)) | (static_cast<W>(side & 1) << (3 * S + 1));
+}
+
 template <int MINI_T, int MINI_K, int MINI_N>
 struct MiniSmem {
   static constexpr int MINI_B = MINI_K;
+  using W = MiniWord<MINI_N>;
   double st[MINI_K];            // S: event times
-  unsigned sw[MINI_K];          // S: a | b << 10 | c << 20 | kind << 30 | side << 31
+  W sw[MINI_K];                 // S: facet words (a, b, c, kind, side)
   double X[MINI_N], Y[MINI_N], Z[MINI_N];
   int G[MINI_N];                // gid
   short2 LN[MINI_N];            // links at t = -inf (job-local)
@@ -48,22 +68,36 @@ struct MiniSmem {
   int cpos[MINI_K + 1];         // kept child events: flags, then exclusive scan
   int nid[MINI_N + 1];          // keep flags, then new ids (exclusive scan)
   double bt[MINI_B];            // bridge events: time
-  unsigned bw[MINI_B];          //   facet a | b << 10 | c << 20 | kind << 30
+  W bw[MINI_B];                 //   facet word (side 0)
   short2 buv[MINI_B];           //   feet after
   double slt[MINI_B];           // per-segment slabs of the sweep (then compacted)
-  unsigned slw[MINI_B];
+  W slw[MINI_B];
   short2 sluv[MINI_B];
   short2 sst[MINI_S];           // segment start bridges
   int sbn[MINI_S + 1];          // bridge events per segment, then offsets
   int flag, nb;
-  typename cub::BlockScan<int, MINI_T>::TempStorage scan;
 };
 
-__device__ __forceinline__ int swa(unsigned w) { return static_cast<int>(w & 1023u); }
-__device__ __forceinline__ int swb(unsigned w) { return static_cast<int>((w >> 10) & 1023u); }
-__device__ __forceinline__ int swc(unsigned w) { return static_cast<int>((w >> 20) & 1023u); }
-__device__ __forceinline__ int swk(unsigned w) { return static_cast<int>((w >> 30) & 1u); }
-__device__ __forceinline__ int sws(unsigned w) { return static_cast<int>(w >> 31); }
+template <class W>
+__device__ __forceinline__ int swa(W w) {
+  return static_cast<int>(w & ((W(1) << wsh<W>()) - 1));
+}
+template <class W>
+__device__ __forceinline__ int swb(W w) {
+  return static_cast<int>((w >> wsh<W>()) & ((W(1) << wsh<W>()) - 1));
+}
+template <class W>
+__device__ __forceinline__ int swc(W w) {
+  return static_cast<int>((w >> (2 * wsh<W>())) & ((W(1) << wsh<W>()) - 1));
+}
+template <class W>
+__device__ __forceinline__ int swk(W w) {
+  return static_cast<int>((w >> (3 * wsh<W>())) & 1u);
+}
+template <class W>
+__device__ __forceinline__ int sws(W w) {
+  return static_cast<int>((w >> (3 * wsh<W>() + 1)) & 1u);
+}
 
 template <class MS>
 __device__ __forceinline__ P3 mpt(const MS &m, int p) {
@@ -193,8 +227,7 @@ __device__ bool mini_sweep(MS &m, bool active, int s, int nseg, int seg, int kin
     if (bridge) {
       if (sideU) { u = nfoot; cu = first; eu = m.ib[u + 1]; }
       else { v = nfoot; cv = first; ev = m.ib[v + 1]; }
-      const unsigned bw = static_cast<unsigned>(a) | (static_cast<unsigned>(b) << 10) |
-                          (static_cast<unsigned>(c) << 20) | (static_cast<unsigned>(kind) << 30);
+      const typename MS::W bw = wpack<typename MS::W>(a, b, c, kind, 0);
       if (MODE == 1 && base + nb < MS::MINI_B) {
         m.bt[base + nb] = best;
         m.bw[base + nb] = bw;
@@ -227,7 +260,8 @@ template <int MINI_T, int MINI_K, int MINI_N>
 __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int lv, long long j0, long long j1,
                                                  long long *err, int seglen, long long *spec,
-                                                 long long *stamp) {
+                                                 long long *stamp, unsigned char *gmem,
+                                                 size_t gstride) {
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -237,8 +271,13 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   constexpr int MINI_B = MS::MINI_B;
   constexpr int PER = (MINI_K + MINI_T) / MINI_T;  // blocked-scan items per thread
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  MS &m = *reinterpret_cast<MS *>(smem_raw);
+  // the huge variant keeps the job's arrays in a global-memory slot (L1/L2
+  // resident; far more than one SM's shared memory), the others in shared
+  // memory
+  MS &m = *reinterpret_cast<MS *>(
+      gmem ? gmem + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * gstride : smem_raw);
   typedef cub::BlockScan<int, MINI_T> Scan;
+  __shared__ typename Scan::TempStorage s_scan;
   const int tid = threadIdx.x, T = MINI_T;
   const long long j = j0 + blockIdx.x;
   if (j >= j1) return;
@@ -328,16 +367,14 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       side = 1;
     }
     m.st[d] = o.t;
-    m.sw[d] = static_cast<unsigned>(o.a) | (static_cast<unsigned>(o.b) << 10) |
-              (static_cast<unsigned>(o.c) << 20) | (static_cast<unsigned>(o.kind & 1) << 30) |
-              (side << 31);
+    m.sw[d] = wpack<typename MS::W>(o.a, o.b, o.c, o.kind, static_cast<int>(side));
   }
   __syncthreads();
   MINI_TICK(2);
   // ---- incidence lists: counts, scan, scatter, per-list sort, links after
   for (int d = tid; d < kin; d += T) {
     if (d > 0 && m.st[d] == m.st[d - 1]) m.flag = 1;  // exact tie
-    const unsigned w = m.sw[d];
+    const auto w = m.sw[d];
     atomicAdd(&m.cur[swa(w)], 1);
     atomicAdd(&m.cur[swb(w)], 1);
     atomicAdd(&m.cur[swc(w)], 1);
@@ -353,7 +390,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       sum += local[q];
     }
     int off;
-    Scan(m.scan).ExclusiveSum(sum, off);
+    Scan(s_scan).ExclusiveSum(sum, off);
     for (int q = 0; q < per && q < PER; ++q) {
       const int p = tid * per + q;
       if (p <= nS) m.ib[p] = off;
@@ -365,7 +402,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   __syncthreads();
   // scatter (arbitrary order within a list; the owner kept alongside) ...
   for (int d = tid; d < kin; d += T) {
-    const unsigned w = m.sw[d];
+    const auto w = m.sw[d];
     const int pa = swa(w), pb = swb(w), pc = swc(w);
     int q = atomicAdd(&m.cur[pa], 1);
     m.eo[q] = static_cast<short>(d);
@@ -394,7 +431,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     const int b0 = m.ib[p], b1 = m.ib[p + 1];
     short2 l = m.LN[p];
     for (int k = b0; k < b1; ++k) {  // links after each incidence (forward fill)
-      const unsigned w = m.sw[m.ei[k]];
+      const auto w = m.sw[m.ei[k]];
       const bool ins = swk(w) == EV_INS;
       if (swa(w) == p) {
         l.y = static_cast<short>(ins ? swb(w) : swc(w));
@@ -529,7 +566,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       int keep = 0;
       if (d < kin) {
         const double t = m.st[d];
-        const unsigned w = m.sw[d];
+        const auto w = m.sw[d];
         const int nbf = bridges_before(t);
         if (nbf < NB && m.bt[nbf] == t) m.flag = 1;
         const int u = nbf ? m.buv[nbf - 1].x : uv0.x, v = nbf ? m.buv[nbf - 1].y : uv0.y;
@@ -539,7 +576,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       sum += keep;
     }
     int off;
-    Scan(m.scan).ExclusiveSum(sum, off);
+    Scan(s_scan).ExclusiveSum(sum, off);
     for (int q = 0; q < per && q < PER; ++q) {
       const int d = tid * per + q;
       if (d <= kin) m.cpos[d] = local[q] ? (off | (1 << 30)) : off;
@@ -561,7 +598,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     const int cp = m.cpos[d];
     if (!(cp & (1 << 30))) continue;
     const double t = m.st[d];
-    const unsigned w = m.sw[d];
+    const auto w = m.sw[d];
     const int idx = (cp & ~(1 << 30)) + bridges_before(t);
     Ev o;
     o.t = t;
@@ -580,7 +617,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       if (m.st[mid] < t) lo = mid + 1; else hi = mid;
     }
     const int idx = i + (m.cpos[lo] & ~(1 << 30));
-    const unsigned w = m.bw[i];
+    const auto w = m.bw[i];
     Ev o;
     o.t = t;
     o.a = swa(w);
@@ -621,7 +658,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       sum += keep;
     }
     int off;
-    Scan(m.scan).ExclusiveSum(sum, off);
+    Scan(s_scan).ExclusiveSum(sum, off);
     for (int q = 0; q < per && q < PER; ++q) {
       const int p = tid * per + q;
       if (p <= nS) m.nid[p] = local[q] ? off : -1;
@@ -658,21 +695,25 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
 template <int T, int K, int N>
 static long long launch_mini(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                              long long j1, long long *err, cudaStream_t s, long long *spec,
-                             long long *stamp) {
+                             long long *stamp, void *gscratch = nullptr, size_t gbytes = 0) {
   static bool attr[64] = {};  // the attribute is per device
   int dev_id = 0;
   cudaGetDevice(&dev_id);
   if (dev_id < 0 || dev_id >= 64) return H3D_E_ARG;
   const size_t bytes = sizeof(MiniSmem<T, K, N>);
-  if (!attr[dev_id]) {
+  const size_t stride = (bytes + 255) & ~size_t(255);
+  if (gscratch) {  // global-memory slots, one per CTA
+    if (2 * static_cast<size_t>(j1 - j0) * stride > gbytes) return 1;
+  } else if (!attr[dev_id]) {
     if (h3d_check(cudaFuncSetAttribute(k_mini<T, K, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(bytes))))
       return H3D_E_CUDA;
     attr[dev_id] = true;
   }
   h3d_count_launches(1);
-  k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, bytes, s>>>(P, pts, n, lv, j0, j1,
-                                                                          err, g_mini_seglen, spec, stamp);
+  k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, gscratch ? 0 : bytes, s>>>(
+      P, pts, n, lv, j0, j1, err, g_mini_seglen, spec, stamp, static_cast<unsigned char *>(gscratch),
+      stride);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
 
@@ -680,9 +721,12 @@ int g_mini_seglen = 3;  // child events per time segment (H3D_MINI_SEG / h3d_tun
 
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant, long long *spec,
-                     long long *stamp) {
+                     long long *stamp, void *gscratch, size_t gbytes) {
   if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
   if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
+  if (variant == 3)
+    return launch_mini<1024, kMiniHugeEvents, kMiniHugePoints>(P, pts, n, lv, j0, j1, err, s, spec, stamp,
+                                                               gscratch, gbytes);
   return launch_mini<1024, 2048, 1024>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
 }
 
