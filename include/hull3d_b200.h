@@ -53,6 +53,7 @@ extern "C" {
 #define H3D_E_NONFINITE (-12)   /* ValueError("coordinates must be finite") */
 #define H3D_E_FASTPATH (-13)     /* fast path declined: caller takes the exact route */
 #define H3D_E_VERIFY (-14)       /* verify mode: a level wrote an inconsistent group */
+#define H3D_E_REDO (-15)         /* h3d_hull internal: the optimistic presort met ties */
 #define H3D_E_ARG (-100)         /* bad argument                            */
 #define H3D_E_CUDA (-101)        /* CUDA runtime error                      */
 
@@ -253,6 +254,37 @@ int64_t h3d_fast_extract(void *ws_lower, void *ws_upper, int64_t n,
                          int64_t final_lower, int64_t final_upper,
                          int32_t *faces, int64_t cap, int64_t *counts_dev,
                          int64_t *err_dev, void *stream);
+
+/* ---- the whole convex_hull_3d device pipeline in ONE call (csrc/hull.cu):
+ * presort + tie path + degeneracy scan (api.py:90-147), both hull passes over
+ * all merge levels (parallel.py:68-112, one launch per level covering both
+ * passes), extract_faces (_ckernels.pyx:324-349), orientation / remap /
+ * vertex compaction (api.py:252-266), then ONE read-back of the sizes (plus
+ * one per measured merge level inside the level loop).
+ *   pts        device (n,3) f64, caller order, n >= 4
+ *   sorted_pts device (n,3) f64 out; order device int64[n] out (api.py:97)
+ *   presort_ws h3d_presort_workspace_bytes(n); ws_lower / ws_upper
+ *              h3d_fast_pass_workspace_bytes(n) each
+ *   faces_raw  device int32 (cap,3) scratch, cap >= 2n; faces device int64
+ *              (cap,3) out (outward, caller indices, lower block then upper
+ *              block in log order); vertices device int64[n] out (sorted
+ *              unique); vertex_mark device int32[n] scratch
+ *   state_dev  device int64[H3D_HULL_STATE] scratch
+ *   flags      bit 0: per-level device time stamps; bit 1: verify mode
+ *   info       host int64[H3D_HULL_INFO]: [0] 0 or the fast path's decline
+ *              code (run the exact engine on sorted_pts), [1] lower events,
+ *              [2] upper events, [3] facets, [4] vertices, [5] perturbed,
+ *              [6] final buffer, [7] verify diagnostics; info[32 + 8 + l] =
+ *              stamp (ns) of level l (0 = presort start, 40 = end).
+ * Returns 0 or a negative code: H3D_E_NONFINITE / _TIES / _COINCIDENT /
+ * _COLLINEAR / _COPLANAR / _NOFACETS (DegenerateInputError, ValueError),
+ * H3D_E_ARG, H3D_E_CUDA. */
+#define H3D_HULL_STATE 96
+#define H3D_HULL_INFO 128
+int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *presort_ws,
+                 size_t presort_ws_bytes, void *ws_lower, void *ws_upper, size_t pass_ws_bytes,
+                 int32_t *faces_raw, int64_t cap, int64_t *faces, int64_t *vertices, int32_t *vertex_mark,
+                 int64_t *state_dev, int32_t flags, int64_t *info, void *stream);
 
 /* ---- device-wide primitives (csrc/prims.cuh), hand-written for sm_100a;
  * exported so the parity tests can check them against numpy on their own.

@@ -53,6 +53,8 @@ SIGNATURES: dict[str, tuple] = {
     "h3d_orient_remap": (i64, [vp, i64, vp, vp, i64, vp, vp, vp, vp, sz, vp]),
     "h3d_orient_remap_ex": (i64, [vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]),
     "h3d_presort_slab": (i64, [vp, i64, i64, i64, ctypes.c_int32, vp, vp, vp, sz, vp]),
+    "h3d_hull": (i64, [vp, i64, vp, vp, vp, sz, vp, vp, sz, vp, i64, vp, vp, vp, vp, ctypes.c_int32,
+                       vp, vp]),
     "h3d_prim_temp_bytes": (sz, [i64]),
     "h3d_radix_sort_pairs": (i64, [vp, vp, vp, vp, i64, ctypes.c_int32, ctypes.c_int32,
                                    ctypes.c_int32, ctypes.c_int32, vp, sz, vp]),

@@ -308,10 +308,47 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
     # the per-device workspaces are shared: one hull at a time per device
     # (calls from several threads are serialised, not interleaved); every
     # launch goes to `dev` whatever the caller's current device is
+    from . import engine as E
+
     with _device_lock(dev), torch.cuda.device(dev):
-        sort_t0 = time.perf_counter()
-        sorted_pts, order, perturbed = presort(pts)
-        sort_ms = (time.perf_counter() - sort_t0) * 1e3
+        if engine == "fast" and E.PROFILE is None:
+            # the whole device pipeline in one native call (csrc/hull.cu)
+            from . import fast
+
+            if E.KERNEL_EVENTS:  # bench.py: events around the lane-per-job launches
+                fast.profile_enable(2)
+            try:
+                h = fast.hull(pts, stamps=True)
+            finally:
+                if E.KERNEL_EVENTS:
+                    fast.profile_enable(0)
+            if not h.declined:
+                lower_levels: list[float] = []
+                upper_levels: list[float] = []
+                if solver == "parallel" and h.level_rows:
+                    _level_rows_to_stats(h.level_rows, n, (lower_levels, upper_levels))
+                verts, faces = h.vertices, h.faces
+                if return_device:  # own the result (the buffers are reused)
+                    verts, faces = verts.clone(), faces.clone()
+                else:
+                    verts, faces = to_host(verts), to_host(faces)
+                total_ms = (time.perf_counter() - total_t0) * 1e3
+                pass_ms = h.passes_ms if h.passes_ms is not None else 0.0
+                stats = HullStats(n=n, levels=level_count(n), lower_events=h.k_lo,
+                                  upper_events=h.k_up,
+                                  sort_ms=h.sort_ms if h.sort_ms is not None else 0.0,
+                                  lower_ms=pass_ms / 2, upper_ms=pass_ms / 2, total_ms=total_ms,
+                                  perturbed=h.perturbed, solver=solver, workers=workers,
+                                  lower_level_ms=lower_levels, upper_level_ms=upper_levels)
+                return HullResult(vertices=verts, faces=faces, stats=stats)
+            # declined: the exact engine on the rows the call presorted
+            sorted_pts, order, perturbed = h.sorted_pts.clone(), h.order.clone(), h.perturbed
+            sort_ms = h.sort_ms or 0.0
+            engine = "exact"
+        else:
+            sort_t0 = time.perf_counter()
+            sorted_pts, order, perturbed = presort(pts)
+            sort_ms = (time.perf_counter() - sort_t0) * 1e3
 
         lower_levels: list[float] = []
         upper_levels: list[float] = []

@@ -85,7 +85,8 @@ void h3d_stamp_now(cudaStream_t s, int slot) {
 
 extern "C" void h3d_profile_stamps(int64_t *dev_buf) {
   t_stamps = reinterpret_cast<long long *>(dev_buf);
-  for (int &r : t_routes) r = -1;
+  if (dev_buf)  // a new recording starts; switching off keeps the routes for h3d_profile_routes
+    for (int &r : t_routes) r = -1;
 }
 extern "C" int64_t h3d_profile_routes(int32_t *out, int64_t max) {
   int64_t m = 0;

@@ -638,7 +638,9 @@ __global__ void k_centroid(const double *partial, int blocks, long long n, doubl
 // orient every facet outward against the centroid, remap, mark vertices
 __global__ void k_orient(const double *__restrict__ P, const double *__restrict__ cen,
                          const long long *__restrict__ order, const int *__restrict__ raw,
-                         long long F, long long *faces, int *mark) {
+                         long long F, long long *faces, int *mark,
+                         const long long *counts = nullptr) {
+  if (counts) F = counts[0] + counts[1];  // F < 0: the facet count is on the device
   const double c0 = cen[0], c1 = cen[1], c2 = cen[2];
   for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < F;
        f += (long long)gridDim.x * blockDim.x) {
@@ -749,6 +751,87 @@ bool degenerate_scan(const double *sorted_pts, long long rows, PresortWS &w, uns
 }
 
 }  // namespace
+
+namespace h3d {
+
+// Gate of the optimistic presort (h3d_hull): its flags and the degeneracy
+// scan decide, on the device, whether the merge levels may run on the sorted
+// rows.  A tie or a long run of equal 32-bit keys needs the exact tie path
+// (the host redoes the presort), a non-finite coordinate or a degenerate
+// input is an error -- either way the error word stops every later launch.
+__global__ void k_presort_gate(const int *flag, const ScanState *st, long long *err) {
+  const long long none = 0x7fffffffffffffffll;
+  long long e = 0;
+  if (flag[1]) e = H3D_E_NONFINITE;
+  else if (flag[0] || flag[2]) e = H3D_E_REDO;
+  else if (st->i == none) e = H3D_E_COINCIDENT;
+  else if (st->j == none) e = H3D_E_COLLINEAR;
+  else if (st->k == none) e = H3D_E_COPLANAR;
+  if (e) raise_err(err, e);
+}
+
+// The presort's common path with no host synchronisation: scan, 32-bit keys,
+// radix sort, tie fix, row gather (+ adjacent-tie test), degeneracy scan
+// (head, then each full stage only if the head left it undecided: the
+// stage kernels return at once otherwise), gate.  Returns 0 or a code.
+int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *workspace,
+                      size_t workspace_bytes, long long *err, cudaStream_t s) {
+  if (n < 1 || n > (1ll << 30)) return H3D_E_ARG;
+  h3d_arena ar(workspace, workspace_bytes);
+  PresortWS w;
+  if (!carve(ar, n, w)) return H3D_E_ARG;
+  const unsigned G = h3d_grid(n, 256) > 4096 ? 4096 : h3d_grid(n, 256);
+  long long *ord = reinterpret_cast<long long *>(order);
+  cudaMemsetAsync(w.flag, 0, sizeof(int) * 4, s);
+  h3d_count_launches(1);
+  k_scan_init<<<1, 1, 0, s>>>(w.scan);
+  const unsigned long long mm_init[2] = {~0ull, 0ull};
+  cudaMemcpyAsync(w.mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, s);
+  h3d_count_launches(2);
+  k_scan_input<<<G > 1184 ? 1184 : G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
+  unsigned *k32a = reinterpret_cast<unsigned *>(w.k0), *k32b = reinterpret_cast<unsigned *>(w.k1);
+  k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, nullptr);
+  bool alt = false;
+  h3d_count_launches(5);
+  if (h3d_check(prim::rs_sort_pairs<unsigned>(w.cub_tmp, w.cub_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32, &alt,
+                                              s, true)))
+    return H3D_E_CUDA;
+  int *vs = alt ? w.v1 : w.v0;
+  h3d_count_launches(2);
+  k_tiefix<<<G, 256, 0, s>>>(pts, alt ? k32b : k32a, vs, n, w.flag + 2);
+  k_gather_rows<<<G, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, nullptr, w.flag);
+  h3d_count_launches(5);
+  k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, n, w.scan, 16384);
+  for (int stage = 0; stage < 3; ++stage) k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
+  k_presort_gate<<<1, 1, 0, s>>>(w.flag, w.scan, err);
+  return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
+}
+
+// The epilogue with no host synchronisation: the facet count comes from the
+// device counts (k_lo + k_up), the kernels stride over it; the vertex count
+// lands in *vcount (device).
+int64_t orient_async(const double *sorted_pts, int64_t n, const int64_t *order, const int32_t *faces_raw,
+                     const long long *counts, int64_t cap, int64_t *faces, int32_t *vertex_mark,
+                     int64_t *vertices, long long *vcount, void *workspace, size_t workspace_bytes,
+                     cudaStream_t s) {
+  h3d_arena ar(workspace, workspace_bytes);
+  PresortWS w;
+  if (!carve(ar, n, w)) return H3D_E_ARG;
+  h3d_count_launches(3);
+  k_colsum<<<kColsumBlocks, 256, 0, s>>>(sorted_pts, n, w.partial);
+  k_centroid<<<1, 32, 0, s>>>(w.partial, kColsumBlocks, n, w.centroid);
+  cudaMemsetAsync(vertex_mark, 0, sizeof(int) * n, s);
+  const unsigned G = h3d_grid(cap, 256) > 1184 ? 1184 : h3d_grid(cap, 256);
+  k_orient<<<G, 256, 0, s>>>(sorted_pts, w.centroid, reinterpret_cast<const long long *>(order), faces_raw,
+                             -1, reinterpret_cast<long long *>(faces), vertex_mark, counts);
+  h3d_count_launches(3);
+  if (h3d_check(prim::select_flagged(w.cub_tmp, w.cub_bytes, vertex_mark, n,
+                                     reinterpret_cast<long long *>(vertices), vcount, s)))
+    return H3D_E_CUDA;
+  return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
+}
+
+}  // namespace h3d
 
 extern "C" {
 

@@ -94,8 +94,10 @@ class tuned:
         return False
 
 
-def profile_enable(on: bool) -> None:
-    _lib.load().h3d_profile_enable(1 if on else 0)
+def profile_enable(on: int) -> None:
+    """0 off; 1 (True): every level bracketed by CUDA events; 2: only the
+    lane-per-job kernel launches (bench.py's roofline)."""
+    _lib.load().h3d_profile_enable(int(on))
 
 
 def kernel_of(tag: int):
@@ -200,5 +202,85 @@ def run_both(sorted_pts: torch.Tensor, stamps: bool = False):
     return faces[: k_lo + k_up], k_lo, k_up
 
 
-__all__ = ["run_both", "profile_enable", "profile_collect", "E_FASTPATH", "E_VERIFY", "VERIFY",
+HULL_STATE = 96
+HULL_INFO = 128
+_STAMP_AT = HULL_INFO - HULL_STATE + 8  # info index of stamp slot 0
+
+
+class HullOut:
+    """Result of one h3d_hull call (csrc/hull.cu)."""
+
+    __slots__ = ("faces", "vertices", "k_lo", "k_up", "perturbed", "declined", "sorted_pts",
+                 "order", "level_rows", "sort_ms", "passes_ms")
+
+
+def hull(pts: torch.Tensor, stamps: bool = True) -> HullOut:
+    """The whole device pipeline in one C-ABI call: presort, both passes,
+    extraction, orientation/remap/vertex compaction, one read-back.  faces
+    and vertices are views of per-device cached buffers (copy before the
+    next call).  declined != 0: the fast path declined the input, run the
+    exact engine on sorted_pts/order.  Raises the API's exceptions."""
+    from .errors import check_api
+
+    L = _lib.load()
+    n = pts.shape[0]
+    dev = pts.device
+    s = stream_ptr(dev)
+    wsb = int(L.h3d_fast_pass_workspace_bytes(n))
+    pwsb = int(L.h3d_presort_workspace_bytes(n))
+    ws_lo = _WS.get(dev, 0, wsb)
+    ws_up = _WS.get(dev, 1, wsb)
+    pws = _WS.get(dev, 2, pwsb)
+    cap = 2 * n
+    # outputs and scratch, carved from one cached buffer per device
+    o_sorted, o_order, o_raw = 0, 24 * n, 32 * n
+    o_faces = o_raw + 12 * cap
+    o_verts = o_faces + 24 * cap
+    o_mark = o_verts + 8 * n
+    o_state = (o_mark + 4 * n + 255) & ~255
+    total = o_state + 8 * HULL_STATE
+    buf = _WS.get(dev, 3, total)
+    base = buf.data_ptr()
+    info = np.zeros(HULL_INFO, dtype=np.int64)
+    flags = (1 if stamps else 0) | (2 if VERIFY[0] else 0)
+    rc = L.h3d_hull(pts.data_ptr(), n, base + o_sorted, base + o_order, pws.data_ptr(), pwsb,
+                    ws_lo.data_ptr(), ws_up.data_ptr(), wsb, base + o_raw, cap, base + o_faces,
+                    base + o_verts, base + o_mark, base + o_state, flags, info.ctypes.data, s)
+    routes = None
+    if stamps:
+        routes = np.zeros(STAMP_SLOTS, dtype=np.int32)
+        L.h3d_profile_routes(routes.ctypes.data, STAMP_SLOTS)
+    check_api(int(rc))
+    out = HullOut()
+    out.sorted_pts = buf[o_sorted:o_sorted + 24 * n].view(torch.float64).view(n, 3)
+    out.order = buf[o_order:o_order + 8 * n].view(torch.int64)
+    out.declined = int(info[0])
+    out.perturbed = bool(info[5])
+    out.k_lo, out.k_up = int(info[1]), int(info[2])
+    out.level_rows, out.sort_ms, out.passes_ms = [], None, None
+    if out.declined == E_VERIFY:
+        d = int(info[7]) & ((1 << 64) - 1)
+        raise VerifyError("fast path: a level wrote a group that fails the device checks "
+                          f"(check {d >> 60}, level {(d >> 54) & 63}, pass {(d >> 53) & 1}, "
+                          f"group {(d >> 20) & 0xffffffff}, item {d & 0xfffff})")
+    if out.declined:
+        FALLBACKS[0] += 1
+        LAST_ERROR[0] = out.declined
+        out.faces = out.vertices = None
+        return out
+    F, V = int(info[3]), int(info[4])
+    out.faces = buf[o_faces:o_faces + 24 * F].view(torch.int64).view(F, 3)
+    out.vertices = buf[o_verts:o_verts + 8 * V].view(torch.int64)
+    if stamps:
+        st = info[_STAMP_AT:_STAMP_AT + STAMP_SLOTS]
+        out.level_rows = stamp_rows(st, routes)
+        LAST_LEVEL_ROWS[:] = out.level_rows
+        if st[0] > 0 and st[1] > 0:
+            out.sort_ms = (int(st[1]) - int(st[0])) / 1e6
+        if st[1] > 0 and st[STAMP_END] > 0:
+            out.passes_ms = (int(st[STAMP_END]) - int(st[1])) / 1e6
+    return out
+
+
+__all__ = ["run_both", "hull", "HullOut", "profile_enable", "profile_collect", "E_FASTPATH", "E_VERIFY", "VERIFY",
            "VerifyError", "verifying", "ctypes"]
