@@ -6,7 +6,7 @@ every step after the host->device copy on sm_100a CUDA kernels behind the
 C ABI in include/hull3d_b200.h.
 """
 
-from .api import CudaBackend, HullResult, HullStats, convex_hull_3d, perturb_ties
+from .api import CudaBackend, HullResult, HullStats, convex_hull_3d, convex_hull_3d_stream, perturb_ties
 from .engine import level_count
 from .errors import (
     BridgeWalkError,
@@ -30,6 +30,7 @@ __all__ = [
     "LogError",
     "MergeOverflowError",
     "convex_hull_3d",
+    "convex_hull_3d_stream",
     "level_count",
     "perturb_ties",
     "__version__",

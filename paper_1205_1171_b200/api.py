@@ -366,6 +366,53 @@ def convex_hull_3d(points, backend=None, *, solver: str = "parallel",
     return HullResult(vertices=verts, faces=faces, stats=stats)
 
 
+def convex_hull_3d_stream(clouds, backend=None, *, solver: str = "parallel", return_device: bool = False):
+    """Throughput form of convex_hull_3d for a sequence of clouds (an
+    extension, not a reference interface): yields one HullResult per cloud,
+    in order, each identical to ``convex_hull_3d(cloud, backend, ...)``.
+    While cloud i's hull runs, the host->device copy of cloud i+1 already
+    runs on a second CUDA stream (pinned CPU tensors copy asynchronously by
+    DMA), so the PCIe transfer hides behind the previous hull's kernels.
+    Every cloud is still copied in full; nothing is cached between clouds."""
+    it = iter(clouds)
+    dev = _device_of(None, backend)
+    copy_stream = torch.cuda.Stream(device=dev)
+    bufs: list = [None, None]
+
+    def stage(cloud, slot):
+        host = cloud if isinstance(cloud, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(np.asarray(cloud, dtype=np.float64)))
+        if host.is_cuda:
+            return host, None
+        host = host.to(dtype=torch.float64)
+        if host.ndim != 2 or host.shape[1] != 3:
+            raise ValueError("points must have shape (n, 3)")
+        b = bufs[slot]
+        if b is None or b.shape != host.shape:
+            b = bufs[slot] = torch.empty(host.shape, dtype=torch.float64, device=dev)
+        with torch.cuda.stream(copy_stream):
+            b.copy_(host, non_blocking=host.is_pinned())
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        return b, ev
+
+    try:
+        nxt = stage(next(it), 0)
+    except StopIteration:
+        return
+    slot = 0
+    while nxt is not None:
+        cur, ev = nxt
+        try:  # the next cloud's copy starts before this hull runs
+            nxt = stage(next(it), slot ^ 1)
+        except StopIteration:
+            nxt = None
+        if ev is not None:
+            torch.cuda.current_stream(dev).wait_event(ev)
+        yield convex_hull_3d(cur, backend, solver=solver, return_device=return_device)
+        slot ^= 1
+
+
 def perturb_ties(points) -> np.ndarray:
     """api.py:61-83, exposed for API parity (host helper, not on the hot path:
     the device presort performs the same perturbation in csrc/presort.cu)."""

@@ -149,3 +149,35 @@ def test_concurrent_threads_one_device(oracle_mod):
         t.join()
     for g, e in zip(got, exp):
         assert np.array_equal(g, e)
+
+
+def test_stream_api_equals_per_call(oracle_mod):
+    """convex_hull_3d_stream (copy of cloud i+1 overlapping hull i) yields,
+    in order, exactly what one convex_hull_3d call per cloud returns --
+    pinned tensors, numpy arrays and clouds of different sizes mixed."""
+    clouds = [torch.from_numpy(generate(20000, "ball", 1)).pin_memory(),
+              generate(7777, "cube", 2),
+              torch.from_numpy(generate(20000, "sphere", 3)).pin_memory(),
+              generate(5000, "gauss", 4)]
+    got = list(H.convex_hull_3d_stream(clouds))
+    assert len(got) == len(clouds)
+    for c, r in zip(clouds, got):
+        pts = c.numpy() if isinstance(c, torch.Tensor) else c
+        exp = oracle_mod.convex_hull_3d(pts)
+        assert np.array_equal(r.faces, exp.faces)
+        assert np.array_equal(r.vertices, exp.vertices)
+    assert list(H.convex_hull_3d_stream([])) == []
+
+
+def test_stats_level_times_from_device_stamps():
+    """Per-level seconds (HullStats.*_level_ms, F12) come from the level
+    kernels' device time stamps: one entry per level, non-negative, and the
+    fused leaf levels report at their last level."""
+    pts = generate(1 << 16, "ball", 7)
+    r = H.convex_hull_3d(pts)
+    L = r.stats.levels
+    assert len(r.stats.lower_level_ms) == L and len(r.stats.upper_level_ms) == L
+    assert all(t >= 0.0 for t in r.stats.lower_level_ms)
+    assert sum(r.stats.lower_level_ms) > 0.0
+    assert r.stats.lower_level_ms[0] == 0.0 and r.stats.lower_level_ms[2] > 0.0  # leaf: levels 1..3
+    assert r.stats.sort_ms > 0.0 and r.stats.lower_ms > 0.0
