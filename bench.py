@@ -568,8 +568,12 @@ def run_ours_distributed(args):
                              "the cloud (multigpu.gather_input)"},
         "gpu_launches": launches, "roofline": None, "cpu_baseline": None, "clocks": clk,
         "rank0_phases_ms": phases,
+        "rank_memory_gb_estimate": {k: round(v / 1e9, 3) for k, v in
+                                    MG.rank_memory_bytes(n, ws, max(2, plan.S // 10)).items()},
         "note": "roofline and cpu_baseline are on the N=1 line; rank0_phases_ms: one untimed "
-                "call, presort / slab levels / cross levels (device events)",
+                "call, presort / slab levels / cross levels (device events); "
+                "rank_memory_gb_estimate: per-rank device bytes from the library's sizing "
+                "functions (slab groups assumed <= S/10 kept points)",
     }
     print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -161,18 +161,24 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts,
                     int32_t *perturbed, void *stream);
 
 /* Sharded presort (multi-GPU): writes rows [q0, p1) of the global sorted
- * order (sorted_pts / order, both full-size n) from the full input without
- * sorting the rest: 32-bit keys, a radix select of the two window
- * boundaries, exact ranking of the boundary key runs, a sort of the window.
- * scan != 0 also runs _scan_degenerate over rows [0, p1) (rank 0, q0 = 0).
- * Returns 0, or H3D_E_FASTPATH whenever the window cannot reproduce
- * h3d_presort on its own (any x tie, a long run of equal keys, non-finite
- * input, a degeneracy not decided inside the window): the caller then runs
- * the replicated h3d_presort.  Needs n >= 2048. */
+ * order (sorted_pts[3*q0 ...], order[q0 ...]: only the window's rows are
+ * touched, so the caller may pass a window-sized buffer minus q0 rows) from
+ * the full input without sorting the rest: 32-bit keys, a radix select of
+ * the two window boundaries, exact ranking of the boundary key runs, a sort
+ * of the window.  scan != 0 also runs _scan_degenerate over rows [0, p1)
+ * (rank 0, q0 = 0).  Workspace: h3d_presort_slab_workspace_bytes(n, p1 - q0)
+ * (4 bytes per input point + O(window)).  Returns 0, or H3D_E_FASTPATH
+ * whenever the window cannot reproduce h3d_presort on its own (any x tie, a
+ * long run of equal keys, non-finite input, a degeneracy not decided inside
+ * the window): the caller then runs the replicated h3d_presort.  Needs
+ * n >= 2048. */
+size_t h3d_presort_slab_workspace_bytes(int64_t n, int64_t m);
 int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1,
                          int32_t scan, double *sorted_pts, int64_t *order,
                          void *workspace, size_t workspace_bytes, void *stream);
 
+/* workspace h3d_orient_remap* needs (<= h3d_presort_workspace_bytes(n)) */
+size_t h3d_epilogue_workspace_bytes(int64_t n);
 /* Epilogue (pkg/src/hull3d/api.py:252-266): faces_raw (F,3) i32 in sorted
  * indices (lower block then upper block) -> faces (F,3) i64 oriented outward
  * against the centroid and mapped through order; vertex_mark (n) i32 scratch;
@@ -211,6 +217,9 @@ int64_t h3d_tune(const char *name, int64_t value);
  * time-split pipeline for large merge jobs, sized for min(n, max(2^21, n/8)) points
  * per pass -- levels beyond it fall back to the warp merge) */
 size_t h3d_fast_pass_workspace_bytes(int64_t n);
+/* the upper pass's workspace needs only this much (no big-job scratch; the
+ * workspace_bytes argument of the calls below stays the lower pass's) */
+size_t h3d_fast_upper_workspace_bytes(int64_t n);
 
 /* Both hull passes (build_movie, pkg/src/hull3d/parallel.py:68-112) over the
  * presorted points, all ceil(log2 n) levels, stream-ordered, no host sync:

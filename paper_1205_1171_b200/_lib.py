@@ -31,6 +31,7 @@ SIGNATURES: dict[str, tuple] = {
     "h3d_profile_stamps": (None, [vp]),
     "h3d_profile_routes": (i64, [vp, i64]),
     "h3d_fast_pass_workspace_bytes": (sz, [i64]),
+    "h3d_fast_upper_workspace_bytes": (sz, [i64]),
     "h3d_fast_passes": (i64, [vp, i64, vp, vp, sz, vp, ctypes.c_int32, vp, vp]),
     "h3d_fast_passes_range": (i64, [vp, i64, i64, i64, ctypes.c_int32, ctypes.c_int32, vp, vp,
                                     sz, vp, ctypes.c_int32, vp]),
@@ -53,6 +54,8 @@ SIGNATURES: dict[str, tuple] = {
     "h3d_orient_remap": (i64, [vp, i64, vp, vp, i64, vp, vp, vp, vp, sz, vp]),
     "h3d_orient_remap_ex": (i64, [vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]),
     "h3d_presort_slab": (i64, [vp, i64, i64, i64, ctypes.c_int32, vp, vp, vp, sz, vp]),
+    "h3d_presort_slab_workspace_bytes": (sz, [i64, i64]),
+    "h3d_epilogue_workspace_bytes": (sz, [i64]),
     "h3d_hull": (i64, [vp, i64, vp, vp, vp, sz, vp, vp, sz, vp, i64, vp, vp, vp, vp, ctypes.c_int32,
                        vp, vp]),
     "h3d_prim_temp_bytes": (sz, [i64]),

@@ -131,17 +131,19 @@ def presort(pts_dev: torch.Tensor):
 
 
 def orient_remap(sorted_pts: torch.Tensor, order: torch.Tensor, raw: torch.Tensor,
-                 centroid_pts: torch.Tensor | None = None):
+                 centroid_pts: torch.Tensor | None = None, n_callers: int | None = None):
     """Device api.py:252-266 -> (vertices i64, faces i64) on device.
     centroid_pts: rows the centroid is taken over (default sorted_pts; the
-    sharded multi-GPU path passes the caller-order input)."""
+    multi-GPU path passes the caller-order input, with n_callers = the
+    number of caller points when sorted_pts holds only the rows the faces
+    index)."""
     L = _lib.load()
-    n = sorted_pts.shape[0]
+    n = n_callers if n_callers is not None else sorted_pts.shape[0]
     dev = sorted_pts.device
     F = raw.shape[0]
     if F == 0:
         raise DegenerateInputError("no facets produced; input is degenerate")
-    ws_bytes = int(L.h3d_presort_workspace_bytes(n))
+    ws_bytes = int(L.h3d_epilogue_workspace_bytes(n))
     ws = _Workspace.get(dev, ws_bytes)
     faces = torch.empty((F, 3), dtype=torch.int64, device=dev)
     mark = torch.empty(n, dtype=torch.int32, device=dev)

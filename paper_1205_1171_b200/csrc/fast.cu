@@ -1651,6 +1651,11 @@ size_t h3d_fast_pass_workspace_bytes(int64_t n) {  // per pass (+ the big-job sc
   return base_pass_bytes(n) + big_workspace_bytes(big_capacity(n)) + 4096;
 }
 
+size_t h3d_fast_upper_workspace_bytes(int64_t n) {  // the upper pass: no big-job scratch
+  if (n < 1) n = 1;
+  return base_pass_bytes(n) + 4096;
+}
+
 int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, int64_t p1,
                               int32_t lv_lo, int32_t lv_hi, void *ws_lower, void *ws_upper,
                               size_t workspace_bytes, int64_t *err_dev, int32_t verify,

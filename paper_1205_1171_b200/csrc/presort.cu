@@ -314,7 +314,7 @@ __global__ void k_sel_pick(unsigned *hist, SelState *st, int pass) {
 constexpr int kSelItems = 8;
 
 __global__ void __launch_bounds__(256) k_sel_compact(const unsigned *__restrict__ k32, long long n,
-                                                     SelState *st, int *out, int *runs) {
+                                                     SelState *st, int *out, int *runs, long long cap) {
   typedef cub::BlockScan<int, 256> BS;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int s_base;
@@ -353,9 +353,14 @@ __global__ void __launch_bounds__(256) k_sel_compact(const unsigned *__restrict_
     if (threadIdx.x == 0) s_base = total ? atomicAdd(&st->count, total) : 0;
     __syncthreads();
     off += s_base;
+    // a bad selection may find more than the window holds: never write past
+    // the window buffer (the count check in k_sel_keys rejects it)
 #pragma unroll
     for (int q = 0; q < kSelItems; ++q)
-      if (inm >> q & 1u) out[off++] = static_cast<int>(i0 + q);
+      if (inm >> q & 1u) {
+        if (off < cap) out[off] = static_cast<int>(i0 + q);
+        ++off;
+      }
     __syncthreads();
   }
 }
@@ -395,7 +400,7 @@ __global__ void k_keys32_hist(const double *__restrict__ pts, long long n,
 
 // boundary runs: global position = (b - rem_b) + rank inside the run
 __global__ void k_sel_runs(const double *__restrict__ pts, const unsigned *__restrict__ k32,
-                           SelState *st, const int *__restrict__ runs, int *out) {
+                           SelState *st, const int *__restrict__ runs, int *out, long long cap) {
   const int nr = min(st->nrun, kSelRunCap);
   const long long q0 = st->b[0] >= 0 ? st->b[0] : 0;
   for (int e = threadIdx.x; e < nr; e += blockDim.x) {
@@ -412,7 +417,10 @@ __global__ void k_sel_runs(const double *__restrict__ pts, const unsigned *__res
     const int b = (st->b[0] >= 0 && k == st->pre[0]) ? 0 : 1;
     const long long pos = st->b[b] - st->rem[b] + r;
     const long long p1 = st->b[1] >= 0 ? st->b[1] : 0x7fffffffffffffffll;
-    if (pos >= q0 && pos < p1) out[atomicAdd(&st->count, 1)] = ve;
+    if (pos >= q0 && pos < p1) {
+      const int at = atomicAdd(&st->count, 1);
+      if (at < cap) out[at] = ve;
+    }
   }
 }
 
@@ -715,6 +723,56 @@ bool carve(h3d_arena &ar, long long n, PresortWS &w) {
   return ar.base == nullptr || w.mm != nullptr;
 }
 
+// the epilogue's workspace: centroid partials, the count, the flagged
+// select's temp (O(n / 2048)) -- carved from the front of whatever buffer
+// the caller passes (a presort workspace, or an epilogue-sized one)
+struct EpiWS {
+  double *partial, *centroid;
+  long long *count;
+  void *tmp;
+  size_t tmp_bytes;
+};
+
+bool carve_epi(h3d_arena &ar, long long n, EpiWS &w) {
+  w.partial = ar.take<double>(3 * kColsumBlocks);
+  w.centroid = ar.take<double>(4);
+  w.count = ar.take<long long>(2);
+  w.tmp_bytes = prim::select_temp_bytes(n);
+  w.tmp = ar.take<char>(w.tmp_bytes);
+  return ar.base == nullptr || w.tmp != nullptr;
+}
+
+// the sharded presort's workspace: keys of all n points, everything else
+// sized by the window (m rows) -- O(n) 4-byte keys, not O(n) rows
+struct SlabWS {
+  unsigned *k32, *lk, *lk_alt;
+  int *idx, *idx_alt, *runs;
+  unsigned *hist;
+  SelState *st;
+  int *flag;
+  ScanState *scan;
+  unsigned long long *mm;
+  void *tmp;
+  size_t tmp_bytes;
+};
+
+bool carve_slab(h3d_arena &ar, long long n, long long m, SlabWS &w) {
+  w.k32 = ar.take<unsigned>(n);
+  w.lk = ar.take<unsigned>(m);
+  w.lk_alt = ar.take<unsigned>(m);
+  w.idx = ar.take<int>(m);
+  w.idx_alt = ar.take<int>(m);
+  w.runs = ar.take<int>(kSelRunCap + 64);
+  w.hist = ar.take<unsigned>(4096);
+  w.st = ar.take<SelState>(1);
+  w.flag = ar.take<int>(4);
+  w.scan = ar.take<ScanState>(1);
+  w.mm = ar.take<unsigned long long>(2);
+  w.tmp_bytes = prim::rs_temp_bytes<unsigned>(m);
+  w.tmp = ar.take<char>(w.tmp_bytes);
+  return ar.base == nullptr || w.tmp != nullptr;
+}
+
 // stable sort of (keys, vals) pairs; result in (*ko, *vo)
 bool radix(PresortWS &w, unsigned long long *kin, int *vin, unsigned long long *kalt, int *valt,
            long long n, unsigned long long **ko, int **vo, cudaStream_t s) {
@@ -733,20 +791,20 @@ bool radix(PresortWS &w, unsigned long long *kin, int *vin, unsigned long long *
 // rest (random inputs stop in the first block, as the reference's block-wise
 // scan does).  Reads back the state and the flag words (one sync, two when
 // the head is undecided).
-bool degenerate_scan(const double *sorted_pts, long long rows, PresortWS &w, unsigned G,
+bool degenerate_scan(const double *sorted_pts, long long rows, ScanState *wscan, int *wflag, unsigned G,
                      ScanState *hs, int *hflag, int nflag, cudaStream_t s) {
   const long long none = 0x7fffffffffffffffll;
   h3d_count_launches(1);
-  k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, rows, w.scan, 16384);
-  if (h3d_check(cudaMemcpyAsync(hs, w.scan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaMemcpyAsync(hflag, w.flag, nflag * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+  k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, rows, wscan, 16384);
+  if (h3d_check(cudaMemcpyAsync(hs, wscan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) ||
+      h3d_check(cudaMemcpyAsync(hflag, wflag, nflag * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
       h3d_check(cudaStreamSynchronize(s)))
     return false;
   if (hs->i != none && hs->j != none && hs->k != none) return true;
   h3d_count_launches(3);
   for (int stage = 0; stage < 3; ++stage)
-    k_degenerate<<<G, 256, 0, s>>>(sorted_pts, rows, w.scan, stage, 1, rows);
-  return !h3d_check(cudaMemcpyAsync(hs, w.scan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) &&
+    k_degenerate<<<G, 256, 0, s>>>(sorted_pts, rows, wscan, stage, 1, rows);
+  return !h3d_check(cudaMemcpyAsync(hs, wscan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) &&
          !h3d_check(cudaStreamSynchronize(s));
 }
 
@@ -815,8 +873,8 @@ int64_t orient_async(const double *sorted_pts, int64_t n, const int64_t *order, 
                      int64_t *vertices, long long *vcount, void *workspace, size_t workspace_bytes,
                      cudaStream_t s) {
   h3d_arena ar(workspace, workspace_bytes);
-  PresortWS w;
-  if (!carve(ar, n, w)) return H3D_E_ARG;
+  EpiWS w;
+  if (!carve_epi(ar, n, w)) return H3D_E_ARG;
   h3d_count_launches(3);
   k_colsum<<<kColsumBlocks, 256, 0, s>>>(sorted_pts, n, w.partial);
   k_centroid<<<1, 32, 0, s>>>(w.partial, kColsumBlocks, n, w.centroid);
@@ -825,7 +883,7 @@ int64_t orient_async(const double *sorted_pts, int64_t n, const int64_t *order, 
   k_orient<<<G, 256, 0, s>>>(sorted_pts, w.centroid, reinterpret_cast<const long long *>(order), faces_raw,
                              -1, reinterpret_cast<long long *>(faces), vertex_mark, counts);
   h3d_count_launches(3);
-  if (h3d_check(prim::select_flagged(w.cub_tmp, w.cub_bytes, vertex_mark, n,
+  if (h3d_check(prim::select_flagged(w.tmp, w.tmp_bytes, vertex_mark, n,
                                      reinterpret_cast<long long *>(vertices), vcount, s)))
     return H3D_E_CUDA;
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
@@ -948,7 +1006,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   // _scan_degenerate on the sorted rows (api.py:113-147)
   ScanState hs;
   int tie2 = 0;
-  if (!degenerate_scan(sorted_pts, n, w, G, &hs, &tie2, 1, s)) return H3D_E_CUDA;
+  if (!degenerate_scan(sorted_pts, n, w.scan, w.flag, G, &hs, &tie2, 1, s)) return H3D_E_CUDA;
   if (tie && tie2) return H3D_E_TIES;
   const long long none = 0x7fffffffffffffffll;
   if (hs.i == none) return H3D_E_COINCIDENT;
@@ -957,21 +1015,38 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   return 0;
 }
 
+size_t h3d_epilogue_workspace_bytes(int64_t n) {
+  if (n < 1) n = 1;
+  h3d_arena ar(nullptr, 0);
+  EpiWS w;
+  carve_epi(ar, n, w);
+  return ar.used + 4096;
+}
+
+size_t h3d_presort_slab_workspace_bytes(int64_t n, int64_t m) {
+  if (n < 1) n = 1;
+  if (m < 1) m = 1;
+  h3d_arena ar(nullptr, 0);
+  SlabWS w;
+  carve_slab(ar, n, m, w);
+  return ar.used + 4096;
+}
+
 int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1, int32_t scan,
                          double *sorted_pts, int64_t *order, void *workspace,
                          size_t workspace_bytes, void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n < 2048 || n > (1ll << 30) || q0 < 0 || p1 > n || q0 >= p1) return H3D_E_ARG;
   h3d_arena ar(workspace, workspace_bytes);
-  PresortWS w;
-  if (!carve(ar, n, w)) return H3D_E_ARG;
-  const unsigned G = h3d_grid(n, 256) > 4096 ? 4096 : h3d_grid(n, 256);
   const long long m = p1 - q0;
-  unsigned *k32 = reinterpret_cast<unsigned *>(w.k0);
-  unsigned *lk = reinterpret_cast<unsigned *>(w.k1), *lk_alt = lk + n;
-  int *idx = w.v0, *idx_alt = w.v1, *runs = w.v2;
-  unsigned *hist = reinterpret_cast<unsigned *>(w.head);
-  SelState *st = reinterpret_cast<SelState *>(w.partial);
+  SlabWS w;
+  if (!carve_slab(ar, n, m, w)) return H3D_E_ARG;
+  const unsigned G = h3d_grid(n, 256) > 4096 ? 4096 : h3d_grid(n, 256);
+  unsigned *k32 = w.k32;
+  unsigned *lk = w.lk, *lk_alt = w.lk_alt;
+  int *idx = w.idx, *idx_alt = w.idx_alt, *runs = w.runs;
+  unsigned *hist = w.hist;
+  SelState *st = w.st;
   SelState init{};
   init.b[0] = q0 > 0 ? q0 : -1;
   init.b[1] = p1 < n ? p1 : -1;
@@ -996,13 +1071,13 @@ int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1, i
     }
   }
   h3d_count_launches(3);
-  k_sel_compact<<<1184, 256, 0, s>>>(k32, n, st, idx, runs);
-  k_sel_runs<<<1, 256, 0, s>>>(pts, k32, st, runs, idx);
+  k_sel_compact<<<1184, 256, 0, s>>>(k32, n, st, idx, runs, m);
+  k_sel_runs<<<1, 256, 0, s>>>(pts, k32, st, runs, idx, m);
   const unsigned Gm = h3d_grid(m, 256) > 4096 ? 4096 : h3d_grid(m, 256);
   k_sel_keys<<<Gm, 256, 0, s>>>(k32, st, idx, lk, m);
   bool alt = false;
   h3d_count_launches(5);
-  if (h3d_check(prim::rs_sort_pairs<unsigned>(w.cub_tmp, w.cub_bytes, lk, idx, lk_alt, idx_alt, m, 0, 32,
+  if (h3d_check(prim::rs_sort_pairs<unsigned>(w.tmp, w.tmp_bytes, lk, idx, lk_alt, idx_alt, m, 0, 32,
                                               &alt, s)))
     return H3D_E_CUDA;
   unsigned *kcur = alt ? lk_alt : lk;
@@ -1017,7 +1092,7 @@ int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1, i
   if (h3d_check(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s)))
     return H3D_E_CUDA;
   if (scan) {  // _scan_degenerate over this window (rank 0: rows [0, p1))
-    if (!degenerate_scan(sorted_pts, p1, w, G, &hs, hflag, 3, s)) return H3D_E_CUDA;
+    if (!degenerate_scan(sorted_pts, p1, w.scan, w.flag, G, &hs, hflag, 3, s)) return H3D_E_CUDA;
   } else if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
              h3d_check(cudaStreamSynchronize(s))) {
     return H3D_E_CUDA;
@@ -1037,8 +1112,8 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n, const int64_t *
                             size_t workspace_bytes, void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h3d_arena ar(workspace, workspace_bytes);
-  PresortWS w;
-  if (!carve(ar, n, w)) return H3D_E_ARG;
+  EpiWS w;
+  if (!carve_epi(ar, n, w)) return H3D_E_ARG;
   if (nfaces == 0) return H3D_E_NOFACETS;
   h3d_count_launches(1);
   k_colsum<<<kColsumBlocks, 256, 0, s>>>(centroid_pts ? centroid_pts : sorted_pts, n, w.partial);
@@ -1051,7 +1126,7 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n, const int64_t *
                              faces_raw, nfaces, reinterpret_cast<long long *>(faces),
                              vertex_mark);
   h3d_count_launches(3);
-  if (h3d_check(prim::select_flagged(w.cub_tmp, w.cub_bytes, vertex_mark, n,
+  if (h3d_check(prim::select_flagged(w.tmp, w.tmp_bytes, vertex_mark, n,
                                      reinterpret_cast<long long *>(vertices), w.count, s)))
     return H3D_E_CUDA;
   long long cnt = 0;

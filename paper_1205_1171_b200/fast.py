@@ -157,7 +157,7 @@ def run_both(sorted_pts: torch.Tensor, stamps: bool = False):
     s = stream_ptr(dev)
     wsb = int(L.h3d_fast_pass_workspace_bytes(n))
     ws_lo = _WS.get(dev, 0, wsb)
-    ws_up = _WS.get(dev, 1, wsb)
+    ws_up = _WS.get(dev, 1, int(L.h3d_fast_upper_workspace_bytes(n)))
     # err, kLo, kUp, verify diagnostics, then the level stamps
     state = torch.zeros(4 + (STAMP_SLOTS if stamps else 0), dtype=torch.int64, device=dev)
     err = state[0:1]
@@ -229,7 +229,7 @@ def hull(pts: torch.Tensor, stamps: bool = True) -> HullOut:
     wsb = int(L.h3d_fast_pass_workspace_bytes(n))
     pwsb = int(L.h3d_presort_workspace_bytes(n))
     ws_lo = _WS.get(dev, 0, wsb)
-    ws_up = _WS.get(dev, 1, wsb)
+    ws_up = _WS.get(dev, 1, int(L.h3d_fast_upper_workspace_bytes(n)))
     pws = _WS.get(dev, 2, pwsb)
     cap = 2 * n
     # outputs and scratch, carved from one cached buffer per device

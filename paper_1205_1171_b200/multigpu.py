@@ -235,50 +235,78 @@ SHARDED_RUNS = [0]  # hulls whose presort ran sharded (tests check it is taken)
 
 def sharded_presort(pts_dev: torch.Tensor, plan: "SlabPlan", rank: int):
     """Every rank sorts only its own slab (plus the row before it, for the
-    tie test across the boundary) with h3d_presort_slab; rank 0 also runs the
-    degeneracy scan.  Returns (sorted_pts, order) -- full-size arrays of which
-    only the rank's window is filled -- or None on every rank when any rank's
+    tie test across the boundary) with h3d_presort_slab into WINDOW-sized
+    buffers; rank 0 also runs the degeneracy scan.  Returns the rank's slab
+    rows and caller indices (rows [p0, p1) of the global sorted order; None
+    for a rank without a slab), or False on every rank when any rank's
     window cannot reproduce the replicated presort (ties, long key runs,
     non-finite input, undecided degeneracy)."""
     import os
 
     import torch.distributed as dist
 
-    from .api import _Workspace
     from .engine import stream_ptr
+    from .fast import _WS
 
     L = _lib.load()
     n = pts_dev.shape[0]
     dev = pts_dev.device
-    if os.environ.get("H3D_DIST_POISON"):  # tests: unfilled rows must never be read
-        sorted_pts = torch.full((n, 3), float("nan"), dtype=torch.float64, device=dev)
-        order = torch.full((n,), -1, dtype=torch.int64, device=dev)
-    else:
-        sorted_pts = torch.empty((n, 3), dtype=torch.float64, device=dev)
-        order = torch.empty(n, dtype=torch.int64, device=dev)
     code = 0
+    local = None
     sl = plan.slab(rank)
     if sl is not None:
-        ws = _Workspace.get(dev, int(L.h3d_presort_workspace_bytes(n)))
-        code = int(L.h3d_presort_slab(pts_dev.data_ptr(), n, max(0, sl[0] - 1), sl[1],
-                                      1 if rank == 0 else 0, sorted_pts.data_ptr(),
-                                      order.data_ptr(), ws.data_ptr(), ws.numel(),
-                                      stream_ptr(dev)))
+        p0, p1 = sl
+        q0 = max(0, p0 - 1)
+        m = p1 - q0
+        if os.environ.get("H3D_DIST_POISON"):  # tests: unfilled rows must never be read
+            rows = torch.full((m, 3), float("nan"), dtype=torch.float64, device=dev)
+            order = torch.full((m,), -1, dtype=torch.int64, device=dev)
+        else:
+            rows = torch.empty((m, 3), dtype=torch.float64, device=dev)
+            order = torch.empty(m, dtype=torch.int64, device=dev)
+        ws = _WS.get(dev, 5, int(L.h3d_presort_slab_workspace_bytes(n, m)))
+        # the window buffers are passed q0 rows before their start: the
+        # function only touches global rows [q0, p1)
+        code = int(L.h3d_presort_slab(pts_dev.data_ptr(), n, q0, p1, 1 if rank == 0 else 0,
+                                      rows.data_ptr() - 24 * q0, order.data_ptr() - 8 * q0,
+                                      ws.data_ptr(), ws.numel(), stream_ptr(dev)))
+        local = (rows[p0 - q0:], order[p0 - q0:])
     flag = torch.tensor([1 if code != 0 else 0], dtype=torch.int64,
                         device="cpu" if _p2p_via_host() else dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MAX)
     if int(flag.item()) != 0:
-        return None
+        return False
     SHARDED_RUNS[0] += 1
-    return sorted_pts, order
+    return local
+
+
+def _pow2_at_least(x: int) -> int:
+    p = 1
+    while p < x:
+        p <<= 1
+    return p
 
 
 def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
-    """Both passes of the hull over x-slabs.  Every rank passes the same
-    input (caller order, on its own device).  Returns on rank 0 the same
-    tuple as fast.run_both plus (sorted points, order, perturbed, sharded);
-    None on the other ranks; None on rank 0 too when the exact engine must
-    take over."""
+    """Both passes of the hull over x-slabs with O(n / G) state per rank.
+    Every rank passes the same input (caller order, on its own device).
+
+    * The slab levels run on the rank's slab as a problem of its own (its
+      rows [p0, p1) only; the merge tree inside a slab is the global one,
+      slabs being aligned level-(L - log2 G) groups).
+    * The cross levels run in a small VIRTUAL space: every slab's final
+      group is relocated to virtual points [r*C, r*C + C), C = a power of two
+      >= twice the largest slab group (its kept points of both passes); with
+      n_v = (non-empty slabs) * C the virtual tree has the real tree's
+      merges and carries at the last log2 G levels, and the merged logs are
+      the real ones (events carry group-local ids; a job's span only bounds
+      its bridge walk and log size, both far above any group's kept points).
+      Group ids of the virtual space index rows_v/order_v (the kept points'
+      sorted rows and caller indices), which travel with the groups.
+
+    Returns on rank 0 (raw faces in virtual ids, lower and upper counts,
+    rows_v, order_v, perturbed, sharded, memory report); None on the other
+    ranks; None on rank 0 too when the exact engine must take over."""
     import torch.distributed as dist
 
     from .api import presort
@@ -291,6 +319,7 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
     s = stream_ptr(dev)
     plan = SlabPlan(n, world)
     marks = []  # (name, event) phase boundaries, only when PHASES is set
+    mem: dict = {}
 
     def mark(name):
         if PHASES is not None:
@@ -299,39 +328,101 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
             marks.append((name, e))
 
     mark("start")
-    sh = sharded_presort(pts_dev, plan, rank) if n >= SHARD_PRESORT_MIN else None
-    if sh is not None:
-        (sorted_pts, order), perturbed = sh, False
-        rows = sh
-    else:
-        sorted_pts, order, perturbed = presort(pts_dev)
-        rows = None
-    wsb = int(L.h3d_fast_pass_workspace_bytes(n))
-    ws = [_WS.get(dev, 0, wsb), _WS.get(dev, 1, wsb)]
-    lays = [GroupLayout(ws[0], n), GroupLayout(ws[1], n)]
+    sl = plan.slab(rank)
+    sh = sharded_presort(pts_dev, plan, rank) if n >= SHARD_PRESORT_MIN else False
+    perturbed = False
+    if sh is not False:
+        local = sh
+    else:  # the replicated presort (ties, long key runs, small n): O(n), rare
+        full_rows, full_order, perturbed = presort(pts_dev)
+        local = (full_rows[sl[0]:sl[1]], full_order[sl[0]:sl[1]]) if sl is not None else None
+    mark("presort")
     state = torch.zeros(4, dtype=torch.int64, device=dev)
     err = state[0:1]
-    sl = plan.slab(rank)
-    mark("presort")
+    # ---- slab levels: the slab as a cloud of its own
+    U = None
     if sl is not None:
-        r = L.h3d_fast_passes_range(sorted_pts.data_ptr(), n, sl[0], sl[1], 1, plan.slab_level,
-                                    ws[0].data_ptr(), ws[1].data_ptr(), wsb, err.data_ptr(), 0, s)
-        if r < 0:
-            err.fill_(int(r))
+        rows_loc, order_loc = local
+        n_r = sl[1] - sl[0]
+        if n_r >= 2:
+            wsb = int(L.h3d_fast_pass_workspace_bytes(n_r))
+            ws_s = [_WS.get(dev, 0, wsb), _WS.get(dev, 1, int(L.h3d_fast_upper_workspace_bytes(n_r)))]
+            mem["slab_passes"] = wsb + int(L.h3d_fast_upper_workspace_bytes(n_r))
+            r = L.h3d_fast_passes_range(rows_loc.data_ptr(), n_r, 0, n_r, 1, plan.slab_level,
+                                        ws_s[0].data_ptr(), ws_s[1].data_ptr(), wsb,
+                                        err.data_ptr(), 0, s)
+            if r < 0:
+                err.fill_(int(r))
+                r = 0
+            lays_s = [GroupLayout(ws_s[0], n_r), GroupLayout(ws_s[1], n_r)]
+            buf_s = int(r)
+            hdr = group_header(lays_s, buf_s, 0).cpu().tolist()
+            if int(err.item()) != 0:
+                # a declined slab level wrote nothing valid: relocate an empty
+                # group (the error flag sends the hull to the exact engine)
+                parts = [(0, 0, torch.zeros(0, dtype=torch.int32, device=dev))] * 2
+            else:
+                parts = []
+                for p, lay in enumerate(lays_s):
+                    nS, k = _sizes(hdr, p, plan.slab_level)
+                    parts.append((nS, k, lay.gid_view(buf_s, 0, nS).view(torch.int32)))
+            U = torch.unique(torch.cat([g for _, _, g in parts]).long())  # sorted = x order
+        else:  # a one-point slab: its group is the point itself
+            parts = [(1, 0, torch.zeros(1, dtype=torch.int32, device=dev))] * 2
+            U = torch.zeros(1, dtype=torch.int64, device=dev)
+            lays_s, buf_s = None, 0
     mark("slab_levels")
-    for lv in range(plan.slab_level + 1, plan.levels + 1):
-        role, peer = plan.role(lv, rank)
-        prev_buf = (lv - 1) & 1
+    # ---- the virtual space of the cross levels
+    u_cnt = torch.tensor([0 if U is None else int(U.numel())], dtype=torch.int64,
+                         device="cpu" if _p2p_via_host() else dev)
+    dist.all_reduce(u_cnt, op=dist.ReduceOp.MAX)
+    C = _pow2_at_least(max(2, 2 * int(u_cnt.item())))
+    G_eff = (n + plan.S - 1) // plan.S  # non-empty slabs
+    n_v = G_eff * C
+    lev_c = C.bit_length() - 1
+    levels_v = (n_v - 1).bit_length()
+    wsb_v = int(L.h3d_fast_pass_workspace_bytes(n_v))
+    ws_v = [_WS.get(dev, 6, wsb_v), _WS.get(dev, 7, int(L.h3d_fast_upper_workspace_bytes(n_v)))]
+    mem["cross_passes"] = wsb_v + int(L.h3d_fast_upper_workspace_bytes(n_v))
+    lays_v = [GroupLayout(ws_v[0], n_v), GroupLayout(ws_v[1], n_v)]
+    rows_v = torch.full((n_v, 3), float("nan"), dtype=torch.float64, device=dev)
+    order_v = torch.full((n_v,), -1, dtype=torch.int64, device=dev)
+    mem["cross_rows"] = 32 * n_v
+    buf_v = lev_c & 1
+    if sl is not None:
+        base = rank * C
+        u = int(U.numel())
+        rows_v[base:base + u] = rows_loc.index_select(0, U)
+        order_v[base:base + u] = order_loc.index_select(0, U)
+        for p, lay in enumerate(lays_v):
+            nS, k, gid = parts[p]
+            vid = (base + torch.searchsorted(U, gid.long())).to(torch.int32)
+            lay.gid_view(buf_v, base, nS).copy_(vid.view(torch.uint8))
+            if lays_s is not None:
+                if nS:
+                    lay.lnk_view(buf_v, base, nS).copy_(lays_s[p].lnk_view(buf_s, 0, nS))
+                if k:
+                    lay.ev_view(buf_v, base, k).copy_(lays_s[p].ev_view(buf_s, 0, k))
+            else:
+                lay.lnk_view(buf_v, base, 1).copy_(
+                    torch.tensor([-1, -1], dtype=torch.int32, device=dev).view(torch.uint8))
+            lay.hdr_view(buf_v, rank).copy_(torch.tensor([nS, k], dtype=torch.int32,
+                                                         device=dev).view(torch.uint8))
+    rows = (rows_v, order_v)
+    for t in range(1, levels_v - lev_c + 1):
+        lv_v = lev_c + t
+        role, peer = plan.role(plan.slab_level + t, rank)
+        prev_buf = (lv_v - 1) & 1
         if role == "send":
-            send_group(lays, prev_buf, lv - 1, (rank * plan.S) >> (lv - 1), peer, rows)
+            send_group(lays_v, prev_buf, lv_v - 1, (rank * C) >> (lv_v - 1), peer, rows)
         elif role in ("merge", "carry"):
             if role == "merge":
-                recv_group(lays, prev_buf, lv - 1, (peer * plan.S) >> (lv - 1), peer, rows)
-            p0 = rank * plan.S
-            p1 = min(n, p0 + (1 << lv))
-            r = L.h3d_fast_passes_range(sorted_pts.data_ptr(), n, p0, p1, lv, lv,
-                                        ws[0].data_ptr(), ws[1].data_ptr(), wsb, err.data_ptr(),
-                                        0, s)
+                recv_group(lays_v, prev_buf, lv_v - 1, (peer * C) >> (lv_v - 1), peer, rows)
+            p0 = rank * C
+            p1 = min(n_v, p0 + (1 << lv_v))
+            r = L.h3d_fast_passes_range(rows_v.data_ptr(), n_v, p0, p1, lv_v, lv_v,
+                                        ws_v[0].data_ptr(), ws_v[1].data_ptr(), wsb_v,
+                                        err.data_ptr(), 0, s)
             if r < 0:
                 err.fill_(int(r))
     mark("cross_levels")
@@ -347,17 +438,44 @@ def hull_distributed(pts_dev: torch.Tensor, rank: int, world: int):
         return None
     if int(flag.item()) != 0:
         return None
-    final = plan.levels & 1
-    cap = max(2 * n, 8)
+    final = levels_v & 1
+    cap = max(2 * n_v, 8)
     faces = torch.empty((cap, 3), dtype=torch.int32, device=dev)
     counts = state[1:3]
-    L.h3d_fast_extract(ws[0].data_ptr(), ws[1].data_ptr(), n, final, final, faces.data_ptr(), cap,
-                       counts.data_ptr(), err.data_ptr(), s)
+    L.h3d_fast_extract(ws_v[0].data_ptr(), ws_v[1].data_ptr(), n_v, final, final, faces.data_ptr(),
+                       cap, counts.data_ptr(), err.data_ptr(), s)
     h = state.cpu()
     if int(h[0]) != 0:
         return None
     k_lo, k_up = int(h[1]), int(h[2])
-    return faces[: k_lo + k_up], k_lo, k_up, sorted_pts, order, perturbed, rows is not None
+    mem["virtual"] = {"C": C, "n_v": n_v}
+    return faces[: k_lo + k_up], k_lo, k_up, rows_v, order_v, perturbed, sh is not False, mem
+
+
+def rank_memory_bytes(n: int, world: int, kept_max: int | None = None) -> dict:
+    """Device bytes one rank holds for an n-point hull on `world` GPUs
+    (host arithmetic from the library's sizing functions): the replicated
+    input and presort keys are O(n); everything else O(n / G) plus the
+    virtual cross-level space (C per slab, C >= 2 * the largest slab group;
+    kept_max defaults to a tenth of a slab)."""
+    L = _lib.load()
+    plan = SlabPlan(n, world)
+    S = plan.S
+    m = min(S + 1, n)
+    kept = kept_max if kept_max is not None else max(2, S // 10)
+    C = _pow2_at_least(2 * kept)
+    n_v = ((n + S - 1) // S) * C
+    out = {
+        "input_replica": 24 * n,
+        "slab_presort_ws": int(L.h3d_presort_slab_workspace_bytes(n, m)),
+        "slab_rows": 32 * m,
+        "slab_passes": int(L.h3d_fast_pass_workspace_bytes(S) + L.h3d_fast_upper_workspace_bytes(S)),
+        "cross_passes": int(L.h3d_fast_pass_workspace_bytes(n_v) + L.h3d_fast_upper_workspace_bytes(n_v)),
+        "cross_rows": 32 * n_v,
+        "epilogue_rank0": int(L.h3d_epilogue_workspace_bytes(n)) + 12 * n + 48 * n_v,
+    }
+    out["total"] = sum(out.values())
+    return out
 
 
 GATHER_INPUT_MIN = 1 << 16
@@ -425,11 +543,11 @@ def convex_hull_3d_distributed(points, device=None, return_device: bool = False)
     with _device_lock(dev), torch.cuda.device(dev):
         res = hull_distributed(pts, rank, world)
         if rank == 0 and res is not None:
-            raw, k_lo, k_up, sorted_pts, order, perturbed, sharded = res
-            # sharded presort: rank 0 holds only the rows its merges touched,
-            # so the centroid is taken over the caller-order input (same
-            # points)
-            verts, faces = orient_remap(sorted_pts, order, raw, pts if sharded else None)
+            raw, k_lo, k_up, rows_v, order_v, perturbed, sharded, _mem = res
+            # faces index the virtual rows; the centroid is taken over the
+            # caller-order input (the same points) and the vertex marks over
+            # the caller indices
+            verts, faces = orient_remap(rows_v, order_v, raw, pts, n_callers=n)
     if rank != 0:
         return None
     if res is None:  # exact engine, single GPU, reference semantics (takes the lock itself)

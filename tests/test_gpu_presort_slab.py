@@ -12,7 +12,7 @@ import pytest
 import torch
 
 from paper_1205_1171_b200 import _lib
-from paper_1205_1171_b200.api import _Workspace, presort
+from paper_1205_1171_b200.api import presort
 from paper_1205_1171_b200.engine import stream_ptr
 
 pytestmark = pytest.mark.gpu
@@ -21,14 +21,24 @@ E_FASTPATH = -13
 
 
 def slab(pts: torch.Tensor, q0: int, p1: int, scan: int):
+    """The window through WINDOW-sized buffers (passed q0 rows before their
+    start, as the multi-GPU path does) and the slim slab workspace; returned
+    embedded in full-size NaN / -1 arrays for the comparisons."""
     L = _lib.load()
     n = pts.shape[0]
+    m = p1 - q0
+    wsp = torch.full((m, 3), float("nan"), dtype=torch.float64, device=pts.device)
+    wod = torch.full((m,), -1, dtype=torch.int64, device=pts.device)
+    ws = torch.empty(int(L.h3d_presort_slab_workspace_bytes(n, m)), dtype=torch.uint8,
+                     device=pts.device)
+    code = int(L.h3d_presort_slab(pts.data_ptr(), n, q0, p1, scan, wsp.data_ptr() - 24 * q0,
+                                  wod.data_ptr() - 8 * q0, ws.data_ptr(), ws.numel(),
+                                  stream_ptr(pts.device)))
+    torch.cuda.synchronize()
     sp = torch.full((n, 3), float("nan"), dtype=torch.float64, device=pts.device)
     od = torch.full((n,), -1, dtype=torch.int64, device=pts.device)
-    ws = _Workspace.get(pts.device, int(L.h3d_presort_workspace_bytes(n)))
-    code = int(L.h3d_presort_slab(pts.data_ptr(), n, q0, p1, scan, sp.data_ptr(), od.data_ptr(),
-                                  ws.data_ptr(), ws.numel(), stream_ptr(pts.device)))
-    torch.cuda.synchronize()
+    sp[q0:p1] = wsp
+    od[q0:p1] = wod
     return code, sp, od
 
 

@@ -179,3 +179,18 @@ def test_group_rows_and_input_gather_gloo():
     assert np.array_equal(od0[moved], od1[moved])
     assert np.array_equal(sp0[moved], sp1[moved])
     assert np.isnan(sp0[~moved]).all()
+
+
+def test_rank_memory_shrinks_with_world():
+    """Per-rank device memory of the x-slab hull is O(n / G) apart from the
+    replicated input and 32-bit presort keys (host arithmetic from the
+    library's sizing functions; C5 = 2^27 points, its slab groups ~2^17)."""
+    from paper_1205_1171_b200.multigpu import rank_memory_bytes
+
+    one = rank_memory_bytes(2**27, 1, 2**20)
+    eight = rank_memory_bytes(2**27, 8, 2**17)
+    assert eight["total"] < one["total"] / 4
+    assert eight["slab_passes"] <= one["slab_passes"] / 8 + 3 * 2**30  # + the fixed big-job scratch
+    assert eight["total"] < 20 * 2**30
+    # the O(n) parts are the input replica and the keys only
+    assert eight["input_replica"] == 24 * 2**27

@@ -61,8 +61,7 @@ def worker(rank, world, port, cases):
                 print("rank0", n, kind, seed, "faces", len(r.faces), "same as 1 GPU:", same, flush=True)
         except Exception as exc:
             import traceback
-            if rank == 0:
-                traceback.print_exc()
+            traceback.print_exc()
             print(f"rank {rank} case {(n, kind, seed)}: {type(exc).__name__}: {exc}", flush=True)
             os._exit(1)
     dist.destroy_process_group()
