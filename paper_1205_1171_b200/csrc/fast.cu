@@ -27,8 +27,11 @@
 // point's gid and kernels read the sorted point array (z negated on the
 // upper pass).
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -559,9 +562,12 @@ template <bool XYZ>
 __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int level, long long j0,
                                                  long long j1, long long *err, int pool,
-                                                 int jpc, int prefetch) {
-  // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
-  if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0)) return;
+                                                 int jpc, int prefetch, long long *spec) {
+  // an earlier level failed, or (a replayed plan, spec) did not fit: stop
+  // (warp-uniform; the words it reads may be stale)
+  if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0 ||
+                                  (spec && *reinterpret_cast<volatile long long *>(spec) != 0)))
+    return;
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   const double zs = blockIdx.y ? -1.0 : 1.0;
@@ -593,8 +599,11 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
     }
   }
   const int nS = nSL + nSR;
-  if (merge && nS >= 0x7fff) {  // int16 local ids; the host never routes such jobs here
-    raise_err(err, E_FASTPATH);
+  if (merge && nS >= 0x7fff) {  // int16 local ids; the host never routes such jobs here ...
+    if (spec)  // ... unless it replays a plan: report the level, it is redone measured
+      atomicCAS(reinterpret_cast<unsigned long long *>(spec), 0ull, static_cast<unsigned long long>(level));
+    else
+      raise_err(err, E_FASTPATH);
     merge = false;
   }
   // pack the slices: warp exclusive prefix sum of the slice sizes
@@ -606,8 +615,13 @@ __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restri
   }
   const int total = __shfl_sync(FULL, off, 31);
   off -= bytes;
-  if (total > pool) {  // the host sizes the pool from the measured need
-    if (lane == 0) raise_err(err, E_FASTPATH);
+  if (total > pool) {  // the host sizes the pool from the measured need (or a replayed plan's)
+    if (lane == 0) {
+      if (spec)
+        atomicCAS(reinterpret_cast<unsigned long long *>(spec), 0ull, static_cast<unsigned long long>(level));
+      else
+        raise_err(err, E_FASTPATH);
+    }
     return;
   }
   // per-job metadata for the cooperative phases (shared, no shuffles); the
@@ -1563,6 +1577,43 @@ long long kTpjPrefetchJobs = 1ll << 18;  // H3D_TPJ_PREFETCH: L2 prefetch of row
 // leaf kernel depth: 3 or 4 fused levels, anything below 3 = off
 int leaf_depth(long long b) { return b >= 4 ? 4 : (b == 3 ? 3 : 0); }
 
+// ---- level plans: record & replay of the routing.  A call that measured
+// every level records what it launched (route + launch parameters); the next
+// call with the same point range launches that plan WITHOUT the per-level
+// measurement and read-back.  Every replayed kernel checks that its jobs fit
+// the recorded launch (shared-memory pool, jobs per CTA, job size caps); a
+// level that does not fit writes nothing, records its level in a device
+// flag, and every later replayed launch exits at once -- after the single
+// read-back at the end of the replay the loop resumes, measured, from that
+// level (its input buffer is intact).  Results never depend on the plan:
+// every route reproduces the reference's logs.
+enum { REC_MINI = 0, REC_LANE = 1, REC_TPJ = 2, REC_WARP = 3, REC_BIG = 4 };
+struct LevelRec {
+  int lv, kind, variant, jpc, prefetch;
+  long long pool;
+  LaneCfg lane;
+};
+struct PlanKey {
+  int dev;
+  long long n, p0, p1;
+  int lo, hi;
+  bool operator<(const PlanKey &o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (n != o.n) return n < o.n;
+    if (p0 != o.p0) return p0 < o.p0;
+    if (p1 != o.p1) return p1 < o.p1;
+    if (lo != o.lo) return lo < o.lo;
+    return hi < o.hi;
+  }
+};
+std::mutex g_plan_mu;
+std::map<PlanKey, std::vector<LevelRec>> g_plans;
+int g_plan = 1;  // H3D_PLAN: replay recorded level plans (0 = measure every level)
+void plans_clear() {
+  std::lock_guard<std::mutex> g(g_plan_mu);
+  g_plans.clear();
+}
+
 // tuning knobs from the environment (read once; h3d_tune overrides)
 void load_env_once() {
   if (g_env_done) return;
@@ -1588,14 +1639,16 @@ void load_env_once() {
   if (const char *e = getenv("H3D_LANE_XYZ_KB")) g_lane_xyz_max = atoll(e) * 1024;
   if (const char *e = getenv("H3D_LANE_STAGE")) g_lane_stage = atoi(e);
   if (const char *e = getenv("H3D_TPJ_PREFETCH")) kTpjPrefetchJobs = atoll(e);
+  if (const char *e = getenv("H3D_PLAN")) g_plan = atoi(e) ? 1 : 0;
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
 template <bool XYZ>
 void launch_tpj(dim3 grid, int pool, int jpc, int prefetch, cudaStream_t s, Pass2 P,
                 const double *pts,
-                long long n, int lv, long long j0, long long j1, long long *err) {
-  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch);
+                long long n, int lv, long long j0, long long j1, long long *err,
+                long long *spec = nullptr) {
+  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec);
 }
 
 }  // namespace
@@ -1606,6 +1659,8 @@ int64_t h3d_tune(const char *name, int64_t value) {
   load_env_once();
   const std::string k(name ? name : "");
   long long old = -1;
+  if (value >= 0) plans_clear();  // recorded plans follow the knobs they were made with
+  if (k == "plan") { old = g_plan; if (value >= 0) g_plan = value ? 1 : 0; }
   if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
   else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = leaf_depth(value); }
   else if (k == "mini") { old = g_mini; if (value >= 0) g_mini = value ? 1 : 0; }
@@ -1736,6 +1791,79 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     P = Pass2{P.out0, P.out1, P.in0, P.in1};
     lv = 2;
   }
+  // ---- replay the level plan the last call with this point range recorded
+  std::vector<LevelRec> rec;  // this call's launches: the next call's plan
+  const PlanKey key{dev_id, n, p0, p1, lv_lo, lv_hi};
+  if (g_plan && lv <= lv_hi) {
+    std::vector<LevelRec> plan;
+    {
+      std::lock_guard<std::mutex> g(g_plan_mu);
+      auto it = g_plans.find(key);
+      if (it != g_plans.end()) plan = it->second;
+    }
+    if (!plan.empty() && plan.front().lv == lv) {
+      long long *spec = reinterpret_cast<long long *>(w0.need + 12);
+      cudaMemsetAsync(spec, 0, sizeof(long long), s);
+      const int lv_start = lv;
+      for (const LevelRec &r : plan) {
+        if (r.lv != lv || lv > lv_hi || r.kind == REC_BIG) break;
+        if (lv > lv_lo) check(P, lv - 1, spec);
+        const long long j0 = p0 >> lv, j1 = (p1 + (1ll << lv) - 1) >> lv;
+        h3d_stamp_now(s, lv);
+        void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
+        int tag = lv;
+        long long rc = 0;
+        if (r.kind == REC_MINI) {
+          tag = lv + 5000;
+          rc = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, r.variant, spec, nullptr, big_ws, big_bytes);
+        } else if (r.kind == REC_LANE) {
+          tag = lv + 1000;
+          void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
+          LaneCfg c = r.lane;
+          rc = lane_level(P, sorted_pts, n, lv, j0, j1, err, nullptr, s, &c, spec);
+          h3d_prof_end(ek, tag, 2, s);
+        } else if (r.kind == REC_TPJ) {
+          tag = lv + 1000;
+          void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
+          h3d_count_launches(1);
+          const dim3 grid(h3d_grid(j1 - j0, r.jpc), 2);
+          if (r.variant)
+            launch_tpj<true>(grid, static_cast<int>(r.pool), r.jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err,
+                             spec);
+          else
+            launch_tpj<false>(grid, static_cast<int>(r.pool), r.jpc, r.prefetch, s, P, sorted_pts, n, lv, j0,
+                              j1, err, spec);
+          h3d_prof_end(ek, tag, 2, s);
+        } else {  // REC_WARP: an oversized job runs in HBM mode, always fits
+          h3d_count_launches(1);
+          k_fast_warp<1><<<dim3(h3d_grid(j1 - j0, 1), 2), 32, r.pool, s>>>(
+              P, sorted_pts, n, lv, j0, j1, err, static_cast<int>(r.pool), w0.seq, w1.seq, w0.rec, w1.rec);
+        }
+        if (rc < 0) return rc;
+        h3d_prof_end(e0, tag, 2, s);
+        h3d_stamp_route(lv, tag);
+        rec.push_back(r);
+        P = Pass2{P.out0, P.out1, P.in0, P.in1};
+        ++lv;
+      }
+      // the replay's one read-back: the first level that did not fit, the error word
+      long long hv[2] = {0, 0};
+      if (h3d_check(cudaMemcpyAsync(&hv[0], spec, sizeof(long long), cudaMemcpyDeviceToHost, s)) ||
+          h3d_check(cudaMemcpyAsync(&hv[1], err, sizeof(long long), cudaMemcpyDeviceToHost, s)) ||
+          h3d_check(cudaStreamSynchronize(s)))
+        return H3D_E_CUDA;
+      if (hv[1] != 0) {
+        lv = lv_hi + 2;  // declined: the caller sees the error word
+      } else if (hv[0] != 0) {
+        // redo from the level that did not fit: it reads buffer (f-1)&1, intact
+        const int f = static_cast<int>(hv[0]);
+        rec.resize(f - lv_start);
+        lv = f;
+        P = (f & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
+        if (g_trace) fprintf(stderr, "h3d plan replay: level %d did not fit, measured from there\n", f);
+      }
+    }
+  }
   for (; lv <= lv_hi; ++lv) {
     if (lv > lv_lo) check(P, lv - 1);  // the previous level's groups
     // the jobs of this level inside the point range [p0, p1)
@@ -1780,6 +1908,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     if (g_mini && mini_tiny) {
       const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, 2);
       if (rm < 0) return rm;
+      rec.push_back(LevelRec{lv, REC_MINI, 2, 0, 0, 0, LaneCfg{}});
       h3d_prof_end(e0, lv + 5000, 2, s);
       h3d_stamp_route(lv, lv + 5000);
       P = Pass2{P.out0, P.out1, P.in0, P.in1};
@@ -1791,6 +1920,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           maxkin <= kMiniMaxEvents))) {
       const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, mini_small ? 0 : 1);
       if (rm < 0) return rm;
+      rec.push_back(LevelRec{lv, REC_MINI, mini_small ? 0 : 1, 0, 0, 0, LaneCfg{}});
       h3d_prof_end(e0, lv + 5000, 2, s);
       h3d_stamp_route(lv, lv + 5000);
       P = Pass2{P.out0, P.out1, P.in0, P.in1};
@@ -1807,6 +1937,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
                                           (p1 + (1ll << l2) - 1) >> l2, err, s, 1, spec,
                                           h3d_stamp_buf() ? h3d_stamp_buf() + l2 : nullptr);
           if (rs < 0) return rs;
+          rec.push_back(LevelRec{l2, REC_MINI, 1, 0, 0, 0, LaneCfg{}});
           if (g_trace) {
             long long f = 0;
             cudaMemcpyAsync(&f, spec, sizeof(f), cudaMemcpyDeviceToHost, s);
@@ -1825,19 +1956,20 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
             h3d_check(cudaStreamSynchronize(s)))
           return H3D_E_CUDA;
         if (serr != 0) {
-          lv = lv_hi;
+          lv = lv_hi + 2;  // declined: nothing more to check or record
           break;
         }
         if (g_trace)
           fprintf(stderr, "h3d levels %d..%d speculative on the large mini: failed at %lld\n",
                   lv + 1, lv_hi, failed);
         if (failed == 0) {
-          lv = lv_hi;
+          lv = lv_hi + 3;  // every level done (each chain level checked above)
           break;
         }
         // redo from the failed level: it reads buffer (f-1)&1, intact
         const int f = static_cast<int>(failed);
         P = (f & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
+        while (!rec.empty() && rec.back().lv >= f) rec.pop_back();
         lv = f - 1;
       }
       continue;
@@ -1851,6 +1983,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
                                       big_ws, big_bytes);
       if (rm < 0) return rm;
       if (rm == 0) {
+        rec.push_back(LevelRec{lv, REC_MINI, 3, 0, 0, 0, LaneCfg{}});
         h3d_prof_end(e0, lv + 5000, 2, s);
         h3d_stamp_route(lv, lv + 5000);
         P = Pass2{P.out0, P.out1, P.in0, P.in1};
@@ -1866,6 +1999,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       const long long rb = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s);
       if (rb < 0) return rb;
       if (rb == 0) {
+        rec.push_back(LevelRec{lv, REC_BIG, 0, 0, 0, 0, LaneCfg{}});
         h3d_prof_end(e0, lv + 4000, 2, s);
       h3d_stamp_route(lv, lv + 4000);
         P = Pass2{P.out0, P.out1, P.in0, P.in1};
@@ -1894,8 +2028,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     }
     if (tpj && g_lane && lv <= g_lane_max_level) {
       void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
-      const long long rl = lane_level(P, sorted_pts, n, lv, j0, j1, err, need, s);
+      LaneCfg lc{};
+      const long long rl = lane_level(P, sorted_pts, n, lv, j0, j1, err, need, s, &lc);
       if (rl < 0) return rl;
+      if (rl == 0) rec.push_back(LevelRec{lv, REC_LANE, 0, 0, 0, 0, lc});
       if (rl == 0) h3d_prof_end(ek, lv + 1000, 2, s); else h3d_prof_drop(ek);
       if (rl == 0) {
         h3d_prof_end(e0, lv + 1000, 2, s);
@@ -1914,6 +2050,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       else
         launch_tpj<false>(grid, static_cast<int>(pool), jpc, jobs >= kTpjPrefetchJobs ? 1 : 0, s, P,
                           sorted_pts, n, lv, j0, j1, err);
+      rec.push_back(LevelRec{lv, REC_TPJ, xyz ? 1 : 0, jpc, jobs >= kTpjPrefetchJobs ? 1 : 0, pool, LaneCfg{}});
       h3d_prof_end(ek, lv + 1000, 2, s);
       h3d_prof_end(e0, lv + 1000, 2, s);
       h3d_stamp_route(lv, lv + 1000);
@@ -1925,13 +2062,22 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       k_fast_warp<1><<<dim3(h3d_grid(jobs, 1), 2), 32, wpool, s>>>(
           P, sorted_pts, n, lv, j0, j1, err, static_cast<int>(wpool), w0.seq, w1.seq, w0.rec,
           w1.rec);
+      rec.push_back(LevelRec{lv, REC_WARP, 0, 0, 0, wpool, LaneCfg{}});
       h3d_prof_end(e0, lv, 2, s);
       h3d_stamp_route(lv, lv);
     }
     P = Pass2{P.out0, P.out1, P.in0, P.in1};
   }
-  if (lv > lv_hi && lv - 1 >= lv_lo) check(P, lv - 1);  // the last level (when the loop ran it)
+  // lv: lv_hi + 1 = the loop ran every level, lv_hi + 3 = the speculative
+  // chain did, lv_hi + 2 = declined, <= lv_hi = a level read an error word
+  if (lv == lv_hi + 1 && lv - 1 >= lv_lo) check(P, lv - 1);  // the last level
   h3d_stamp_now(s, H3D_STAMP_END);
+  // the next call with this point range replays what this one launched
+  // (only a complete record: a declined or failed run records nothing)
+  if (g_plan && (lv == lv_hi + 1 || lv == lv_hi + 3) && !rec.empty() && rec.back().lv == lv_hi) {
+    std::lock_guard<std::mutex> g(g_plan_mu);
+    g_plans[key] = rec;
+  }
   if (h3d_check(cudaGetLastError())) return H3D_E_CUDA;
   return lv_hi & 1;  // buffer holding the last level's groups
 }

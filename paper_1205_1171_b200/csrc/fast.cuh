@@ -221,9 +221,15 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
 // CTAs per SM); variant 1: <= 1024 points and 2048 events (~154 KB)
 // one level of both passes, one lane per job (lane.cu); need = the level's
 // measurement (k_tpj_need); returns 0, 1 (does not fit) or a negative code
+// the launch lane_level chose (variant v = 2 * xyz + staged, 32 >> r jobs per
+// CTA, pool bytes): recorded in a level plan, replayed with need == nullptr
+struct LaneCfg {
+  int v, r;
+  long long pool;
+};
 long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, const unsigned long long *need,
-                     cudaStream_t s);
+                     cudaStream_t s, LaneCfg *cfg = nullptr, long long *spec = nullptr);
 extern long long g_lane_xyz_max;  // lane.cu knobs
 extern int g_lane_stage;
 

@@ -329,9 +329,13 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
 template <bool XYZ>
 __global__ void __launch_bounds__(32) k_lane(Pass2 P, const double *__restrict__ pts, long long n,
                                              int level, long long j0, long long j1,
-                                             long long *err, int pool, int jpc, int stage) {
-  // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
-  if (__any_sync(FULL, *reinterpret_cast<volatile long long *>(err) != 0)) return;
+                                             long long *err, int pool, int jpc, int stage,
+                                             long long *spec) {
+  // an earlier level failed, or (a replayed plan, spec) did not fit: stop
+  // (warp-uniform; the words it reads may be stale)
+  if (__any_sync(FULL, *reinterpret_cast<volatile long long *>(err) != 0 ||
+                           (spec && *reinterpret_cast<volatile long long *>(spec) != 0)))
+    return;
   const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
   const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
   const double zs = blockIdx.y ? -1.0 : 1.0;
@@ -362,8 +366,11 @@ __global__ void __launch_bounds__(32) k_lane(Pass2 P, const double *__restrict__
     }
   }
   const int nS = nSL + nSR;
-  if (merge && nS >= 0x7fff) {  // int16 local ids; the host never routes such jobs here
-    raise_err(err, E_FASTPATH);
+  if (merge && nS >= 0x7fff) {  // int16 local ids; the host never routes such jobs here ...
+    if (spec)  // ... unless it replays a plan: report the level, it is redone measured
+      atomicCAS(reinterpret_cast<unsigned long long *>(spec), 0ull, static_cast<unsigned long long>(level));
+    else
+      raise_err(err, E_FASTPATH);
     merge = false;
   }
   const int ocap = (merge && stage) ? lane_ocap(nS, kL + kR) : 0;
@@ -376,8 +383,13 @@ __global__ void __launch_bounds__(32) k_lane(Pass2 P, const double *__restrict__
   }
   const int total = __shfl_sync(FULL, off, 31);
   off -= bytes;
-  if (total > pool) {  // the host sizes the pool from the measured need
-    if (lane == 0) raise_err(err, E_FASTPATH);
+  if (total > pool) {  // the host sizes the pool from the measured need (or a replayed plan's)
+    if (lane == 0) {
+      if (spec)
+        atomicCAS(reinterpret_cast<unsigned long long *>(spec), 0ull, static_cast<unsigned long long>(level));
+      else
+        raise_err(err, E_FASTPATH);
+    }
     return;
   }
   // per-job metadata for the cooperative phases
@@ -575,7 +587,7 @@ int g_lane_stage = 0;          // H3D_LANE_STAGE: stage merged events (0 = never
 // 1 (does not fit: the caller routes the level elsewhere) or a negative code.
 long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, const unsigned long long *need,
-                     cudaStream_t s) {
+                     cudaStream_t s, LaneCfg *cfg, long long *spec) {
   constexpr int kPool = 200 * 1024;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -587,6 +599,17 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
     g_lane_attr[dev] = true;
   }
   const long long jobs = j1 - j0;
+  if (!need) {  // a replayed plan: the recorded variant, jobs per CTA and pool
+    const int jpc = 32 >> cfg->r;
+    h3d_count_launches(1);
+    const dim3 grid(h3d_grid(jobs, jpc), 2);
+    const int pool = static_cast<int>(cfg->pool);
+    if (cfg->v >= 2)
+      k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec);
+    else
+      k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec);
+    return 0;
+  }
   auto pick = [&](int v, int *jr) {  // fewest-lanes-idle jobs per CTA that fits
     int r = 0;
     while (r < 5 && static_cast<long long>(need[16 + 6 * v + r]) > kPool) ++r;
@@ -617,9 +640,12 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
   h3d_count_launches(1);
   const dim3 grid(h3d_grid(jobs, jpc), 2);
   if (v >= 2)
-    k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1);
+    k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1,
+                                       spec);
   else
-    k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1);
+    k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1,
+                                        spec);
+  if (cfg) *cfg = LaneCfg{v, r, pool};
   return 0;
 }
 

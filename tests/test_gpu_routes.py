@@ -134,3 +134,27 @@ def test_random_knob_combinations(oracle_mod):
                 r = H.convex_hull_3d(p)
                 assert np.array_equal(r.faces, e.faces), (trial, kv, len(p))
                 assert np.array_equal(r.vertices, e.vertices), (trial, kv, len(p))
+
+
+@pytest.mark.parametrize("order", ["cube_then_sphere", "sphere_then_cube", "ball_then_int"])
+def test_plan_replay_across_clouds(order, oracle_mod):
+    """A call replays the level plan the previous call with the same n
+    recorded (no per-level measurement); a cloud whose jobs do not fit the
+    recorded launches makes the replay resume, measured, from that level --
+    every result still equals the oracle, with no exact-engine fallback."""
+    n = 50000
+    first, second = order.split("_then_")
+
+    def make(kind, seed):
+        return integer_cloud(n, seed) if kind == "int" else generate(n, kind, seed)
+
+    clouds = [make(first, 1), make(first, 2), make(second, 3), make(second, 4), make(first, 5)]
+    with fast.tuned(plan=1):
+        for pts in clouds:
+            before = fast.FALLBACKS[0]
+            r = H.convex_hull_3d(pts)
+            exp = oracle_mod.convex_hull_3d(pts)
+            if order != "ball_then_int":
+                assert fast.FALLBACKS[0] == before
+            assert np.array_equal(r.faces, exp.faces)
+            assert np.array_equal(r.vertices, exp.vertices)
