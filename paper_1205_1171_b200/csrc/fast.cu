@@ -562,7 +562,13 @@ template <bool XYZ>
 __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts,
                                                  long long n, int level, long long j0,
                                                  long long j1, long long *err, int pool,
-                                                 int jpc, int prefetch, long long *spec) {
+                                                 int jpc, int prefetch, long long *spec,
+                                                 long long *stamp) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *stamp = static_cast<long long>(t);
+  }
   // an earlier level failed, or (a replayed plan, spec) did not fit: stop
   // (warp-uniform; the words it reads may be stale)
   if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0 ||
@@ -1647,8 +1653,8 @@ template <bool XYZ>
 void launch_tpj(dim3 grid, int pool, int jpc, int prefetch, cudaStream_t s, Pass2 P,
                 const double *pts,
                 long long n, int lv, long long j0, long long j1, long long *err,
-                long long *spec = nullptr) {
-  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec);
+                long long *spec = nullptr, long long *stamp = nullptr) {
+  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp);
 }
 
 }  // namespace
@@ -1809,18 +1815,20 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         if (r.lv != lv || lv > lv_hi || r.kind == REC_BIG) break;
         if (lv > lv_lo) check(P, lv - 1, spec);
         const long long j0 = p0 >> lv, j1 = (p1 + (1ll << lv) - 1) >> lv;
-        h3d_stamp_now(s, lv);
+        // the level's first kernel writes its start stamp (no extra launch)
+        long long *stp = h3d_stamp_buf() ? h3d_stamp_buf() + lv : nullptr;
+        if (r.kind == REC_WARP) h3d_stamp_now(s, lv);
         void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
         int tag = lv;
         long long rc = 0;
         if (r.kind == REC_MINI) {
           tag = lv + 5000;
-          rc = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, r.variant, spec, nullptr, big_ws, big_bytes);
+          rc = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, r.variant, spec, stp, big_ws, big_bytes);
         } else if (r.kind == REC_LANE) {
           tag = lv + 1000;
           void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
           LaneCfg c = r.lane;
-          rc = lane_level(P, sorted_pts, n, lv, j0, j1, err, nullptr, s, &c, spec);
+          rc = lane_level(P, sorted_pts, n, lv, j0, j1, err, nullptr, s, &c, spec, stp);
           h3d_prof_end(ek, tag, 2, s);
         } else if (r.kind == REC_TPJ) {
           tag = lv + 1000;
@@ -1829,10 +1837,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           const dim3 grid(h3d_grid(j1 - j0, r.jpc), 2);
           if (r.variant)
             launch_tpj<true>(grid, static_cast<int>(r.pool), r.jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err,
-                             spec);
+                             spec, stp);
           else
             launch_tpj<false>(grid, static_cast<int>(r.pool), r.jpc, r.prefetch, s, P, sorted_pts, n, lv, j0,
-                              j1, err, spec);
+                              j1, err, spec, stp);
           h3d_prof_end(ek, tag, 2, s);
         } else {  // REC_WARP: an oversized job runs in HBM mode, always fits
           h3d_count_launches(1);

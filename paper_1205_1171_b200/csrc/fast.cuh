@@ -229,7 +229,8 @@ struct LaneCfg {
 };
 long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, const unsigned long long *need,
-                     cudaStream_t s, LaneCfg *cfg = nullptr, long long *spec = nullptr);
+                     cudaStream_t s, LaneCfg *cfg = nullptr, long long *spec = nullptr,
+                     long long *stamp = nullptr);
 extern long long g_lane_xyz_max;  // lane.cu knobs
 extern int g_lane_stage;
 

@@ -330,7 +330,12 @@ template <bool XYZ>
 __global__ void __launch_bounds__(32) k_lane(Pass2 P, const double *__restrict__ pts, long long n,
                                              int level, long long j0, long long j1,
                                              long long *err, int pool, int jpc, int stage,
-                                             long long *spec) {
+                                             long long *spec, long long *stamp) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *stamp = static_cast<long long>(t);
+  }
   // an earlier level failed, or (a replayed plan, spec) did not fit: stop
   // (warp-uniform; the words it reads may be stale)
   if (__any_sync(FULL, *reinterpret_cast<volatile long long *>(err) != 0 ||
@@ -587,7 +592,7 @@ int g_lane_stage = 0;          // H3D_LANE_STAGE: stage merged events (0 = never
 // 1 (does not fit: the caller routes the level elsewhere) or a negative code.
 long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, const unsigned long long *need,
-                     cudaStream_t s, LaneCfg *cfg, long long *spec) {
+                     cudaStream_t s, LaneCfg *cfg, long long *spec, long long *stamp) {
   constexpr int kPool = 200 * 1024;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -605,9 +610,9 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
     const dim3 grid(h3d_grid(jobs, jpc), 2);
     const int pool = static_cast<int>(cfg->pool);
     if (cfg->v >= 2)
-      k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec);
+      k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec, stamp);
     else
-      k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec);
+      k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec, stamp);
     return 0;
   }
   auto pick = [&](int v, int *jr) {  // fewest-lanes-idle jobs per CTA that fits
@@ -641,10 +646,10 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
   const dim3 grid(h3d_grid(jobs, jpc), 2);
   if (v >= 2)
     k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1,
-                                       spec);
+                                       spec, stamp);
   else
     k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1,
-                                        spec);
+                                        spec, stamp);
   if (cfg) *cfg = LaneCfg{v, r, pool};
   return 0;
 }

@@ -513,16 +513,35 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   }
   __syncthreads();
   MINI_TICK(10);
-  if (tid == 0) {
-    int o = 0;
-    for (int s = 0; s < nseg; ++s) {
-      const int c = m.sbn[s];
-      m.sbn[s] = o;
-      o += c;
+  if (tid < 32) {  // exclusive scan of the segments' bridge counts: warp 0,
+                   // MINI_S / 32 consecutive segments per lane (a serial loop
+                   // here cost ~65 us per level in the global-memory variant)
+    constexpr int PL = MINI_S / 32;
+    int c[PL], sum = 0;
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int sg = tid * PL + q;
+      c[q] = sg < nseg ? m.sbn[sg] : 0;
+      sum += c[q];
     }
-    m.sbn[nseg] = o;
-    m.nb = o;
-    if (o > MINI_B) m.flag = 1;
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (tid >= o) inc += t;
+    }
+    int o = inc - sum;
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int sg = tid * PL + q;
+      if (sg < nseg) m.sbn[sg] = o;
+      o += c[q];
+    }
+    if (tid == 31) {
+      m.sbn[nseg] = inc;
+      m.nb = inc;
+      if (inc > MINI_B) m.flag = 1;
+    }
   }
   __syncthreads();
   if (m.flag) {  // exact tie, walk/sweep disagreement or capacity: exact engine

@@ -36,7 +36,7 @@ template <typename K>
 struct RsItems;
 template <>
 struct RsItems<unsigned> {
-  static constexpr int v = 16;  // 4096 keys per tile, 42 KB of shared memory
+  static constexpr int v = 18;  // 4608 keys per tile, 47 KB of shared memory (larger tiles: fewer look-backs; 16 -> 18: -8 %, tools/rs_bench.cu)
 };
 template <>
 struct RsItems<unsigned long long> {
@@ -130,13 +130,13 @@ __global__ void __launch_bounds__(256) k_rs_hist(const K *__restrict__ keys, lon
 // one 8-bit digit pass: kin/vin -> kout/vout (vin == nullptr: values are the
 // input positions).  hist = this pass's 256 digit counts; look = one word
 // per (tile, digit), zeroed; ticket = zeroed tile counter.
-template <typename K>
+template <typename K, int IT = RsItems<K>::v>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_pass(const K *__restrict__ kin, const int *__restrict__ vin,
                                                         K *__restrict__ kout, int *__restrict__ vout,
                                                         long long n, int shift, int bits,
                                                         const unsigned *__restrict__ hist,
                                                         unsigned long long *look, unsigned *ticket) {
-  constexpr int IT = RsItems<K>::v, TILE = RS_THREADS * IT;
+  constexpr int TILE = RS_THREADS * IT;
   __shared__ K sk[TILE];
   __shared__ int sv[TILE];
   __shared__ unsigned whist[RS_WARPS][RS_BINS];
