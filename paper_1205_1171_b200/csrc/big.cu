@@ -938,7 +938,7 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   const long long J2 = 2 * J;
   if (J2 + 1 > W.m + 64) return 1;
   auto scan = [&](int *in, int *out, long long items) -> bool {
-    h3d_count_launches(3);
+    h3d_count_launches(1);
     return h3d_check(prim::scan<true, int>(W.tmp, W.tmp_bytes, in, out, items, prim::OpSum(), 0, 0, s));
   };
   h3d_count_launches(1);
@@ -988,7 +988,7 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
     k_big_incidx<<<grid_of(3 * kin), 256, 0, s>>>(kcur, static_cast<int>(3 * kin), W);
     k_big_fill_init<<<grid_of(3 * kin), 256, 0, s>>>(P, n, lv, j0, J, W, kcur, vcur,
                                                     static_cast<int>(3 * kin));
-    h3d_count_launches(3);
+    h3d_count_launches(1);
     if (h3d_check(prim::scan<false, unsigned long long>(W.tmp, W.tmp_bytes, W.sc0, W.sc1, 3 * kin,
                                                         LinkScanOp(), 0ull, 0ull, s)))
       return H3D_E_CUDA;

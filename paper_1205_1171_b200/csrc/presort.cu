@@ -982,7 +982,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     // perturb_ties: run heads by max-scan, then base + rank*step
     h3d_count_launches(1);
     k_run_heads<<<G, 256, 0, s>>>(w.work, n, w.head);
-    h3d_count_launches(3);
+    h3d_count_launches(1);
     if (h3d_check(prim::scan<false, long long>(w.cub_tmp, w.cub_bytes, w.head, w.head, n, prim::OpMax(),
                                                -1ll, -1ll, s)))
       return H3D_E_CUDA;

@@ -12,8 +12,8 @@
 //    The presort's x keys (api.py:97, `np.argsort(kind="stable")`) and the
 //    lexsort / perturbation passes (api.py:86-87, :97-105) run on it, as do
 //    the incidence lists of the time-split pipeline (big.cu).
-//  * scan: inclusive or exclusive scan with any associative operator
-//    (block reduce -> scan of the block aggregates -> block scan + carry-in);
+//  * scan: inclusive or exclusive scan with any associative operator, one
+//    pass with decoupled look-back (k_scan_1p);
 //  * select_flagged: indices of the nonzero flags, in order (np.unique of
 //    the facet vertices, api.py:266, as a vertex-mark compaction).
 //
@@ -397,25 +397,113 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_down(const T *__restrict__ 
   for (int i = threadIdx.x; i < nvalid; i += SC_THREADS) out[base + i] = s_tile[i];
 }
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Single-pass scan with decoupled look-back: tiles take tickets in start
+// order, publish their aggregate, and warp 0 combines the predecessors'
+// values 32 tiles per round trip (in tile order: the operator need not
+// commute) until it meets an inclusive prefix.  One launch, one read and one
+// write of the data.  Status per tile: flag (0 none, 1 aggregate, 2
+// inclusive) + the two values in separate slots (an aggregate is never
+// overwritten by the inclusive value a reader might be fetching).
+template <typename T, typename Op, bool EXCL>
+__global__ void __launch_bounds__(SC_THREADS) k_scan_1p(const T *__restrict__ in, T *__restrict__ out, long long n,
+                                                        Op op, T pad, T init, unsigned *flags, T *aggv, T *incv,
+                                                        unsigned *ticket) {
+  __shared__ T s_tile[SC_TILE + 1];
+  __shared__ T s_warp[SC_THREADS / 32];
+  __shared__ T s_prefix;
+  __shared__ long long s_tile_id;
+  if (threadIdx.x == 0) s_tile_id = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const long long tile = s_tile_id;
+  const long long base = tile * SC_TILE;
+  T x[SC_ITEMS];
+  load_blocked(in, base, n, pad, x, s_tile);
+  const T agg = block_incl_scan(x, op, s_warp);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (tile == 0) {
+      if (lane == 0) {
+        incv[0] = agg;
+        st_release_u32(flags, 2u);
+      }
+    } else {
+      if (lane == 0) {
+        aggv[tile] = agg;
+        st_release_u32(flags + tile, 1u);
+      }
+      T prefix = pad;
+      bool have = false;
+      for (long long j = tile - 1;; j -= 32) {
+        const long long tj = j - lane;  // lane 0 = the nearest predecessor
+        unsigned f = 2u;
+        T v = pad;
+        if (tj >= 0) {
+          do {
+            f = ld_acquire_u32(flags + tj);
+          } while (f == 0u);
+          v = f == 2u ? incv[tj] : aggv[tj];
+        }
+        const unsigned incm = __ballot_sync(0xffffffffu, f == 2u);
+        const int stop = incm ? __ffs(incm) - 1 : 31;  // lanes 0..stop count
+        T acc = __shfl_sync(0xffffffffu, v, stop);     // the oldest first
+        for (int l = stop - 1; l >= 0; --l) acc = op(acc, __shfl_sync(0xffffffffu, v, l));
+        prefix = have ? op(acc, prefix) : acc;
+        have = true;
+        if (incm) break;
+      }
+      if (lane == 0) {
+        incv[tile] = op(prefix, agg);
+        st_release_u32(flags + tile, 2u);
+        s_prefix = prefix;
+      }
+    }
+  }
+  __syncthreads();
+  const bool hc = tile > 0;
+  const T carry = hc ? s_prefix : init;
+#pragma unroll
+  for (int i = 0; i < SC_ITEMS; ++i) s_tile[threadIdx.x * SC_ITEMS + i + (EXCL ? 1 : 0)] = hc ? op(carry, x[i]) : x[i];
+  if (EXCL && threadIdx.x == 0) s_tile[0] = carry;
+  __syncthreads();
+  const int nvalid = n - base < SC_TILE ? static_cast<int>(n - base) : SC_TILE;
+  for (int i = threadIdx.x; i < nvalid; i += SC_THREADS) out[base + i] = s_tile[i];
+}
+
 template <typename T>
 inline size_t scan_temp_bytes(long long n) {
   const long long np = (n + SC_TILE - 1) / SC_TILE;
-  return static_cast<size_t>(np > 0 ? np : 1) * sizeof(T) + 256;
+  const size_t t = static_cast<size_t>(np > 0 ? np : 1);
+  return 256 + ((t * 4 + 255) & ~size_t(255)) + 2 * ((t * sizeof(T) + 255) & ~size_t(255));
 }
 
 // inclusive (EXCL = false) or exclusive (EXCL = true: item 0 gets init)
-// scan; in == out allowed (every block reads its tile before any block of
-// the last kernel writes, and each block writes only its own tile)
+// scan, one launch (k_scan_1p); in == out allowed (a tile reads its own
+// input before it writes its own output, and only its own)
 template <bool EXCL, typename T, typename Op>
 inline cudaError_t scan(void *tmp, size_t tmp_bytes, const T *in, T *out, long long n, Op op, T pad, T init,
                         cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   if (tmp_bytes < scan_temp_bytes<T>(n)) return cudaErrorInvalidValue;
-  T *part = static_cast<T *>(tmp);
   const long long np = (n + SC_TILE - 1) / SC_TILE;
-  k_scan_reduce<T, Op><<<static_cast<unsigned>(np), SC_THREADS, 0, s>>>(in, n, op, pad, part);
-  if (np > 1) k_scan_parts<T, Op><<<1, SC_THREADS, 0, s>>>(part, np, op, pad);
-  k_scan_down<T, Op, EXCL><<<static_cast<unsigned>(np), SC_THREADS, 0, s>>>(in, out, n, op, pad, part, init);
+  char *b = static_cast<char *>(tmp);
+  unsigned *ticket = reinterpret_cast<unsigned *>(b);
+  unsigned *flags = reinterpret_cast<unsigned *>(b + 256);
+  const size_t fb = (static_cast<size_t>(np) * 4 + 255) & ~size_t(255);
+  T *aggv = reinterpret_cast<T *>(b + 256 + fb);
+  T *incv = reinterpret_cast<T *>(b + 256 + fb + ((static_cast<size_t>(np) * sizeof(T) + 255) & ~size_t(255)));
+  cudaError_t e = cudaMemsetAsync(tmp, 0, 256 + fb, s);  // ticket + flags
+  if (e != cudaSuccess) return e;
+  k_scan_1p<T, Op, EXCL><<<static_cast<unsigned>(np), SC_THREADS, 0, s>>>(in, out, n, op, pad, init, flags, aggv,
+                                                                          incv, ticket);
   return cudaGetLastError();
 }
 
