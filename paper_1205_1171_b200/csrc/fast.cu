@@ -559,7 +559,12 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
 }
 
 template <bool XYZ>
-__global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts,
+#ifdef H3D_TPJ_MINB  // register cap experiments (tools/ab_libs.sh); unset by default
+__global__ void __launch_bounds__(32, H3D_TPJ_MINB) k_fast_tpj(
+#else
+__global__ void __launch_bounds__(32) k_fast_tpj(
+#endif
+Pass2 P, const double *__restrict__ pts,
                                                  long long n, int level, long long j0,
                                                  long long j1, long long *err, int pool,
                                                  int jpc, int prefetch, long long *spec,

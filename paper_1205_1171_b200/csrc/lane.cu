@@ -327,7 +327,12 @@ __device__ long long lane_sweep(const LSlice<XYZ> &S, int ocap, bool active, int
 
 // One warp = up to 32 merge jobs (jpc per CTA), one per lane.
 template <bool XYZ>
-__global__ void __launch_bounds__(32) k_lane(Pass2 P, const double *__restrict__ pts, long long n,
+#ifdef H3D_LANE_MINB  // register cap experiments (tools/ab_libs.sh); unset by default
+__global__ void __launch_bounds__(32, H3D_LANE_MINB) k_lane(
+#else
+__global__ void __launch_bounds__(32) k_lane(
+#endif
+Pass2 P, const double *__restrict__ pts, long long n,
                                              int level, long long j0, long long j1,
                                              long long *err, int pool, int jpc, int stage,
                                              long long *spec, long long *stamp) {

@@ -31,6 +31,8 @@ for route, kv in sorted(ROUTES.items()):
             r = H.convex_hull_3d(pts)
             e = O.convex_hull_3d(pts)
             ok = np.array_equal(r.faces, e.faces)
+            r2 = H.convex_hull_3d(generate(n, dist, n % 13 + 1))  # replays the recorded level plan
+            ok = ok and np.array_equal(r2.faces, O.convex_hull_3d(generate(n, dist, n % 13 + 1)).faces)
             bad += not ok
             print(f"{route:24s} {dist:7s} {n:6d} {'ok' if ok else 'MISMATCH'}", flush=True)
 pts = integer_cloud(4000, 3)
