@@ -437,6 +437,57 @@ __global__ void k_sel_keys(const unsigned *__restrict__ k32, SelState *st, int *
 }
 
 // run start index per row of lex-sorted x (0 where the row continues a run)
+// The lexsort of the tie path (api.py:86-87, np.lexsort((z, y, x))) from the
+// stable x order already at hand: runs of equal x are contiguous and hold
+// the same points in both orders, so only each run is re-ordered, by
+// (y, z, index) -- an insertion sort per run (runs longer than RUN_MAX set
+// *flag: the caller does the three full stable passes instead).
+__global__ void k_lexruns(const double *__restrict__ pts, int *perm, long long n, int *flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i + 1 < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double x = pts[3ll * perm[i]];
+    if (pts[3ll * perm[i + 1]] != x || (i > 0 && pts[3ll * perm[i - 1]] == x)) continue;  // i: run head
+    long long e = i + 1;
+    while (e < n && pts[3ll * perm[e]] == x && e - i <= RUN_MAX) ++e;
+    if (e - i > RUN_MAX) {
+      *flag = 1;
+      continue;
+    }
+    for (long long a = i + 1; a < e; ++a) {
+      const int va = perm[a];
+      const unsigned long long ya = order_key(pts[3ll * va + 1]), za = order_key(pts[3ll * va + 2]);
+      long long b = a - 1;
+      while (b >= i) {
+        const int vb = perm[b];
+        const unsigned long long yb = order_key(pts[3ll * vb + 1]), zb = order_key(pts[3ll * vb + 2]);
+        if (yb < ya || (yb == ya && (zb < za || (zb == za && vb < va)))) break;
+        perm[b + 1] = vb;
+        --b;
+      }
+      perm[b + 1] = va;
+    }
+  }
+}
+
+// After the perturbation: is x still non-decreasing along the lexsorted
+// rows (then the reference's stable re-sort, api.py:102-104, is the
+// identity)?  flag[3] = a descent (re-sort needed), flag[0] = equal
+// neighbours (the ties survived: DegenerateInputError).
+__global__ void k_perturbed_order(const double *__restrict__ w, long long n, int *flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i + 1 < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double a = w[3 * i], b = w[3 * (i + 1)];
+    if (a > b) flag[3] = 1;
+    if (a == b) flag[0] = 1;
+  }
+}
+
+__global__ void k_perm_to_order(const int *__restrict__ perm, long long n, long long *order) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    order[i] = perm[i];
+}
+
 __global__ void k_run_heads(const double *__restrict__ w, long long n, long long *head) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -960,23 +1011,36 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   }
   const int tie = hflag[0];
   if (tie) {
-    // lexsort (x, y, z): stable LSD passes on z, then y, then x (api.py:86-87)
-    int *perm = nullptr;
-    h3d_count_launches(1);
-    k_keys<<<G, 256, 0, s>>>(pts, nullptr, 2, n, w.k0, w.v0);
-    if (!radix(w, w.k0, w.v0, w.k1, w.v1, n, &ks, &vs, s)) return H3D_E_CUDA;
-    perm = vs;
-    int *other = (perm == w.v0) ? w.v1 : w.v0;
-    h3d_count_launches(1);
-    k_keys<<<G, 256, 0, s>>>(pts, perm, 1, n, w.k0, other);
-    if (!radix(w, w.k0, other, w.k1, perm, n, &ks, &vs, s)) return H3D_E_CUDA;
-    perm = vs;
-    other = (perm == w.v0) ? w.v1 : w.v0;
-    h3d_count_launches(1);
-    k_keys<<<G, 256, 0, s>>>(pts, perm, 0, n, w.k0, other);
-    if (!radix(w, w.k0, other, w.k1, perm, n, &ks, &vs, s)) return H3D_E_CUDA;
-    // lex-sorted rows -> w.work; lexsort permutation kept in v2
+    // lexsort (x, y, z) (api.py:86-87): the runs of equal x of the stable x
+    // order re-ordered by (y, z, index); with a run longer than RUN_MAX the
+    // three stable LSD passes on z, then y, then x
+    int lexflag[4] = {0, 0, 0, 0};
     cudaMemcpyAsync(w.v2, vs, sizeof(int) * n, cudaMemcpyDeviceToDevice, s);
+    cudaMemsetAsync(w.flag, 0, sizeof(int) * 4, s);
+    h3d_count_launches(1);
+    k_lexruns<<<G, 256, 0, s>>>(pts, w.v2, n, w.flag + 2);
+    if (h3d_check(cudaMemcpyAsync(lexflag, w.flag, sizeof(lexflag), cudaMemcpyDeviceToHost, s)) ||
+        h3d_check(cudaStreamSynchronize(s)))
+      return H3D_E_CUDA;
+    if (lexflag[2]) {
+      int *perm = nullptr;
+      h3d_count_launches(1);
+      k_keys<<<G, 256, 0, s>>>(pts, nullptr, 2, n, w.k0, w.v0);
+      if (!radix(w, w.k0, w.v0, w.k1, w.v1, n, &ks, &vs, s)) return H3D_E_CUDA;
+      perm = vs;
+      int *other = (perm == w.v0) ? w.v1 : w.v0;
+      h3d_count_launches(1);
+      k_keys<<<G, 256, 0, s>>>(pts, perm, 1, n, w.k0, other);
+      if (!radix(w, w.k0, other, w.k1, perm, n, &ks, &vs, s)) return H3D_E_CUDA;
+      perm = vs;
+      other = (perm == w.v0) ? w.v1 : w.v0;
+      h3d_count_launches(1);
+      k_keys<<<G, 256, 0, s>>>(pts, perm, 0, n, w.k0, other);
+      if (!radix(w, w.k0, other, w.k1, perm, n, &ks, &vs, s)) return H3D_E_CUDA;
+      // lexsort permutation kept in v2
+      cudaMemcpyAsync(w.v2, vs, sizeof(int) * n, cudaMemcpyDeviceToDevice, s);
+    }
+    // lex-sorted rows -> w.work
     h3d_count_launches(1);
     k_gather_rows<<<G, 256, 0, s>>>(pts, w.v2, n, w.work, nullptr, nullptr);
     // perturb_ties: run heads by max-scan, then base + rank*step
@@ -988,15 +1052,29 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
       return H3D_E_CUDA;
     h3d_count_launches(1);
     k_perturb<<<G, 256, 0, s>>>(w.work, w.head, n);
-    // stable re-sort of the perturbed x (api.py:102-104)
-    h3d_count_launches(1);
-    k_keys<<<G, 256, 0, s>>>(w.work, nullptr, 0, n, w.k0, w.v0);
-    if (!radix(w, w.k0, w.v0, w.k1, w.v1, n, &ks, &vs, s)) return H3D_E_CUDA;
-    h3d_count_launches(1);
-    k_gather_rows<<<G, 256, 0, s>>>(w.work, vs, n, sorted_pts, ord, w.v2);
+    // stable re-sort of the perturbed x (api.py:102-104): the identity when
+    // x did not descend anywhere (checked on the device)
     cudaMemsetAsync(w.flag, 0, sizeof(int) * 4, s);
     h3d_count_launches(1);
-    k_adjacent_tie<<<G, 256, 0, s>>>(ks, n, w.flag);
+    k_perturbed_order<<<G, 256, 0, s>>>(w.work, n, w.flag);
+    int pflag[4] = {0, 0, 0, 0};
+    if (h3d_check(cudaMemcpyAsync(pflag, w.flag, sizeof(pflag), cudaMemcpyDeviceToHost, s)) ||
+        h3d_check(cudaStreamSynchronize(s)))
+      return H3D_E_CUDA;
+    if (!pflag[3]) {
+      cudaMemcpyAsync(sorted_pts, w.work, 3 * sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+      h3d_count_launches(1);
+      k_perm_to_order<<<G, 256, 0, s>>>(w.v2, n, ord);  // flag[0]: the ties that survived
+    } else {
+      h3d_count_launches(1);
+      k_keys<<<G, 256, 0, s>>>(w.work, nullptr, 0, n, w.k0, w.v0);
+      if (!radix(w, w.k0, w.v0, w.k1, w.v1, n, &ks, &vs, s)) return H3D_E_CUDA;
+      h3d_count_launches(1);
+      k_gather_rows<<<G, 256, 0, s>>>(w.work, vs, n, sorted_pts, ord, w.v2);
+      cudaMemsetAsync(w.flag, 0, sizeof(int) * 4, s);
+      h3d_count_launches(1);
+      k_adjacent_tie<<<G, 256, 0, s>>>(ks, n, w.flag);
+    }
     *perturbed = 1;
     // the perturbation changed x: the scale is re-taken on the sorted rows
     h3d_count_launches(2);

@@ -181,3 +181,26 @@ def test_stats_level_times_from_device_stamps():
     assert sum(r.stats.lower_level_ms) > 0.0
     assert r.stats.lower_level_ms[0] == 0.0 and r.stats.lower_level_ms[2] > 0.0  # leaf: levels 1..3
     assert r.stats.sort_ms > 0.0 and r.stats.lower_ms > 0.0
+
+
+@pytest.mark.parametrize("case", ["short_runs", "long_run", "perturbed_descends"])
+def test_tie_path_variants(case, oracle_mod):
+    """The device tie path (api.py:86-110): lexsort by re-ordering the runs
+    of equal x (short runs), the three full stable passes (a run longer than
+    64), and the stable re-sort after the perturbation when a perturbed x
+    overtakes the next distinct x (otherwise the re-sort is the identity)."""
+    rng = np.random.default_rng(11)
+    pts = rng.uniform(-1, 1, (3000, 3))
+    if case == "short_runs":
+        pts[:600, 0] = np.repeat(rng.uniform(-1, 1, 200), 3)
+    elif case == "long_run":
+        pts[:100, 0] = 0.25
+    else:  # a run at 1.0, the next distinct x two ulps above: base + 16 eps > it
+        pts[:5, 0] = 1.0
+        pts[5, 0] = np.nextafter(np.nextafter(1.0, 2.0), 2.0)
+    rng.shuffle(pts)
+    r = H.convex_hull_3d(pts)
+    exp = oracle_mod.convex_hull_3d(pts)
+    assert r.stats.perturbed and exp.perturbed
+    assert np.array_equal(r.faces, exp.faces)
+    assert np.array_equal(r.vertices, exp.vertices)
