@@ -579,14 +579,15 @@ Pass2 P, const double *__restrict__ pts,
   if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0 ||
                                   (spec && *reinterpret_cast<volatile long long *>(spec) != 0)))
     return;
-  const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
-  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
-  const double zs = blockIdx.y ? -1.0 : 1.0;
+  const int pass = lvl_pass();
+  const GroupBuf in = pass ? P.in1 : P.in0;
+  const GroupBuf out = pass ? P.out1 : P.out0;
+  const double zs = pass ? -1.0 : 1.0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x;
   const long long size = 1ll << level, half = size >> 1;
   // jpc (1..32) jobs per CTA: lanes >= jpc idle (large jobs, few per CTA)
-  const long long j = j0 + (long long)blockIdx.x * jpc + lane;
+  const long long j = j0 + lvl_blk() * jpc + lane;
   const long long L = j << level, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
   int nSL = 0, kL = 0, nSR = 0, kR = 0;
@@ -853,11 +854,12 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   // an earlier level failed: stop (warp-uniform; the words it reads may be stale)
   if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0)) return;
   constexpr int NP = 1 << B;
-  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
-  const double zs = blockIdx.y ? -1.0 : 1.0;
+  const int pass = lvl_pass();
+  const GroupBuf out = pass ? P.out1 : P.out0;
+  const double zs = pass ? -1.0 : 1.0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x;
-  const long long blk = (p0 >> B) + (long long)blockIdx.x * 32 + lane;
+  const long long blk = (p0 >> B) + lvl_blk() * 32 + lane;
   const long long base = blk << B;
   const long long top = p1 < n ? p1 : n;
   const int cnt = base < top ? static_cast<int>((top - base) < NP ? (top - base) : NP) : 0;
@@ -1620,6 +1622,11 @@ struct PlanKey {
 std::mutex g_plan_mu;
 std::map<PlanKey, std::vector<LevelRec>> g_plans;
 int g_plan = 1;  // H3D_PLAN: replay recorded level plans (0 = measure every level)
+}  // namespace
+namespace h3d {
+int g_interleave = 1;  // H3D_INTERLEAVE: the two passes of the same jobs in adjacent CTAs
+}  // namespace h3d
+namespace {
 void plans_clear() {
   std::lock_guard<std::mutex> g(g_plan_mu);
   g_plans.clear();
@@ -1651,6 +1658,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_LANE_STAGE")) g_lane_stage = atoi(e);
   if (const char *e = getenv("H3D_TPJ_PREFETCH")) kTpjPrefetchJobs = atoll(e);
   if (const char *e = getenv("H3D_PLAN")) g_plan = atoi(e) ? 1 : 0;
+  if (const char *e = getenv("H3D_INTERLEAVE")) g_interleave = atoi(e) ? 1 : 0;
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
@@ -1672,6 +1680,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   long long old = -1;
   if (value >= 0) plans_clear();  // recorded plans follow the knobs they were made with
   if (k == "plan") { old = g_plan; if (value >= 0) g_plan = value ? 1 : 0; }
+  if (k == "interleave") { old = g_interleave; if (value >= 0) g_interleave = value ? 1 : 0; }
   if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
   else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = leaf_depth(value); }
   else if (k == "mini") { old = g_mini; if (value >= 0) g_mini = value ? 1 : 0; }
@@ -1779,7 +1788,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     h3d_stamp_route(1, 3000 + g_leaf_b);
     void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
     h3d_count_launches(1);
-    const dim3 grid(h3d_grid(blocks, 32), 2);
+    const dim3 grid = lvl_grid(h3d_grid(blocks, 32), g_interleave != 0);
     // level B's groups go to buffer B&1
     const Pass2 LP = (g_leaf_b & 1) ? Pass2{w0.A, w1.A, w0.B, w1.B} : Pass2{w0.B, w1.B, w0.A, w1.A};
     if (g_leaf_b == 4)
@@ -1839,7 +1848,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           tag = lv + 1000;
           void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
           h3d_count_launches(1);
-          const dim3 grid(h3d_grid(j1 - j0, r.jpc), 2);
+          const dim3 grid = lvl_grid(h3d_grid(j1 - j0, r.jpc), g_interleave != 0);
           if (r.variant)
             launch_tpj<true>(grid, static_cast<int>(r.pool), r.jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err,
                              spec, stp);
@@ -2057,7 +2066,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     if (tpj) {
       h3d_count_launches(1);
       void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
-      const dim3 grid(h3d_grid(jobs, jpc), 2);
+      const dim3 grid = lvl_grid(h3d_grid(jobs, jpc), g_interleave != 0);
       if (xyz)
         launch_tpj<true>(grid, static_cast<int>(pool), jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err);
       else

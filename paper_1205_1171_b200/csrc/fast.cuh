@@ -88,6 +88,18 @@ struct Pass2 {
 };
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// Which pass and which block of jobs a CTA of a level launch covers.  Grid
+// (g, 2): blockIdx.y is the pass (all lower-pass CTAs are scheduled before
+// the upper-pass ones); grid (2g, 1): the two passes of the same jobs are
+// adjacent CTAs, so the rows both read (the same sorted points, z negated on
+// the upper pass) are fetched from DRAM once and hit in L2 for the other.
+__device__ __forceinline__ int lvl_pass() { return gridDim.y == 2 ? blockIdx.y : (blockIdx.x & 1); }
+__device__ __forceinline__ long long lvl_blk() {
+  return gridDim.y == 2 ? static_cast<long long>(blockIdx.x) : static_cast<long long>(blockIdx.x >> 1);
+}
+inline dim3 lvl_grid(unsigned g, bool interleave) { return interleave ? dim3(2 * g, 1) : dim3(g, 2); }
+extern int g_interleave;  // H3D_INTERLEAVE: pass-interleaved level grids
 constexpr int FIRST_FLAG = 1 << 30;        // "on a child's -inf chain"
 constexpr int FIRST_NONE = FIRST_FLAG - 1; // no event yet
 

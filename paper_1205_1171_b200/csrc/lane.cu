@@ -346,13 +346,14 @@ Pass2 P, const double *__restrict__ pts, long long n,
   if (__any_sync(FULL, *reinterpret_cast<volatile long long *>(err) != 0 ||
                            (spec && *reinterpret_cast<volatile long long *>(spec) != 0)))
     return;
-  const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
-  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
-  const double zs = blockIdx.y ? -1.0 : 1.0;
+  const int pass = lvl_pass();
+  const GroupBuf in = pass ? P.in1 : P.in0;
+  const GroupBuf out = pass ? P.out1 : P.out0;
+  const double zs = pass ? -1.0 : 1.0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x;
   const long long size = 1ll << level, half = size >> 1;
-  const long long j = j0 + (long long)blockIdx.x * jpc + lane;
+  const long long j = j0 + lvl_blk() * jpc + lane;
   const long long L = j << level, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
   int nSL = 0, kL = 0, nSR = 0, kR = 0;
@@ -612,7 +613,7 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
   if (!need) {  // a replayed plan: the recorded variant, jobs per CTA and pool
     const int jpc = 32 >> cfg->r;
     h3d_count_launches(1);
-    const dim3 grid(h3d_grid(jobs, jpc), 2);
+    const dim3 grid = lvl_grid(h3d_grid(jobs, jpc), g_interleave != 0);
     const int pool = static_cast<int>(cfg->pool);
     if (cfg->v >= 2)
       k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec, stamp);
@@ -648,7 +649,7 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
   const int jpc = 32 >> r;
   if (pool < 1024) pool = 1024;
   h3d_count_launches(1);
-  const dim3 grid(h3d_grid(jobs, jpc), 2);
+  const dim3 grid = lvl_grid(h3d_grid(jobs, jpc), g_interleave != 0);
   if (v >= 2)
     k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1,
                                        spec, stamp);

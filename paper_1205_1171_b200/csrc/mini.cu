@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   typedef cub::BlockScan<int, MINI_T> Scan;
   __shared__ typename Scan::TempStorage s_scan;
   const int tid = threadIdx.x, T = MINI_T;
-  const long long j = j0 + blockIdx.x;
+  const long long j = j0 + lvl_blk();
   if (j >= j1) return;
   // Stop when an earlier launch failed, or (speculative top levels) when a
   // job of an earlier level did not fit, so this level's input is not valid:
@@ -292,9 +292,10 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
              (spec && *reinterpret_cast<volatile long long *>(spec) != 0);
   __syncthreads();
   if (s_stop) return;
-  const GroupBuf in = blockIdx.y ? P.in1 : P.in0;
-  const GroupBuf out = blockIdx.y ? P.out1 : P.out0;
-  const double zs = blockIdx.y ? -1.0 : 1.0;
+  const int pass = lvl_pass();
+  const GroupBuf in = pass ? P.in1 : P.in0;
+  const GroupBuf out = pass ? P.out1 : P.out0;
+  const double zs = pass ? -1.0 : 1.0;
   const long long size = 1ll << lv, half = size >> 1;
   const long long L = j << lv, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
@@ -730,7 +731,7 @@ static long long launch_mini(const Pass2 &P, const double *pts, long long n, int
     attr[dev_id] = true;
   }
   h3d_count_launches(1);
-  k_mini<T, K, N><<<dim3(static_cast<unsigned>(j1 - j0), 2), T, gscratch ? 0 : bytes, s>>>(
+  k_mini<T, K, N><<<lvl_grid(static_cast<unsigned>(j1 - j0), g_interleave != 0), T, gscratch ? 0 : bytes, s>>>(
       P, pts, n, lv, j0, j1, err, g_mini_seglen, spec, stamp, static_cast<unsigned char *>(gscratch),
       stride);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
