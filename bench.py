@@ -365,6 +365,7 @@ def run_ours(args):
     E.KERNEL_EVENTS = True
     F.profile_collect(1 << 20)  # drop the warm-up's records
     l0 = E.launch_count()
+    y0 = E.sync_count()
     clocks = ClockSampler(local)
     clocks.start()
     torch.cuda.synchronize()
@@ -381,6 +382,7 @@ def run_ours(args):
         prof.append((name, p_idx, lv, t_ms))
     E.KERNEL_EVENTS = False
     launches = (E.launch_count() - l0) // args.steps
+    host_syncs = (E.sync_count() - y0) / args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     value = n / (ms / 1e3)
     fallbacks = F.FALLBACKS[0] - fb0
@@ -478,7 +480,8 @@ def run_ours(args):
                    "seed": seed, "engine": args.engine, "parallelism": "1 GPU",
                    "l2": "input 24n bytes > 126 MB L2 (C4/C5); no explicit flush",
                    "faces": nfaces, "vertices": nverts},
-        "e2e": e2e, "e2e_pipelined": e2e_pipelined, "gpu_launches": launches, "roofline": roof,
+        "e2e": e2e, "e2e_pipelined": e2e_pipelined, "gpu_launches": launches,
+        "host_syncs_per_step": host_syncs, "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk, "fallbacks": fallbacks, "routes_per_step": routes,
         "level_ms_last_step": level_ms,

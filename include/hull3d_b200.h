@@ -63,6 +63,8 @@ const char *h3d_impl(void);
 const char *h3d_last_error(void);
 /* number of this library's own kernel launches so far (process-wide) */
 int64_t h3d_launch_count(void);
+/* number of host synchronisations (stream syncs) the library made so far */
+int64_t h3d_sync_count(void);
 /* per-level profile of the CALLING THREAD: when enabled (per thread; on = 1),
  * every merge level of h3d_fast_passes* run by this thread is bracketed by
  * CUDA events on its stream (events pooled per device); on = 2 brackets only

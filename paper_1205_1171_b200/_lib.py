@@ -26,6 +26,7 @@ SIGNATURES: dict[str, tuple] = {
     "h3d_impl": (ctypes.c_char_p, []),
     "h3d_last_error": (ctypes.c_char_p, []),
     "h3d_launch_count": (i64, []),
+    "h3d_sync_count": (i64, []),
     "h3d_profile_enable": (None, [ctypes.c_int32]),
     "h3d_profile_collect": (i64, [vp, vp, vp, i64]),
     "h3d_profile_stamps": (None, [vp]),

@@ -948,7 +948,7 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   int tot[3];
   if (h3d_check(cudaMemcpyAsync(&tot[0], W.jkinoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
       h3d_check(cudaMemcpyAsync(&tot[1], W.jnsoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaStreamSynchronize(s)))
+      h3d_check(h3d_sync(s)))
     return H3D_E_CUDA;
   const long long kin = tot[0], pts_n = tot[1];
   // segment length: enough segments to give every SM a few warps
@@ -963,7 +963,7 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   k_big_segs<<<grid_of(J2 + 1), 256, 0, s>>>(J, W, static_cast<int>(SEG));
   if (scan(W.jseg, W.jsegoff, J2 + 1)) return H3D_E_CUDA;
   if (h3d_check(cudaMemcpyAsync(&tot[2], W.jsegoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaStreamSynchronize(s)))
+      h3d_check(h3d_sync(s)))
     return H3D_E_CUDA;
   const long long nseg = tot[2];
   if (kin > 4 * W.m || pts_n > 2 * W.m || nseg > 4 * W.m / SEG_MIN + W.m) {

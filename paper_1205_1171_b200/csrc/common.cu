@@ -11,6 +11,13 @@ static std::atomic<long long> g_launches{0};
 
 void h3d_count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+static std::atomic<long long> g_syncs{0};
+cudaError_t h3d_sync(cudaStream_t s) {
+  g_syncs.fetch_add(1, std::memory_order_relaxed);
+  return cudaStreamSynchronize(s);
+}
+extern "C" int64_t h3d_sync_count(void) { return g_syncs.load(); }
+
 bool h3d_check(cudaError_t e) {
   if (e == cudaSuccess) return false;
   std::strncpy(g_last_error, cudaGetErrorString(e), sizeof(g_last_error) - 1);

@@ -1872,7 +1872,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       long long hv[2] = {0, 0};
       if (h3d_check(cudaMemcpyAsync(&hv[0], spec, sizeof(long long), cudaMemcpyDeviceToHost, s)) ||
           h3d_check(cudaMemcpyAsync(&hv[1], err, sizeof(long long), cudaMemcpyDeviceToHost, s)) ||
-          h3d_check(cudaStreamSynchronize(s)))
+          h3d_check(h3d_sync(s)))
         return H3D_E_CUDA;
       if (hv[1] != 0) {
         lv = lv_hi + 2;  // declined: the caller sees the error word
@@ -1905,7 +1905,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         P, n, lv, j0, j1, w0.need, err, h3d_stamp_buf() ? h3d_stamp_buf() + lv : nullptr);
     unsigned long long need[40];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
-        h3d_check(cudaStreamSynchronize(s)))
+        h3d_check(h3d_sync(s)))
       return H3D_E_CUDA;
     const long long herr = static_cast<long long>(need[10]);
     // A launch declined the input (or failed): its level wrote nothing, so
@@ -1963,7 +1963,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           if (g_trace) {
             long long f = 0;
             cudaMemcpyAsync(&f, spec, sizeof(f), cudaMemcpyDeviceToHost, s);
-            const cudaError_t ce = cudaStreamSynchronize(s);
+            const cudaError_t ce = h3d_sync(s);
             fprintf(stderr, "h3d level %d speculative: flag %lld (%s)\n", l2, f,
                     cudaGetErrorString(ce));
           }
@@ -1975,7 +1975,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         long long failed = 0, serr = 0;
         if (h3d_check(cudaMemcpyAsync(&failed, spec, sizeof(failed), cudaMemcpyDeviceToHost, s)) ||
             h3d_check(cudaMemcpyAsync(&serr, err, sizeof(serr), cudaMemcpyDeviceToHost, s)) ||
-            h3d_check(cudaStreamSynchronize(s)))
+            h3d_check(h3d_sync(s)))
           return H3D_E_CUDA;
         if (serr != 0) {
           lv = lv_hi + 2;  // declined: nothing more to check or record

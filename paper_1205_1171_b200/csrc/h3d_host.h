@@ -9,6 +9,9 @@
 bool h3d_check(cudaError_t e);
 // counts this library's own kernel launches (bench.py reports gpu_launches)
 void h3d_count_launches(int k);
+// every host synchronisation of the library goes through here (counted:
+// bench.py reports host_syncs per step)
+cudaError_t h3d_sync(cudaStream_t s);
 // per-level CUDA-event profile (h3d_profile_enable); no-ops when disabled.
 // Mode 1: every level bracketed (measurement + routing + kernels); mode 2:
 // only the lane-per-job kernel launches (h3d_prof_kernels()), for bench.py's

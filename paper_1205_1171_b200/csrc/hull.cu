@@ -11,7 +11,8 @@
 // input with ties is redone through the exact tie path (h3d_presort, api.py
 // :90-110), an error is returned, and a fast-path decline is reported in
 // info[0] for the caller's exact engine.  Host synchronisations per hull:
-// the level loop's routing read-backs (one per measured level) + one.
+// one for a replayed level plan (fast.cu), one per measured level otherwise,
+// plus this final one -- counted by h3d_sync_count().
 #include "../../include/hull3d_b200.h"
 #include "fast.cuh"
 #include "h3d_host.h"
@@ -81,7 +82,7 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
   const int words = stamps ? H3D_HULL_STATE : kStStamps;
   if (rc == 0 && (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev,
                                             words * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) ||
-                  h3d_check(cudaStreamSynchronize(s))))
+                  h3d_check(h3d_sync(s))))
     rc = H3D_E_CUDA;
   const int64_t *hs = info + H3D_HULL_INFO - H3D_HULL_STATE;
   int32_t perturbed = 0;
@@ -96,7 +97,7 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
                                &fin, s);
     if (rc == 0 && (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev,
                                               words * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) ||
-                    h3d_check(cudaStreamSynchronize(s))))
+                    h3d_check(h3d_sync(s))))
       rc = H3D_E_CUDA;
   }
   if (stamps) h3d_profile_stamps(nullptr);

@@ -849,14 +849,14 @@ bool degenerate_scan(const double *sorted_pts, long long rows, ScanState *wscan,
   k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, rows, wscan, 16384);
   if (h3d_check(cudaMemcpyAsync(hs, wscan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) ||
       h3d_check(cudaMemcpyAsync(hflag, wflag, nflag * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaStreamSynchronize(s)))
+      h3d_check(h3d_sync(s)))
     return false;
   if (hs->i != none && hs->j != none && hs->k != none) return true;
   h3d_count_launches(3);
   for (int stage = 0; stage < 3; ++stage)
     k_degenerate<<<G, 256, 0, s>>>(sorted_pts, rows, wscan, stage, 1, rows);
   return !h3d_check(cudaMemcpyAsync(hs, wscan, sizeof(ScanState), cudaMemcpyDeviceToHost, s)) &&
-         !h3d_check(cudaStreamSynchronize(s));
+         !h3d_check(h3d_sync(s));
 }
 
 }  // namespace
@@ -992,7 +992,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
   k_gather_rows<<<G, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, nullptr, w.flag);
   int hflag[3] = {0, 0, 0};
   if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaStreamSynchronize(s)))
+      h3d_check(h3d_sync(s)))
     return H3D_E_CUDA;
   if (hflag[1]) return H3D_E_NONFINITE;
   if (hflag[2]) {  // long runs of equal 32-bit keys: the exact 64-bit sort
@@ -1002,7 +1002,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     if (!radix(w, w.k0, w.v0, w.k1, w.v1, n, &ks, &vs, s)) return H3D_E_CUDA;
     k_adjacent_tie<<<G, 256, 0, s>>>(ks, n, w.flag);
     if (h3d_check(cudaMemcpyAsync(hflag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-        h3d_check(cudaStreamSynchronize(s)))
+        h3d_check(h3d_sync(s)))
       return H3D_E_CUDA;
     if (!hflag[0]) {
       h3d_count_launches(1);
@@ -1020,7 +1020,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     h3d_count_launches(1);
     k_lexruns<<<G, 256, 0, s>>>(pts, w.v2, n, w.flag + 2);
     if (h3d_check(cudaMemcpyAsync(lexflag, w.flag, sizeof(lexflag), cudaMemcpyDeviceToHost, s)) ||
-        h3d_check(cudaStreamSynchronize(s)))
+        h3d_check(h3d_sync(s)))
       return H3D_E_CUDA;
     if (lexflag[2]) {
       int *perm = nullptr;
@@ -1059,7 +1059,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     k_perturbed_order<<<G, 256, 0, s>>>(w.work, n, w.flag);
     int pflag[4] = {0, 0, 0, 0};
     if (h3d_check(cudaMemcpyAsync(pflag, w.flag, sizeof(pflag), cudaMemcpyDeviceToHost, s)) ||
-        h3d_check(cudaStreamSynchronize(s)))
+        h3d_check(h3d_sync(s)))
       return H3D_E_CUDA;
     if (!pflag[3]) {
       cudaMemcpyAsync(sorted_pts, w.work, 3 * sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
@@ -1172,7 +1172,7 @@ int64_t h3d_presort_slab(const double *pts, int64_t n, int64_t q0, int64_t p1, i
   if (scan) {  // _scan_degenerate over this window (rank 0: rows [0, p1))
     if (!degenerate_scan(sorted_pts, p1, w.scan, w.flag, G, &hs, hflag, 3, s)) return H3D_E_CUDA;
   } else if (h3d_check(cudaMemcpyAsync(hflag, w.flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-             h3d_check(cudaStreamSynchronize(s))) {
+             h3d_check(h3d_sync(s))) {
     return H3D_E_CUDA;
   }
   // ties, long key runs, a bad selection, non-finite input or a degeneracy
@@ -1209,7 +1209,7 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n, const int64_t *
     return H3D_E_CUDA;
   long long cnt = 0;
   if (h3d_check(cudaMemcpyAsync(&cnt, w.count, sizeof(cnt), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaStreamSynchronize(s)))
+      h3d_check(h3d_sync(s)))
     return H3D_E_CUDA;
   return cnt;
 }

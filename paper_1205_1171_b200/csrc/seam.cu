@@ -271,7 +271,7 @@ struct Res {
     if (!d) return H3D_E_CUDA;
     if (h3d_check(cudaMemcpyAsync(h, d, sizeof(long long) * words,
                                   cudaMemcpyDeviceToHost, s)) ||
-        h3d_check(cudaStreamSynchronize(s)))
+        h3d_check(h3d_sync(s)))
       return H3D_E_CUDA;
     return h[0];
   }
@@ -292,7 +292,7 @@ int64_t h3d_seam_init_base_logs(int32_t *links, int32_t *slots, int64_t n, void 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h3d_count_launches(1);
   k_init_base<<<h3d_grid(n, 256), 256, 0, s>>>(links, slots, n);
-  if (h3d_check(cudaGetLastError()) || h3d_check(cudaStreamSynchronize(s))) return H3D_E_CUDA;
+  if (h3d_check(cudaGetLastError()) || h3d_check(h3d_sync(s))) return H3D_E_CUDA;
   return 0;
 }
 

@@ -70,6 +70,11 @@ def launch_count() -> int:
     return int(_lib.load().h3d_launch_count())
 
 
+def sync_count() -> int:
+    """Host synchronisations the library made so far (h3d_sync_count)."""
+    return int(_lib.load().h3d_sync_count())
+
+
 def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
