@@ -59,23 +59,31 @@ struct MiniSmem {
   double X[MINI_N], Y[MINI_N], Z[MINI_N];
   int G[MINI_N];                // gid
   short2 LN[MINI_N];            // links at t = -inf (job-local)
-  short2 KL[MINI_N];            // rebuilt links
+
   int ib[MINI_N + 1];           // incidence list bounds (exclusive scan)
   int cur[MINI_N];              // scatter cursors, then first output event
-  short ei[3 * MINI_K];         // incidence: event index (each list in event order)
-  short eo[3 * MINI_K];         // incidence: scattered event index (before ordering)
+  short ei[3 * MINI_K];         // incidence: event index (each list in event order);
+                                // the rebuild's links KL live here (dead after the sweeps)
   short2 el[3 * MINI_K];        // incidence: links after the event
   int cpos[MINI_K + 1];         // kept child events: flags, then exclusive scan
   int nid[MINI_N + 1];          // keep flags, then new ids (exclusive scan)
   double bt[MINI_B];            // bridge events: time
   W bw[MINI_B];                 //   facet word (side 0)
   short2 buv[MINI_B];           //   feet after
-  double slt[MINI_B];           // per-segment slabs of the sweep (then compacted)
+  // per-segment slabs of the sweep (then compacted); the incidence
+  // scatter's temporary (eo: 3K shorts, dead before the sweeps) lives in
+  // slt: the smaller footprint lets the tiny variant fit 7 CTAs per SM
+  static_assert(3 * MINI_K * sizeof(short) <= MINI_B * sizeof(double), "eo must fit slt");
+  double slt[MINI_B];
   W slw[MINI_B];
   short2 sluv[MINI_B];
-  short2 sst[MINI_S];           // segment start bridges
-  int sbn[MINI_S + 1];          // bridge events per segment, then offsets
-  int flag, nb;
+  static constexpr int NSEG = MINI_T < MINI_S ? MINI_T : MINI_S;  // segments <= threads
+  short2 sst[NSEG];             // segment start bridges
+  int sbn[NSEG + 1];            // bridge events per segment, then offsets
+  int flag, nb, kept;
+  __device__ __forceinline__ short *eo() { return reinterpret_cast<short *>(slt); }
+  static_assert(MINI_N * sizeof(short2) <= 3 * MINI_K * sizeof(short), "KL must fit ei");
+  __device__ __forceinline__ short2 *KL() { return reinterpret_cast<short2 *>(ei); }
 };
 
 template <class W>
@@ -406,13 +414,13 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     const auto w = m.sw[d];
     const int pa = swa(w), pb = swb(w), pc = swc(w);
     int q = atomicAdd(&m.cur[pa], 1);
-    m.eo[q] = static_cast<short>(d);
+    m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pa);
     q = atomicAdd(&m.cur[pb], 1);
-    m.eo[q] = static_cast<short>(d);
+    m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pb);
     q = atomicAdd(&m.cur[pc], 1);
-    m.eo[q] = static_cast<short>(d);
+    m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pc);
   }
   __syncthreads();
@@ -422,9 +430,9 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   // not a sequential L^2 sort)
   for (int k = tid; k < 3 * kin; k += T) {
     const int p = m.el[k].x, b0 = m.ib[p], b1 = m.ib[p + 1];
-    const short x = m.eo[k];
+    const short x = m.eo()[k];
     int rank = 0;
-    for (int q = b0; q < b1; ++q) rank += m.eo[q] < x;
+    for (int q = b0; q < b1; ++q) rank += m.eo()[q] < x;
     m.ei[b0 + rank] = x;
   }
   __syncthreads();
@@ -449,7 +457,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   MINI_TICK(4);
   // ---- segments: start bridges by walks
   int nseg = kin / seglen;
-  if (nseg > MINI_S) nseg = MINI_S;
+  if (nseg > MS::NSEG) nseg = MS::NSEG;
   if (nseg > T) nseg = T;
   if (nseg < 1) nseg = 1;
   const int seg = (kin + nseg - 1) / nseg > 0 ? (kin + nseg - 1) / nseg : 1;
@@ -517,7 +525,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   if (tid < 32) {  // exclusive scan of the segments' bridge counts: warp 0,
                    // MINI_S / 32 consecutive segments per lane (a serial loop
                    // here cost ~65 us per level in the global-memory variant)
-    constexpr int PL = MINI_S / 32;
+    constexpr int PL = (MS::NSEG + 31) / 32;
     int c[PL], sum = 0;
 #pragma unroll
     for (int q = 0; q < PL; ++q) {
@@ -672,7 +680,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
           const Ev e = evo[f];
           o = make_short2(static_cast<short>(e.a), static_cast<short>(e.c));
         }
-        m.KL[p] = o;
+        m.KL()[p] = o;
       }
       local[q] = keep;
       sum += keep;
@@ -684,14 +692,14 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       if (p <= nS) m.nid[p] = local[q] ? off : -1;
       off += local[q];
     }
-    if (tid == T - 1) m.sbn[MINI_S] = off;  // kept points
+    if (tid == T - 1) m.kept = off;  // kept points
   }
   __syncthreads();
   bool bad = false;
   for (int p = tid; p < nS; p += T) {
     const int id = m.nid[p];
     if (id < 0) continue;
-    const short2 l = m.KL[p];
+    const short2 l = m.KL()[p];
     int2 o;
     o.x = l.x == NIL ? NIL : m.nid[l.x];
     o.y = l.y == NIL ? NIL : m.nid[l.y];
@@ -709,7 +717,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   }
   if (bad) raise_err(err, E_FASTPATH);
   MINI_TICK(9);
-  if (tid == 0) out.hdr[j] = make_int2(m.sbn[MINI_S], kout);
+  if (tid == 0) out.hdr[j] = make_int2(m.kept, kout);
 }
 
 template <int T, int K, int N>
