@@ -57,16 +57,12 @@ struct MiniSmem {
   double st[MINI_K];            // S: event times
   W sw[MINI_K];                 // S: facet words (a, b, c, kind, side)
   double X[MINI_N], Y[MINI_N], Z[MINI_N];
-  int G[MINI_N];                // gid
   short2 LN[MINI_N];            // links at t = -inf (job-local)
 
   int ib[MINI_N + 1];           // incidence list bounds (exclusive scan)
-  int cur[MINI_N];              // scatter cursors, then first output event
   short ei[3 * MINI_K];         // incidence: event index (each list in event order);
                                 // the rebuild's links KL live here (dead after the sweeps)
   short2 el[3 * MINI_K];        // incidence: links after the event
-  int cpos[MINI_K + 1];         // kept child events: flags, then exclusive scan
-  int nid[MINI_N + 1];          // keep flags, then new ids (exclusive scan)
   double bt[MINI_B];            // bridge events: time
   W bw[MINI_B];                 //   facet word (side 0)
   short2 buv[MINI_B];           //   feet after
@@ -84,6 +80,16 @@ struct MiniSmem {
   __device__ __forceinline__ short *eo() { return reinterpret_cast<short *>(slt); }
   static_assert(MINI_N * sizeof(short2) <= 3 * MINI_K * sizeof(short), "KL must fit ei");
   __device__ __forceinline__ short2 *KL() { return reinterpret_cast<short2 *>(ei); }
+  // after the sweeps the incidence arrays are dead: the kept-child-event
+  // positions live in el, the new point ids in ib
+  static_assert((MINI_K + 1) * sizeof(int) <= 3 * MINI_K * sizeof(short2), "cpos must fit el");
+  __device__ __forceinline__ int *cpos() { return reinterpret_cast<int *>(el); }
+  __device__ __forceinline__ int *nid() { return ib; }
+  // the per-point counts / scatter cursors (phase 2) and first output
+  // events (after the compaction) live in the sweep slab's word array, dead
+  // in both phases
+  static_assert(MINI_N * sizeof(int) <= MINI_B * sizeof(W), "cur must fit slw");
+  __device__ __forceinline__ int *cur() { return reinterpret_cast<int *>(slw); }
 };
 
 template <class W>
@@ -105,6 +111,25 @@ __device__ __forceinline__ int swk(W w) {
 template <class W>
 __device__ __forceinline__ int sws(W w) {
   return static_cast<int>((w >> (3 * wsh<W>() + 1)) & 1u);
+}
+
+// exclusive prefix sum of one value per thread over a T-thread block
+template <int T>
+__device__ __forceinline__ int mini_excl_sum(int v, int *s_w) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  int pre = 0;
+#pragma unroll
+  for (int q = 0; q < T / 32; ++q) pre += q < w ? s_w[q] : 0;
+  __syncthreads();
+  return pre + x - v;
 }
 
 template <class MS>
@@ -284,8 +309,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   // memory
   MS &m = *reinterpret_cast<MS *>(
       gmem ? gmem + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * gstride : smem_raw);
-  typedef cub::BlockScan<int, MINI_T> Scan;
-  __shared__ typename Scan::TempStorage s_scan;
+  __shared__ int s_scan[MINI_T / 32];  // mini_excl_sum's warp totals
   const int tid = threadIdx.x, T = MINI_T;
   const long long j = j0 + lvl_blk();
   if (j >= j1) return;
@@ -344,9 +368,8 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     m.X[p] = c.x;
     m.Y[p] = c.y;
     m.Z[p] = c.z;
-    m.G[p] = g;
     m.LN[p] = make_short2(static_cast<short>(l.x), static_cast<short>(l.y));
-    m.cur[p] = 0;
+    m.cur()[p] = 0;
   }
   MINI_TICK(1);
   // ---- merged child sequence S (merge path, left first on equal times);
@@ -384,9 +407,9 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   for (int d = tid; d < kin; d += T) {
     if (d > 0 && m.st[d] == m.st[d - 1]) m.flag = 1;  // exact tie
     const auto w = m.sw[d];
-    atomicAdd(&m.cur[swa(w)], 1);
-    atomicAdd(&m.cur[swb(w)], 1);
-    atomicAdd(&m.cur[swc(w)], 1);
+    atomicAdd(&m.cur()[swa(w)], 1);
+    atomicAdd(&m.cur()[swb(w)], 1);
+    atomicAdd(&m.cur()[swc(w)], 1);
   }
   __syncthreads();
   {
@@ -395,11 +418,11 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     int sum = 0;
     for (int q = 0; q < per && q < PER; ++q) {
       const int p = tid * per + q;
-      local[q] = p < nS ? m.cur[p] : 0;
+      local[q] = p < nS ? m.cur()[p] : 0;
       sum += local[q];
     }
     int off;
-    Scan(s_scan).ExclusiveSum(sum, off);
+    off = mini_excl_sum<MINI_T>(sum, s_scan);
     for (int q = 0; q < per && q < PER; ++q) {
       const int p = tid * per + q;
       if (p <= nS) m.ib[p] = off;
@@ -407,19 +430,19 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     }
   }
   __syncthreads();
-  for (int p = tid; p < nS; p += T) m.cur[p] = m.ib[p];
+  for (int p = tid; p < nS; p += T) m.cur()[p] = m.ib[p];
   __syncthreads();
   // scatter (arbitrary order within a list; the owner kept alongside) ...
   for (int d = tid; d < kin; d += T) {
     const auto w = m.sw[d];
     const int pa = swa(w), pb = swb(w), pc = swc(w);
-    int q = atomicAdd(&m.cur[pa], 1);
+    int q = atomicAdd(&m.cur()[pa], 1);
     m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pa);
-    q = atomicAdd(&m.cur[pb], 1);
+    q = atomicAdd(&m.cur()[pb], 1);
     m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pb);
-    q = atomicAdd(&m.cur[pc], 1);
+    q = atomicAdd(&m.cur()[pc], 1);
     m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pc);
   }
@@ -604,16 +627,16 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       sum += keep;
     }
     int off;
-    Scan(s_scan).ExclusiveSum(sum, off);
+    off = mini_excl_sum<MINI_T>(sum, s_scan);
     for (int q = 0; q < per && q < PER; ++q) {
       const int d = tid * per + q;
-      if (d <= kin) m.cpos[d] = local[q] ? (off | (1 << 30)) : off;
+      if (d <= kin) m.cpos()[d] = local[q] ? (off | (1 << 30)) : off;
       off += local[q];
     }
   }
-  for (int p = tid; p < nS; p += T) m.cur[p] = 0x7fffffff;  // first output event
+  for (int p = tid; p < nS; p += T) m.cur()[p] = 0x7fffffff;  // first output event
   __syncthreads();
-  const int kept = m.cpos[kin] & ~(1 << 30);
+  const int kept = m.cpos()[kin] & ~(1 << 30);
   const int kout = kept + NB;
   if (m.flag || kout > 2 * (R_ - L) - 1) {
     if (tid == 0) raise_err(err, m.flag ? E_FASTPATH : H3D_E_OVERFLOW);
@@ -623,7 +646,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   // ---- merged log (job-local ids) straight to HBM, first event per point
   EvP *evo = out.ev + 2 * L;
   for (int d = tid; d < kin; d += T) {
-    const int cp = m.cpos[d];
+    const int cp = m.cpos()[d];
     if (!(cp & (1 << 30))) continue;
     const double t = m.st[d];
     const auto w = m.sw[d];
@@ -635,7 +658,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     o.c = swc(w);
     o.kind = swk(w);
     evo[idx] = o;
-    atomicMin(&m.cur[o.b], idx);
+    atomicMin(&m.cur()[o.b], idx);
   }
   for (int i = tid; i < NB; i += T) {
     const double t = m.bt[i];
@@ -644,7 +667,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       const int mid = (lo + hi) >> 1;
       if (m.st[mid] < t) lo = mid + 1; else hi = mid;
     }
-    const int idx = i + (m.cpos[lo] & ~(1 << 30));
+    const int idx = i + (m.cpos()[lo] & ~(1 << 30));
     const auto w = m.bw[i];
     Ev o;
     o.t = t;
@@ -653,7 +676,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     o.c = swc(w);
     o.kind = swk(w);
     evo[idx] = o;
-    atomicMin(&m.cur[o.b], idx);
+    atomicMin(&m.cur()[o.b], idx);
   }
   __syncthreads();
   MINI_TICK(8);
@@ -669,7 +692,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
         const short2 l = m.LN[p];
         bool chain = p == 0 || p == nSL || (l.x != NIL && m.LN[l.x].y == p);
         chain = chain && (p < nSL ? p <= uv0.x : p >= uv0.y);
-        const int f = m.cur[p];
+        const int f = m.cur()[p];
         keep = chain || f != 0x7fffffff;
         short2 o = make_short2(NIL, NIL);
         if (chain) {
@@ -686,10 +709,10 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       sum += keep;
     }
     int off;
-    Scan(s_scan).ExclusiveSum(sum, off);
+    off = mini_excl_sum<MINI_T>(sum, s_scan);
     for (int q = 0; q < per && q < PER; ++q) {
       const int p = tid * per + q;
-      if (p <= nS) m.nid[p] = local[q] ? off : -1;
+      if (p <= nS) m.nid()[p] = local[q] ? off : -1;
       off += local[q];
     }
     if (tid == T - 1) m.kept = off;  // kept points
@@ -697,21 +720,21 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   __syncthreads();
   bool bad = false;
   for (int p = tid; p < nS; p += T) {
-    const int id = m.nid[p];
+    const int id = m.nid()[p];
     if (id < 0) continue;
     const short2 l = m.KL()[p];
     int2 o;
-    o.x = l.x == NIL ? NIL : m.nid[l.x];
-    o.y = l.y == NIL ? NIL : m.nid[l.y];
+    o.x = l.x == NIL ? NIL : m.nid()[l.x];
+    o.y = l.y == NIL ? NIL : m.nid()[l.y];
     bad |= (l.x != NIL && o.x < 0) | (l.y != NIL && o.y < 0);
     out.lnk[L + id] = o;
-    out.gid[L + id] = m.G[p];
+    out.gid[L + id] = in.gid[p < nSL ? L + p : M + (p - nSL)];  // the gid, re-read (not kept in smem)
   }
   for (int e = tid; e < kout; e += T) {
     Ev o = evo[e];
-    o.a = m.nid[o.a];
-    o.b = m.nid[o.b];
-    o.c = m.nid[o.c];
+    o.a = m.nid()[o.a];
+    o.b = m.nid()[o.b];
+    o.c = m.nid()[o.c];
     bad |= (o.a < 0) | (o.b < 0) | (o.c < 0);
     evo[e] = o;
   }
