@@ -191,24 +191,27 @@ struct LEvIn {
     r.a = r.b = r.c = r.kind = 0;
     return r;
   }
-  const double *t;
+  // the event time is not stored: it is the canonical time of the facet
+  // (evtime of the x-ordered triple, F4), re-derived from the block's
+  // coordinates in shared memory -- bit for bit the stored value, and the
+  // leaf's shared memory drops to 320 B per lane (16 CTAs per SM, was 12)
+  const double *x, *y, *z;  // lane-interleaved block coordinates
   const unsigned short *w;
   __device__ __forceinline__ Ev get(int i) const {
     Ev e;
-    e.t = t[i * 32];
-    const unsigned x = w[i * 32];
-    e.a = x & 0xf;
-    e.b = (x >> 4) & 0xf;
-    e.c = (x >> 8) & 0xf;
-    e.kind = x >> 12;
+    const unsigned v = w[i * 32];
+    e.a = v & 0xf;
+    e.b = (v >> 4) & 0xf;
+    e.c = (v >> 8) & 0xf;
+    e.kind = v >> 12;
+    e.t = evtime_xyz(x[e.a * 32], y[e.a * 32], z[e.a * 32], x[e.b * 32], y[e.b * 32], z[e.b * 32],
+                     x[e.c * 32], y[e.c * 32], z[e.c * 32]);
     return e;
   }
 };
 struct LEvOut {
-  double *t;
   unsigned short *w;
   __device__ __forceinline__ void put(long long k, const Ev &o) const {
-    t[k * 32] = o.t;
     w[k * 32] = static_cast<unsigned short>(o.a | (o.b << 4) | (o.c << 8) | (o.kind << 12));
   }
 };
@@ -844,7 +847,7 @@ Pass2 P, const double *__restrict__ pts,
 // kernels read.  Per lane: 30 B per point + 2 x 2 x 10 B event slots.
 template <int B>
 __host__ __device__ constexpr int leaf_lane_bytes() {
-  return (1 << B) * (24 + 4 + 2) + 2 * (2 << B) * 10 + ((1 << B) / 2) * 4;
+  return (1 << B) * (24 + 4 + 2) + 2 * (2 << B) * 2 + ((1 << B) / 2) * 4;
 }
 
 template <int B>
@@ -867,9 +870,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   double *X = reinterpret_cast<double *>(smem) + lane;
   double *Y = X + 32 * NP;
   double *Z = Y + 32 * NP;
-  double *ET0 = Z + 32 * NP;
-  double *ET1 = ET0 + 32 * 2 * NP;
-  short2 *LK = reinterpret_cast<short2 *>(reinterpret_cast<double *>(smem) + 32 * 7 * NP) + lane;
+  short2 *LK = reinterpret_cast<short2 *>(reinterpret_cast<double *>(smem) + 32 * 3 * NP) + lane;
   unsigned short *FI = reinterpret_cast<unsigned short *>(LK - lane + 32 * NP) + lane;
   constexpr unsigned FULL16 = 0xffffu;  // "not kept" in the 16-bit words
   unsigned short *EW0 = reinterpret_cast<unsigned short *>(FI - lane + 32 * NP) + lane;
@@ -902,7 +903,6 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   bool ok = true;
   int u0 = 0, v0 = 0;
   long long kfin = 0;
-  double *ETi = ET0, *ETo = ET1;
   unsigned short *EWi = EW0, *EWo = EW1;
 #pragma unroll 1
   for (int lv = 2; lv <= B; ++lv) {
@@ -913,10 +913,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
       const bool merge = ok && R - L > half;
       const int kL = KG[(2 * g) * 32 + lane], kR = KG[(2 * g + 1) * 32 + lane];
       if (!merge && L < cnt) {  // carry (copy_log): the short last group
-        for (int e = 0; e < kL; ++e) {
-          ETo[(2 * L + e) * 32] = ETi[(2 * L + e) * 32];
-          EWo[(2 * L + e) * 32] = EWi[(2 * L + e) * 32];
-        }
+        for (int e = 0; e < kL; ++e) EWo[(2 * L + e) * 32] = EWi[(2 * L + e) * 32];
       }
       // block-relative ids throughout (links, events, first-event info)
       if (merge) {
@@ -927,8 +924,8 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
         }
       }
       const long long k = merge_tpj2(
-          S, merge, M - 1, 0, pts, zs, LEvIn{ETi + 2 * L * 32, EWi + 2 * L * 32}, kL,
-          LEvIn{ETi + 2 * M * 32, EWi + 2 * M * 32}, kR, LEvOut{ETo + 2 * L * 32, EWo + 2 * L * 32},
+          S, merge, M - 1, 0, pts, zs, LEvIn{X, Y, Z, EWi + 2 * L * 32}, kL,
+          LEvIn{X, Y, Z, EWi + 2 * M * 32}, kR, LEvOut{EWo + 2 * L * 32},
           2 * (R - L), R - L, &u0, &v0);
       if (merge && k < 0) {
         raise_err(err, k);
@@ -960,7 +957,6 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
       KG[g * 32 + lane] = merge ? static_cast<int>(k) : (L < cnt ? kL : 0);
       kfin = KG[g * 32 + lane];
     }
-    double *tt = ETi; ETi = ETo; ETo = tt;
     unsigned short *tw = EWi; EWi = EWo; EWo = tw;
     __syncwarp();
   }
@@ -1004,7 +1000,7 @@ __global__ void __launch_bounds__(32) k_fast_leaf(Pass2 P, const double *__restr
   for (int e = 0; e < kfin; ++e) {
     const unsigned w = EWi[e * 32];
     Ev o;
-    o.t = ETi[e * 32];
+    o.t = LEvIn{X, Y, Z, EWi}.get(e).t;  // the canonical time, re-derived
     const unsigned na = FI[(w & 0xf) * 32], nb = FI[((w >> 4) & 0xf) * 32],
                    nc = FI[((w >> 8) & 0xf) * 32];
     bad |= (na == FULL16) | (nb == FULL16) | (nc == FULL16);
