@@ -562,16 +562,9 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
 }
 
 template <bool XYZ>
-#ifdef H3D_TPJ_MINB  // register cap experiments (tools/ab_libs.sh); unset by default
-__global__ void __launch_bounds__(32, H3D_TPJ_MINB) k_fast_tpj(
-#else
-__global__ void __launch_bounds__(32) k_fast_tpj(
-#endif
-Pass2 P, const double *__restrict__ pts,
-                                                 long long n, int level, long long j0,
-                                                 long long j1, long long *err, int pool,
-                                                 int jpc, int prefetch, long long *spec,
-                                                 long long *stamp) {
+__device__ __forceinline__ void tpj_body(Pass2 P, const double *__restrict__ pts, long long n, int level,
+                                         long long j0, long long j1, long long *err, int pool, int jpc,
+                                         int prefetch, long long *spec, long long *stamp) {
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -833,6 +826,25 @@ Pass2 P, const double *__restrict__ pts,
     }
   }
   if (__any_sync(FULL, bad) && lane == 0) raise_err(err, E_FASTPATH);
+}
+
+// the lane-per-job level kernel.  Two register budgets of the same body: the
+// compiler's own (156 registers, 12 warps/SM) and a 128-register cap (16
+// warps/SM) that pays at the lower levels, where more resident jobs hide the
+// gathers (measured per level, g_tpj_cap_level)
+template <bool XYZ>
+__global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts, long long n,
+                                                 int level, long long j0, long long j1, long long *err,
+                                                 int pool, int jpc, int prefetch, long long *spec,
+                                                 long long *stamp) {
+  tpj_body<XYZ>(P, pts, n, level, j0, j1, err, pool, jpc, prefetch, spec, stamp);
+}
+template <bool XYZ>
+__global__ void __launch_bounds__(32, 16) k_fast_tpj_r128(Pass2 P, const double *__restrict__ pts, long long n,
+                                                          int level, long long j0, long long j1, long long *err,
+                                                          int pool, int jpc, int prefetch, long long *spec,
+                                                          long long *stamp) {
+  tpj_body<XYZ>(P, pts, n, level, j0, j1, err, pool, jpc, prefetch, spec, stamp);
 }
 
 // ------------------------------------------------------------- leaf levels
@@ -1576,6 +1588,7 @@ long long kMiniHugeKin = 1000;   // H3D_MINI_HUGE_KIN
 // without measuring them (no read-back and host sync per level)
 int g_mini_spec = 1;  // H3D_MINI_SPEC
 int g_trace = 0;      // H3D_TRACE: one stderr line per routed level
+int g_tpj_cap_level = 6;  // H3D_TPJ_CAP_LEVEL: k_fast_tpj levels <= this at 128 registers
 int g_lane = 1;       // H3D_LANE: lane-per-job levels on lane.cu (0 = k_fast_tpj)
 // highest level routed to lane.cu; k_fast_tpj above (measured per level, C4:
 // lane.cu 2.33 / 1.90 ms at levels 4 / 5 vs 2.60 / 2.13; k_fast_tpj ahead
@@ -1655,6 +1668,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_TPJ_PREFETCH")) kTpjPrefetchJobs = atoll(e);
   if (const char *e = getenv("H3D_PLAN")) g_plan = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_INTERLEAVE")) g_interleave = atoi(e) ? 1 : 0;
+  if (const char *e = getenv("H3D_TPJ_CAP_LEVEL")) g_tpj_cap_level = atoi(e);
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
@@ -1663,7 +1677,10 @@ void launch_tpj(dim3 grid, int pool, int jpc, int prefetch, cudaStream_t s, Pass
                 const double *pts,
                 long long n, int lv, long long j0, long long j1, long long *err,
                 long long *spec = nullptr, long long *stamp = nullptr) {
-  k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp);
+  if (lv <= g_tpj_cap_level)
+    k_fast_tpj_r128<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp);
+  else
+    k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp);
 }
 
 }  // namespace
@@ -1677,6 +1694,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   if (value >= 0) plans_clear();  // recorded plans follow the knobs they were made with
   if (k == "plan") { old = g_plan; if (value >= 0) g_plan = value ? 1 : 0; }
   if (k == "interleave") { old = g_interleave; if (value >= 0) g_interleave = value ? 1 : 0; }
+  else if (k == "tpj_cap_level") { old = g_tpj_cap_level; if (value >= 0) g_tpj_cap_level = value; }
   if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
   else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = leaf_depth(value); }
   else if (k == "mini") { old = g_mini; if (value >= 0) g_mini = value ? 1 : 0; }
@@ -1749,6 +1767,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         h3d_check(cudaFuncSetAttribute(k_fast_tpj<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
         h3d_check(cudaFuncSetAttribute(k_fast_tpj<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj_r128<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj_r128<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)))
       return H3D_E_CUDA;
     load_env_once();
