@@ -296,7 +296,7 @@ def level_bytes(cfg: str):
 # bench kernel names -> the ncu kernel names they cover
 NCU_NAMES = {
     # the lane-per-job route: lane.cu (levels <= 5) and k_fast_tpj above
-    "k_fast_tpj": ("h3d::k_fast_tpj<", "h3d::k_lane<"),
+    "k_fast_tpj": ("h3d::k_fast_tpj<", "h3d::k_fast_tpj_r128<", "h3d::k_lane<"),
     "k_fast_warp": ("h3d::k_fast_warp<",),
     "k_fast_leaf": ("h3d::k_fast_leaf<",),
     "k_fast_init1": ("h3d::k_fast_init1",),

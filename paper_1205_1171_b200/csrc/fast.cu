@@ -33,7 +33,6 @@
 #include <type_traits>
 #include <vector>
 
-#include <cub/cub.cuh>
 
 #include "fast.cuh"
 #include "h3d_host.h"
@@ -2082,6 +2081,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       tpj = false;
     }
     if (tpj) {
+      if (g_trace) fprintf(stderr, "h3d level %d: tpj xyz %d jpc %d pool %lld\n", lv, xyz ? 1 : 0, jpc, pool);
       h3d_count_launches(1);
       void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
       const dim3 grid = lvl_grid(h3d_grid(jobs, jpc), g_interleave != 0);

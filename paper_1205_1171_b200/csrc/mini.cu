@@ -13,7 +13,6 @@
 // instead of HBM ones, and one launch per level.
 #include <type_traits>
 
-#include <cub/cub.cuh>
 
 #include "fast.cuh"
 

@@ -11,8 +11,6 @@
 // onto +0.0 first so that the two compare equal, as they do under numpy's
 // comparisons.  Stability + index payload reproduces argsort(kind="stable")
 // and np.lexsort((z, y, x)) exactly (three stable passes z, y, x).
-#include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
 
 #include "h3d_device.cuh"
 #include "h3d_host.h"
@@ -283,8 +281,7 @@ __global__ void k_sel_hist(const unsigned *__restrict__ k32, long long n,
 
 // one block of 256 threads, 8 bins each: the bucket holding each boundary's rank
 __global__ void k_sel_pick(unsigned *hist, SelState *st, int pass) {
-  typedef cub::BlockScan<long long, 256> BS;
-  __shared__ typename BS::TempStorage tmp;
+  __shared__ long long s_warp[8];
   const int bins = 1 << sel_bits(pass);
   const int t = threadIdx.x;
   for (int b = 0; b < 2; ++b) {
@@ -296,9 +293,7 @@ __global__ void k_sel_pick(unsigned *hist, SelState *st, int pass) {
       c[q] = 8 * t + q < bins ? hist[(pass == 0 ? 0 : 2048 * b) + 8 * t + q] : 0;
       tot += c[q];
     }
-    long long before;
-    BS(tmp).ExclusiveSum(tot, before);
-    __syncthreads();
+    long long before = prim::block_excl_sum256(tot, s_warp);
     if (has && rem >= before && rem < before + tot) {
       int d = 0;
       while (rem >= before + c[d]) before += c[d++];
@@ -315,8 +310,7 @@ constexpr int kSelItems = 8;
 
 __global__ void __launch_bounds__(256) k_sel_compact(const unsigned *__restrict__ k32, long long n,
                                                      SelState *st, int *out, int *runs, long long cap) {
-  typedef cub::BlockScan<int, 256> BS;
-  __shared__ typename BS::TempStorage tmp;
+  __shared__ int s_warp[8];
   __shared__ int s_base;
   const bool h0 = st->b[0] >= 0, h1 = st->b[1] >= 0;
   const unsigned K0 = st->pre[0], K1 = st->pre[1];
@@ -348,8 +342,8 @@ __global__ void __launch_bounds__(256) k_sel_compact(const unsigned *__restrict_
         else st->bad = 1;
       }
     }
-    int off, total;
-    BS(tmp).ExclusiveSum(cnt, off, total);
+    int total;
+    int off = prim::block_excl_sum256(cnt, s_warp, &total);
     if (threadIdx.x == 0) s_base = total ? atomicAdd(&st->count, total) : 0;
     __syncthreads();
     off += s_base;
@@ -517,9 +511,8 @@ __global__ void k_absmax(const double *__restrict__ p, long long m, unsigned lon
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x)
     best = fmax(best, fabs(p[i]));
-  typedef cub::BlockReduce<double, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const double b = BR(tmp).Reduce(best, cub::Max());
+  __shared__ double s_warp[8];
+  const double b = prim::block_reduce256(best, s_warp, [](double a, double c) { return fmax(a, c); });
   if (threadIdx.x == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(b)));
 }
 
@@ -674,15 +667,13 @@ __global__ void k_colsum(const double *__restrict__ P, long long n, double *part
     s1 += P[3 * i + 1];
     s2 += P[3 * i + 2];
   }
-  typedef cub::BlockReduce<double, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  double r = BR(tmp).Sum(s0);
-  __syncthreads();
+  __shared__ double s_warp[8];
+  const prim::OpSum add;
+  double r = prim::block_reduce256(s0, s_warp, add);
   if (threadIdx.x == 0) partial[3 * blockIdx.x] = r;
-  r = BR(tmp).Sum(s1);
-  __syncthreads();
+  r = prim::block_reduce256(s1, s_warp, add);
   if (threadIdx.x == 0) partial[3 * blockIdx.x + 1] = r;
-  r = BR(tmp).Sum(s2);
+  r = prim::block_reduce256(s2, s_warp, add);
   if (threadIdx.x == 0) partial[3 * blockIdx.x + 2] = r;
 }
 
@@ -733,8 +724,8 @@ struct PresortWS {
   int *v0, *v1, *v2;
   double *work;
   long long *head;
-  void *cub_tmp;
-  size_t cub_bytes;
+  void *prim_tmp;
+  size_t prim_bytes;
   int *flag;
   ScanState *scan;
   double *partial;
@@ -746,7 +737,7 @@ struct PresortWS {
 constexpr int kColsumBlocks = 296;
 
 // temporary bytes of the device-wide primitives (prims.cuh) over n items
-size_t cub_bytes_for(long long n) {
+size_t prim_bytes_for(long long n) {
   size_t m = prim::rs_temp_bytes<unsigned long long>(n);
   const size_t a = prim::rs_temp_bytes<unsigned>(n), b = prim::scan_temp_bytes<long long>(n),
                c = prim::select_temp_bytes(n);
@@ -763,8 +754,8 @@ bool carve(h3d_arena &ar, long long n, PresortWS &w) {
   w.v2 = ar.take<int>(n);
   w.work = ar.take<double>(3 * n);
   w.head = ar.take<long long>(n);
-  w.cub_bytes = cub_bytes_for(n);
-  w.cub_tmp = ar.take<char>(w.cub_bytes);
+  w.prim_bytes = prim_bytes_for(n);
+  w.prim_tmp = ar.take<char>(w.prim_bytes);
   w.flag = ar.take<int>(4);
   w.scan = ar.take<ScanState>(1);
   w.partial = ar.take<double>(3 * kColsumBlocks);
@@ -829,7 +820,7 @@ bool radix(PresortWS &w, unsigned long long *kin, int *vin, unsigned long long *
            long long n, unsigned long long **ko, int **vo, cudaStream_t s) {
   bool alt = false;
   h3d_count_launches(9);
-  if (h3d_check(prim::rs_sort_pairs<unsigned long long>(w.cub_tmp, w.cub_bytes, kin, vin, kalt, valt, n, 0,
+  if (h3d_check(prim::rs_sort_pairs<unsigned long long>(w.prim_tmp, w.prim_bytes, kin, vin, kalt, valt, n, 0,
                                                         64, &alt, s)))
     return false;
   *ko = alt ? kalt : kin;
@@ -902,7 +893,7 @@ int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t 
   k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, nullptr);
   bool alt = false;
   h3d_count_launches(5);
-  if (h3d_check(prim::rs_sort_pairs<unsigned>(w.cub_tmp, w.cub_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32, &alt,
+  if (h3d_check(prim::rs_sort_pairs<unsigned>(w.prim_tmp, w.prim_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32, &alt,
                                               s, true)))
     return H3D_E_CUDA;
   int *vs = alt ? w.v1 : w.v0;
@@ -981,7 +972,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     // values = the row positions, generated by the first digit pass
     bool alt = false;
     h3d_count_launches(5);
-    if (h3d_check(prim::rs_sort_pairs<unsigned>(w.cub_tmp, w.cub_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32,
+    if (h3d_check(prim::rs_sort_pairs<unsigned>(w.prim_tmp, w.prim_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32,
                                                 &alt, s, true)))
       return H3D_E_CUDA;
     vs = alt ? w.v1 : w.v0;
@@ -1047,7 +1038,7 @@ int64_t h3d_presort(const double *pts, int64_t n, double *sorted_pts, int64_t *o
     h3d_count_launches(1);
     k_run_heads<<<G, 256, 0, s>>>(w.work, n, w.head);
     h3d_count_launches(1);
-    if (h3d_check(prim::scan<false, long long>(w.cub_tmp, w.cub_bytes, w.head, w.head, n, prim::OpMax(),
+    if (h3d_check(prim::scan<false, long long>(w.prim_tmp, w.prim_bytes, w.head, w.head, n, prim::OpMax(),
                                                -1ll, -1ll, s)))
       return H3D_E_CUDA;
     h3d_count_launches(1);

@@ -85,22 +85,43 @@ __device__ __forceinline__ unsigned long long lookback(const unsigned long long 
   return prefix;
 }
 
-// exclusive scan of one value per thread over a 256-thread block
-__device__ __forceinline__ unsigned block_excl_sum256(unsigned v, unsigned *s_warp) {
+// exclusive scan of one value per thread over a 256-thread block (s_warp:
+// 8 words of shared memory); *total, when given, gets the block's sum
+template <typename T>
+__device__ __forceinline__ T block_excl_sum256(T v, T *s_warp, T *total = nullptr) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned x = v;
+  T x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned t = __shfl_up_sync(0xffffffffu, x, o);
+    const T t = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += t;
   }
   if (lane == 31) s_warp[w] = x;
   __syncthreads();
-  unsigned wp = 0;
+  T wp = 0, all = 0;
 #pragma unroll
-  for (int q = 0; q < RS_WARPS; ++q) wp += q < w ? s_warp[q] : 0u;
+  for (int q = 0; q < RS_WARPS; ++q) {
+    wp += q < w ? s_warp[q] : T(0);
+    all += s_warp[q];
+  }
   __syncthreads();
+  if (total) *total = all;
   return wp + x - v;
+}
+
+// reduction over a 256-thread block, the result in every thread (fixed
+// order: a butterfly within each warp, then the 8 warp values in order)
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce256(T v, T *s_warp, Op op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = v;
+  __syncthreads();
+  T r = s_warp[0];
+#pragma unroll
+  for (int q = 1; q < RS_WARPS; ++q) r = op(r, s_warp[q]);
+  __syncthreads();
+  return r;
 }
 
 // digit histograms of every pass in one read of the keys
