@@ -1573,7 +1573,7 @@ bool g_attr_done[64] = {};
 bool g_env_done = false;
 int g_leaf_b = 3;  // H3D_LEAF_B: levels 1..B fused (0 = off)
 int g_mini = 1;    // H3D_MINI: few small jobs -> mini.cu (0 = warp kernel)
-long long kMiniMaxCtas = 2 * 148;  // H3D_MINI_CTAS
+long long kMiniMaxCtas = 32 * 148;  // H3D_MINI_CTAS
 // the tiny mini variant (several CTAs per SM): at most this many CTAs, and
 // over the lane-per-job kernel only when the longest merged child log is at
 // least kMiniTinyKin events (the lane kernel's serial path then dominates)
@@ -1581,7 +1581,8 @@ long long kMiniTinyCtas = 16384;  // H3D_MINI_TINY_CTAS
 long long kMiniTinyKin = 160;    // H3D_MINI_TINY_KIN
 // the huge mini variant (global-memory slots): at most this many CTAs, and
 // only from this merged child log size (below it the shared-memory ones)
-long long kMiniHugeCtas = 296;   // H3D_MINI_HUGE_CTAS
+long long kMiniOneWave = 2 * 148;  // mini_one_wave: CTAs up to which the large variant runs
+long long kMiniHugeCtas = 32 * 148;  // H3D_MINI_HUGE_CTAS (capped by the workspace slots)
 long long kMiniHugeKin = 1000;   // H3D_MINI_HUGE_KIN
 // after a level on the large mini variant, launch the remaining levels on it
 // without measuring them (no read-back and host sync per level)
@@ -1700,6 +1701,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "mini_ctas") { old = kMiniMaxCtas; if (value >= 0) kMiniMaxCtas = value; }
   else if (k == "mini_tiny_ctas") { old = kMiniTinyCtas; if (value >= 0) kMiniTinyCtas = value; }
   else if (k == "mini_tiny_kin") { old = kMiniTinyKin; if (value >= 0) kMiniTinyKin = value; }
+  else if (k == "mini_one_wave") { old = kMiniOneWave; if (value >= 0) kMiniOneWave = value; }
   else if (k == "mini_huge_ctas") { old = kMiniHugeCtas; if (value >= 0) kMiniHugeCtas = value; }
   else if (k == "mini_huge_kin") { old = kMiniHugeKin; if (value >= 0) kMiniHugeKin = value; }
   else if (k == "mini_seg") { old = g_mini_seglen; if (value >= 1) g_mini_seglen = static_cast<int>(value); }
@@ -1955,15 +1957,25 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     }
     if (g_mini && 2 * jobs < kTpjMinTotalJobs &&
         ((mini_small && 2 * jobs <= 4 * kMiniMaxCtas) ||
-         (2 * jobs <= kMiniMaxCtas && static_cast<long long>(need[6]) <= kMiniMaxPoints &&
-          maxkin <= kMiniMaxEvents))) {
-      const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, mini_small ? 0 : 1);
+         (2 * jobs <= kMiniMaxCtas && static_cast<long long>(need[6]) <= kMiniXlPoints &&
+          maxkin <= kMiniXlEvents))) {
+      // up to two CTAs per SM the large variant (one wave); more jobs take
+      // the smallest variant the level's largest job fits (more CTAs per SM)
+      const long long np = static_cast<long long>(need[6]);
+      const bool one_wave = 2 * jobs <= kMiniOneWave;
+      int var = mini_small ? 0
+                      : one_wave ? 1
+                      : (np <= kMiniMedPoints && maxkin <= kMiniMedEvents)
+                          ? 4
+                          : (np <= kMiniL2Points && maxkin <= kMiniL2Events) ? 5 : 1;
+      if (var == 1 && (np > kMiniMaxPoints || maxkin > kMiniMaxEvents)) var = 6;
+      const long long rm = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, var);
       if (rm < 0) return rm;
-      rec.push_back(LevelRec{lv, REC_MINI, mini_small ? 0 : 1, 0, 0, 0, LaneCfg{}});
+      rec.push_back(LevelRec{lv, REC_MINI, var, 0, 0, 0, LaneCfg{}});
       h3d_prof_end(e0, lv + 5000, 2, s);
       h3d_stamp_route(lv, lv + 5000);
       P = Pass2{P.out0, P.out1, P.in0, P.in1};
-      if (g_mini_spec && !mini_small && lv < lv_hi) {
+      if (g_mini_spec && var == 1 && one_wave && lv < lv_hi) {
         // the remaining levels have at most half these jobs: launch them all
         // on the large variant unmeasured; a job that does not fit records
         // its level in `spec` (later launches then write nothing) and the

@@ -255,6 +255,9 @@ long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, lon
 constexpr int kMiniMaxPoints = 1024, kMiniMaxEvents = 2048;
 constexpr int kMiniHugePoints = 8192, kMiniHugeEvents = 16384;
 constexpr int kMiniSmallPoints = 256, kMiniSmallEvents = 512;
+constexpr int kMiniMedPoints = 320, kMiniMedEvents = 640;
+constexpr int kMiniL2Points = 640, kMiniL2Events = 1280;
+constexpr int kMiniXlPoints = 1152, kMiniXlEvents = 2304;
 constexpr int kMiniTinyPoints = 192, kMiniTinyEvents = 320;
 extern int g_mini_seglen;  // mini.cu: child events per time segment
 

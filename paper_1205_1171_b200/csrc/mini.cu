@@ -774,6 +774,15 @@ long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, lon
                      long long *stamp, void *gscratch, size_t gbytes) {
   if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
   if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
+  // medium (50 KB: 4 CTAs per SM) and large2 (100 KB: 2 per SM) for levels of
+  // many mid-size jobs (sphere-like clouds keep every point)
+  if (variant == 4)
+    return launch_mini<256, kMiniMedEvents, kMiniMedPoints>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
+  if (variant == 5)
+    return launch_mini<512, kMiniL2Events, kMiniL2Points>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
+  // xl: a little past the large variant (64-bit facet words), one CTA per SM
+  if (variant == 6)
+    return launch_mini<1024, kMiniXlEvents, kMiniXlPoints>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
   if (variant == 3)
     return launch_mini<1024, kMiniHugeEvents, kMiniHugePoints>(P, pts, n, lv, j0, j1, err, s, spec, stamp,
                                                                gscratch, gbytes);

@@ -7,8 +7,8 @@ for bit with no exact-engine fallback:
 * lane-per-job on every level (tpj_min_jobs=1, pipeline off), on k_fast_tpj
   and on lane.cu (coordinates / merged events staged in shared memory or not);
 * warp-per-job on every level (tpj_min_jobs huge, pipeline off);
-* each mini variant (one CTA per job in shared memory) wherever its jobs fit,
-  and the huge one (one CTA per job, its arrays in global memory).
+* each mini variant (one CTA per job in shared memory) wherever its jobs fit
+  (tiny, small, medium, large2, large), and the huge one (one CTA per job, its arrays in global memory).
 """
 
 from __future__ import annotations
@@ -42,6 +42,10 @@ ROUTES = {
     "warp_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 0},
     "mini_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
                         "mini_ctas": BIG_OFF, "mini_tiny_ctas": 0},
+    # every level past the one-wave limit: the medium / large2 / large
+    # variants by fit (several CTAs per SM)
+    "mini_multiwave_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
+                                  "mini_ctas": BIG_OFF, "mini_tiny_ctas": 0, "mini_one_wave": 0},
     "mini_huge_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 1,
                              "mini_ctas": 0, "mini_tiny_ctas": 0, "mini_huge_kin": 0,
                              "mini_huge_ctas": 1 << 20},
