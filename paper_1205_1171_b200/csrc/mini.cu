@@ -308,6 +308,10 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   // memory
   MS &m = *reinterpret_cast<MS *>(
       gmem ? gmem + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * gstride : smem_raw);
+  // the per-point counters / cursors / first output events: in shared
+  // memory for the global-memory variant too (its hot atomics), else in the
+  // sweep slab's word array
+  int *const curp = gmem ? reinterpret_cast<int *>(smem_raw) : m.cur();
   __shared__ int s_scan[MINI_T / 32];  // mini_excl_sum's warp totals
   const int tid = threadIdx.x, T = MINI_T;
   const long long j = j0 + lvl_blk();
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     m.Y[p] = c.y;
     m.Z[p] = c.z;
     m.LN[p] = make_short2(static_cast<short>(l.x), static_cast<short>(l.y));
-    m.cur()[p] = 0;
+    curp[p] = 0;
   }
   MINI_TICK(1);
   // ---- merged child sequence S (merge path, left first on equal times);
@@ -406,9 +410,9 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   for (int d = tid; d < kin; d += T) {
     if (d > 0 && m.st[d] == m.st[d - 1]) m.flag = 1;  // exact tie
     const auto w = m.sw[d];
-    atomicAdd(&m.cur()[swa(w)], 1);
-    atomicAdd(&m.cur()[swb(w)], 1);
-    atomicAdd(&m.cur()[swc(w)], 1);
+    atomicAdd(&curp[swa(w)], 1);
+    atomicAdd(&curp[swb(w)], 1);
+    atomicAdd(&curp[swc(w)], 1);
   }
   __syncthreads();
   {
@@ -417,7 +421,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     int sum = 0;
     for (int q = 0; q < per && q < PER; ++q) {
       const int p = tid * per + q;
-      local[q] = p < nS ? m.cur()[p] : 0;
+      local[q] = p < nS ? curp[p] : 0;
       sum += local[q];
     }
     int off;
@@ -429,19 +433,19 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     }
   }
   __syncthreads();
-  for (int p = tid; p < nS; p += T) m.cur()[p] = m.ib[p];
+  for (int p = tid; p < nS; p += T) curp[p] = m.ib[p];
   __syncthreads();
   // scatter (arbitrary order within a list; the owner kept alongside) ...
   for (int d = tid; d < kin; d += T) {
     const auto w = m.sw[d];
     const int pa = swa(w), pb = swb(w), pc = swc(w);
-    int q = atomicAdd(&m.cur()[pa], 1);
+    int q = atomicAdd(&curp[pa], 1);
     m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pa);
-    q = atomicAdd(&m.cur()[pb], 1);
+    q = atomicAdd(&curp[pb], 1);
     m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pb);
-    q = atomicAdd(&m.cur()[pc], 1);
+    q = atomicAdd(&curp[pc], 1);
     m.eo()[q] = static_cast<short>(d);
     m.el[q].x = static_cast<short>(pc);
   }
@@ -633,7 +637,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
       off += local[q];
     }
   }
-  for (int p = tid; p < nS; p += T) m.cur()[p] = 0x7fffffff;  // first output event
+  for (int p = tid; p < nS; p += T) curp[p] = 0x7fffffff;  // first output event
   __syncthreads();
   const int kept = m.cpos()[kin] & ~(1 << 30);
   const int kout = kept + NB;
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     o.c = swc(w);
     o.kind = swk(w);
     evo[idx] = o;
-    atomicMin(&m.cur()[o.b], idx);
+    atomicMin(&curp[o.b], idx);
   }
   for (int i = tid; i < NB; i += T) {
     const double t = m.bt[i];
@@ -675,7 +679,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
     o.c = swc(w);
     o.kind = swk(w);
     evo[idx] = o;
-    atomicMin(&m.cur()[o.b], idx);
+    atomicMin(&curp[o.b], idx);
   }
   __syncthreads();
   MINI_TICK(8);
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
         const short2 l = m.LN[p];
         bool chain = p == 0 || p == nSL || (l.x != NIL && m.LN[l.x].y == p);
         chain = chain && (p < nSL ? p <= uv0.x : p >= uv0.y);
-        const int f = m.cur()[p];
+        const int f = curp[p];
         keep = chain || f != 0x7fffffff;
         short2 o = make_short2(NIL, NIL);
         if (chain) {
@@ -761,7 +765,8 @@ static long long launch_mini(const Pass2 &P, const double *pts, long long n, int
     attr[dev_id] = true;
   }
   h3d_count_launches(1);
-  k_mini<T, K, N><<<lvl_grid(static_cast<unsigned>(j1 - j0), g_interleave != 0), T, gscratch ? 0 : bytes, s>>>(
+  k_mini<T, K, N><<<lvl_grid(static_cast<unsigned>(j1 - j0), g_interleave != 0), T,
+                    gscratch ? N * sizeof(int) : bytes, s>>>(
       P, pts, n, lv, j0, j1, err, g_mini_seglen, spec, stamp, static_cast<unsigned char *>(gscratch),
       stride);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
