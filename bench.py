@@ -75,7 +75,7 @@ def sample_points(cfg: str, sn: int) -> np.ndarray:
         return integer_cloud(sn, seed)
     return generate(sn, dist, seed)
 STATS_KEY = {"C2": "C2_ball_2^20", "C3": "C3_sphere_2^20", "C4": "C4_cube_2^24",
-             "INT": "int_2^20_R2^31"}
+             "INT": "int_2^20_R2^31", "C5": "C5_mixed_2^27"}
 
 
 def parse():

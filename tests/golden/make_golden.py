@@ -197,6 +197,16 @@ if __name__ == "__main__":
     ref = O.reference()
     if ref is None:
         sys.exit("build the reference first: oracle/build_ref.sh")
+    if "--c5-stats" in sys.argv:  # C5 per-level statistics (C restatement, ~20 GB of RAM)
+        from paper_1205_1171_b200.generators import generate
+        spath = os.path.join(HERE, "level_stats.json")
+        stats = json.load(open(spath)) if os.path.exists(spath) else {}
+        sp, _, _ = O.sort_and_perturb(generate(2**27, "mixed", 0))
+        lower = level_stats(sp)
+        sp[:, 2] = -sp[:, 2]
+        stats["C5_mixed_2^27"] = {"lower": lower, "upper": level_stats(sp)}
+        json.dump(stats, open(spath, "w"), indent=1)
+        sys.exit(0)
     if "--c5" in sys.argv:
         make_large(ref, with_c4=False, only_c5=True)
         sys.exit(0)
