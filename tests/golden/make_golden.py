@@ -12,7 +12,7 @@ Needs oracle/_ref/site (oracle/build_ref.sh).  Writes:
                  kernels.copy_log) for a few n, the per-level parity gate.
 * large.json  -- sha256 digests of inputs and outputs for C2/C3/C4 and an
                  integer-coordinate 2^20 cloud (outputs too big to commit).
-* level_stats.json -- per-level J, E_in, E_out, D, kmax for C2/C3/C4, both
+* level_stats.json -- per-level J, E_in, E_out, D, kmax for C2/C3/C4/C5, both
                  passes (SURVEY.md 8(d) algorithmic-bytes model inputs),
                  computed with the C restatement (pinned by small.npz).
 """
