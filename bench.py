@@ -305,6 +305,23 @@ NCU_NAMES = {
 }
 
 
+def measured_inst(cfg: str, name: str):
+    """Warp instructions per launch (smsp__inst_executed.sum) of the kernel,
+    from the same committed ncu launch list as measured_traffic."""
+    import glob
+
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_launches_{cfg.lower()}.json")),
+                   key=lambda q: int(os.path.basename(q)[1:].split("_", 1)[0]))
+    if not cands:
+        return None
+    doc = json.load(open(cands[-1]))
+    pre = NCU_NAMES.get(name, (name,))
+    ks = [k for k in doc["kernels"] if k["kernel"].startswith(pre) and k.get("warp_inst")]
+    if not ks or name == "k_big_level":
+        return None
+    return sum(k["warp_inst"] for k in ks) // max(sum(k["launches"] for k in ks), 1)
+
+
 def measured_traffic(cfg: str, name: str):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
     of the kernel, from the committed ncu launch list of this config
@@ -427,6 +444,17 @@ def run_ours(args):
                 "kernel_ms_per_step": d["time"] * 1e3 / args.steps,
                 "share_of_step": d["time"] * 1e3 / args.steps / ms,
                 "bytes_per_step": d["bytes"] // args.steps}
+        # the bound these sweeps actually meet: instruction issue (4 warp
+        # instructions per SM per cycle at the measured SM clock), from the
+        # ncu instruction count per launch and this run's kernel time
+        wi = measured_inst(args.config, name)
+        if wi and d["time"] > 0:
+            sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+            peak_issue = 4 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
+            got = wi * d["launches"] / d["time"]
+            roof["issue"] = {"achieved": got, "peak": peak_issue, "unit": "warp instructions/s",
+                             "frac": got / peak_issue, "warp_inst_per_launch": wi,
+                             "source": "smsp__inst_executed.sum, " + (tsrc or "")}
 
     # end to end through the public API with host buffers (W untimed calls
     # first: the pinned result buffers come from torch's caching host

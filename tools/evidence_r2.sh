@@ -4,7 +4,7 @@
 # dominant kernels.   gpurun -- 'bash tools/evidence_r2.sh TAG'
 tag=${1:-r2ev}
 out=gpurun_out/$tag; mkdir -p $out
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum
 for c in C4 C2 C3; do
   timeout 900 ncu --metrics $M --clock-control none --csv --log-file $out/launches_${c}.csv \
     python tools/one_hull.py $c 3 > $out/ncu_list_${c}.log 2>&1

@@ -39,10 +39,11 @@ def launches(path: str, hulls: int, out: str) -> None:
         k = name.split("(")[0].replace("void ", "")
         t_ms = m.get("gpu__time_duration.sum", 0.0) / 1e6
         dram = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-        a = agg.setdefault(k, {"launches": 0, "ms": 0.0, "dram_bytes": 0.0})
+        a = agg.setdefault(k, {"launches": 0, "ms": 0.0, "dram_bytes": 0.0, "warp_inst": 0.0})
         a["launches"] += 1
         a["ms"] += t_ms
         a["dram_bytes"] += dram
+        a["warp_inst"] += m.get("smsp__inst_executed.sum", 0.0)
         seq.append({"kernel": k, "ms": round(t_ms, 4), "dram_bytes": int(dram)})
     total = sum(a["ms"] for a in agg.values())
     kernels = []
@@ -51,7 +52,9 @@ def launches(path: str, hulls: int, out: str) -> None:
                         "share": round(a["ms"] / total, 4) if total else None,
                         "dram_bytes": int(a["dram_bytes"]),
                         "dram_bytes_per_launch": int(a["dram_bytes"] / a["launches"]),
-                        "dram_gbps": round(a["dram_bytes"] / a["ms"] / 1e6, 1) if a["ms"] else None})
+                        "dram_gbps": round(a["dram_bytes"] / a["ms"] / 1e6, 1) if a["ms"] else None,
+                        "warp_inst": int(a["warp_inst"]),
+                        "warp_inst_per_launch": int(a["warp_inst"] / a["launches"])})
     doc = {"source": path, "hulls_in_capture": hulls, "note":
            "ncu --clock-control none, serialised cold-cache launches: compare shares, not absolutes",
            "total_ms": round(total, 4), "kernels": kernels, "sequence": seq}
