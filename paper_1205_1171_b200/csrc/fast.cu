@@ -449,6 +449,14 @@ __host__ __device__ __forceinline__ long long warp_job_bytes(int nS, int kin) {
   return align8(32ll * nS + 4ll * nS) + 24ll * kin;
 }
 
+// histogram bin of a CTA's point sum (six bins per octave) and the largest
+// sum a bin holds
+__host__ __device__ __forceinline__ int need_bin(unsigned long long t) {
+  const int b = static_cast<int>(6.0 * log2(static_cast<double>(t)));
+  return b < 0 ? 0 : (b >= kNeedHistBins ? kNeedHistBins - 1 : b);
+}
+inline long long need_bin_max(int b) { return static_cast<long long>(floor(exp2((b + 1) / 6.0))); }
+
 // Shared-memory need of the thread-per-job launch, for every jobs-per-CTA
 // choice at once: out[r] = max over CTAs of sum(nS) when a CTA takes
 // 32 >> r consecutive jobs (r = 0..5); out[6] = largest single nS; out[7] =
@@ -477,6 +485,12 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
 #pragma unroll
   for (int q = 0; q < 24; ++q) lb[q] = 0;
   unsigned long long ksum = 0;
+  // out[kNeedHist + b]: CTAs (32 jobs) whose point sum falls in bin b
+  // (b = floor(6 log2 sum): six bins per octave) -- the host sizes a split
+  // level's small pool from it
+  __shared__ unsigned s_hist[kNeedHistBins];
+  for (int q = threadIdx.x; q < kNeedHistBins; q += blockDim.x) s_hist[q] = 0;
+  __syncthreads();
   for (long long c = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
     const long long j = j0 + c * 32 + lane;
@@ -521,6 +535,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
       t += __shfl_xor_sync(FULL, t, 1 << (4 - r));
       mx[r] = t > mx[r] ? t : mx[r];
     }
+    if (lane == 0 && t > 0) atomicAdd(&s_hist[need_bin(t)], 1u);
   }
   // warp, then block reduction; one atomic per value per block
   __shared__ unsigned long long red[32][34];
@@ -558,23 +573,23 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
       if (threadIdx.x == 9) atomicAdd(out + 9, m); else atomicMax(out + slot, m);
     }
   }
+  for (int q = threadIdx.x; q < kNeedHistBins; q += blockDim.x)
+    if (s_hist[q]) atomicAdd(out + kNeedHist + q, static_cast<unsigned long long>(s_hist[q]));
 }
 
+// One CTA (32 jobs of pass `pass`, job chunk `blk`).  With ovf (a split
+// level): a CTA whose jobs do not fit the pool is appended to the overflow
+// list for the big-pool launch instead of failing.
 template <bool XYZ>
 __device__ __forceinline__ void tpj_body(Pass2 P, const double *__restrict__ pts, long long n, int level,
                                          long long j0, long long j1, long long *err, int pool, int jpc,
-                                         int prefetch, long long *spec, long long *stamp) {
-  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    *stamp = static_cast<long long>(t);
-  }
+                                         int prefetch, long long *spec, long long blk, int pass, int *ovf,
+                                         long long ovf_cap) {
   // an earlier level failed, or (a replayed plan, spec) did not fit: stop
   // (warp-uniform; the words it reads may be stale)
   if (__any_sync(0xffffffffu, *reinterpret_cast<volatile long long *>(err) != 0 ||
                                   (spec && *reinterpret_cast<volatile long long *>(spec) != 0)))
     return;
-  const int pass = lvl_pass();
   const GroupBuf in = pass ? P.in1 : P.in0;
   const GroupBuf out = pass ? P.out1 : P.out0;
   const double zs = pass ? -1.0 : 1.0;
@@ -582,7 +597,7 @@ __device__ __forceinline__ void tpj_body(Pass2 P, const double *__restrict__ pts
   const int lane = threadIdx.x;
   const long long size = 1ll << level, half = size >> 1;
   // jpc (1..32) jobs per CTA: lanes >= jpc idle (large jobs, few per CTA)
-  const long long j = j0 + lvl_blk() * jpc + lane;
+  const long long j = j0 + blk * jpc + lane;
   const long long L = j << level, M = L + half;
   const long long R_ = (L + size < n) ? L + size : n;
   int nSL = 0, kL = 0, nSR = 0, kR = 0;
@@ -623,6 +638,14 @@ __device__ __forceinline__ void tpj_body(Pass2 P, const double *__restrict__ pts
   const int total = __shfl_sync(FULL, off, 31);
   off -= bytes;
   if (total > pool) {  // the host sizes the pool from the measured need (or a replayed plan's)
+    if (ovf) {  // a split level: the big-pool launch takes this CTA
+      if (lane == 0) {
+        const int i = atomicAdd(ovf, 1);
+        if (i < ovf_cap) ovf[1 + i] = static_cast<int>(2 * blk + pass);
+        else raise_err(err, E_FASTPATH);
+      }
+      return;
+    }
     if (lane == 0) {
       if (spec)
         atomicCAS(reinterpret_cast<unsigned long long *>(spec), 0ull, static_cast<unsigned long long>(level));
@@ -831,19 +854,41 @@ __device__ __forceinline__ void tpj_body(Pass2 P, const double *__restrict__ pts
 // compiler's own (156 registers, 12 warps/SM) and a 128-register cap (16
 // warps/SM) that pays at the lower levels, where more resident jobs hide the
 // gathers (measured per level, g_tpj_cap_level)
+__device__ __forceinline__ void level_stamp(long long *stamp) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *stamp = static_cast<long long>(t);
+  }
+}
 template <bool XYZ>
 __global__ void __launch_bounds__(32) k_fast_tpj(Pass2 P, const double *__restrict__ pts, long long n,
                                                  int level, long long j0, long long j1, long long *err,
                                                  int pool, int jpc, int prefetch, long long *spec,
-                                                 long long *stamp) {
-  tpj_body<XYZ>(P, pts, n, level, j0, j1, err, pool, jpc, prefetch, spec, stamp);
+                                                 long long *stamp, int *ovf, long long ovf_cap) {
+  level_stamp(stamp);
+  tpj_body<XYZ>(P, pts, n, level, j0, j1, err, pool, jpc, prefetch, spec, lvl_blk(), lvl_pass(), ovf, ovf_cap);
 }
 template <bool XYZ>
 __global__ void __launch_bounds__(32, 16) k_fast_tpj_r128(Pass2 P, const double *__restrict__ pts, long long n,
                                                           int level, long long j0, long long j1, long long *err,
                                                           int pool, int jpc, int prefetch, long long *spec,
-                                                          long long *stamp) {
-  tpj_body<XYZ>(P, pts, n, level, j0, j1, err, pool, jpc, prefetch, spec, stamp);
+                                                          long long *stamp, int *ovf, long long ovf_cap) {
+  level_stamp(stamp);
+  tpj_body<XYZ>(P, pts, n, level, j0, j1, err, pool, jpc, prefetch, spec, lvl_blk(), lvl_pass(), ovf, ovf_cap);
+}
+// the CTAs a split level's small-pool launch left (the list it wrote),
+// with the level's full pool; any grid (a CTA loops over the list)
+__global__ void __launch_bounds__(32) k_fast_tpj_ovf(Pass2 P, const double *__restrict__ pts, long long n,
+                                                     int level, long long j0, long long j1, long long *err,
+                                                     int pool, int jpc, int prefetch, long long *spec,
+                                                     const int *ovf) {
+  const int cnt = *reinterpret_cast<const volatile int *>(ovf);
+  for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
+    const int e = ovf[1 + i];
+    tpj_body<false>(P, pts, n, level, j0, j1, err, pool, jpc, prefetch, spec, e >> 1, e & 1, nullptr, 0);
+    __syncwarp();
+  }
 }
 
 // ------------------------------------------------------------- leaf levels
@@ -1591,6 +1636,8 @@ long long kMiniHugeKin = 1000;   // H3D_MINI_HUGE_KIN
 // without measuring them (no read-back and host sync per level)
 int g_mini_spec = 1;  // H3D_MINI_SPEC
 int g_trace = 0;      // H3D_TRACE: one stderr line per routed level
+long long kTpjXyzCtas = 4 * 148;  // tpj_xyz_ctas: stage coordinates on levels of at most this many CTAs
+int g_tpj_split = 1;  // H3D_TPJ_SPLIT: small-pool launch + big-pool launch for levels of a few large CTAs
 int g_tpj_cap_level = 6;  // H3D_TPJ_CAP_LEVEL: k_fast_tpj levels <= this at 128 registers
 int g_lane = 1;       // H3D_LANE: lane-per-job levels on lane.cu (0 = k_fast_tpj)
 // highest level routed to lane.cu; k_fast_tpj above (measured per level, C4:
@@ -1617,6 +1664,8 @@ struct LevelRec {
   int lv, kind, variant, jpc, prefetch;
   long long pool;
   LaneCfg lane;
+  long long pool2 = 0;  // a split lane-per-job level: the big pool (0: not split)
+  int ogrid = 0;        // ... and the big-pool launch's grid
 };
 struct PlanKey {
   int dev;
@@ -1672,6 +1721,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_PLAN")) g_plan = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_INTERLEAVE")) g_interleave = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_TPJ_CAP_LEVEL")) g_tpj_cap_level = atoi(e);
+  if (const char *e = getenv("H3D_TPJ_SPLIT")) g_tpj_split = atoi(e);
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
@@ -1679,11 +1729,56 @@ template <bool XYZ>
 void launch_tpj(dim3 grid, int pool, int jpc, int prefetch, cudaStream_t s, Pass2 P,
                 const double *pts,
                 long long n, int lv, long long j0, long long j1, long long *err,
-                long long *spec = nullptr, long long *stamp = nullptr) {
+                long long *spec = nullptr, long long *stamp = nullptr, const TpjSplit *sp = nullptr) {
+  // a split level: the CTAs that do not fit the small pool go to the list,
+  // then to the big-pool launch
+  int *ovf = sp ? sp->ovf : nullptr;
+  const long long cap = sp ? sp->cap : 0;
+  if (ovf) cudaMemsetAsync(ovf, 0, sizeof(int), s);
   if (lv <= g_tpj_cap_level)
-    k_fast_tpj_r128<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp);
+    k_fast_tpj_r128<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp, ovf,
+                                                cap);
   else
-    k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp);
+    k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp, ovf, cap);
+  if (ovf) {
+    h3d_count_launches(1);
+    k_fast_tpj_ovf<<<sp->grid, 32, sp->pool, s>>>(P, pts, n, lv, j0, j1, err, sp->pool, jpc, prefetch, spec,
+                                                  ovf);
+  }
+}
+
+// Split a lane-per-job level whose largest CTA needs far more shared memory
+// than most (x-extreme runs of hull points, C5's shell): the small pool
+// covers all CTAs but at most an eighth, and at most about one wave of the
+// big-pool launch, and only when it fits more CTAs per SM.
+// need[kNeedHist ..]: the per-CTA histogram of point sums.  tpj_split = 2
+// (tests): split at the median, whatever the occupancy.
+bool tpj_split(const unsigned long long *need, long long pool, int lv, TpjSplit *sp) {
+  if (!g_tpj_split) return false;
+  const int regcap = lv <= g_tpj_cap_level ? 16 : 12;
+  auto occ = [&](long long P) {
+    const long long by_smem = 233472 / (P + 1024);
+    return by_smem < regcap ? by_smem : static_cast<long long>(regcap);
+  };
+  long long C = 0;
+  for (int b = 0; b < kNeedHistBins; ++b) C += static_cast<long long>(need[kNeedHist + b]);
+  const bool force = g_tpj_split == 2;
+  long long allowed = 148 * occ(pool);
+  if (allowed > C / 8) allowed = C / 8;
+  if (force) allowed = C / 2;
+  long long above = C;
+  for (int b = 0; b < kNeedHistBins; ++b) {
+    above -= static_cast<long long>(need[kNeedHist + b]);
+    if (above > allowed) continue;
+    long long small = 12 * need_bin_max(b) + 32 * 16;
+    if (small < 1024) small = 1024;
+    if (small >= pool || (!force && occ(small) <= occ(pool))) return false;
+    sp->small = small;
+    sp->pool = static_cast<int>(pool);
+    sp->grid = static_cast<int>(above < 1 ? 1 : above);
+    return true;
+  }
+  return false;
 }
 
 }  // namespace
@@ -1698,6 +1793,8 @@ int64_t h3d_tune(const char *name, int64_t value) {
   if (k == "plan") { old = g_plan; if (value >= 0) g_plan = value ? 1 : 0; }
   if (k == "interleave") { old = g_interleave; if (value >= 0) g_interleave = value ? 1 : 0; }
   else if (k == "tpj_cap_level") { old = g_tpj_cap_level; if (value >= 0) g_tpj_cap_level = value; }
+  else if (k == "tpj_xyz_ctas") { old = kTpjXyzCtas; if (value >= 0) kTpjXyzCtas = value; }
+  else if (k == "tpj_split") { old = g_tpj_split; if (value >= 0) g_tpj_split = static_cast<int>(value); }
   if (k == "big_kin") { old = kBigKin; if (value >= 0) kBigKin = value; }
   else if (k == "leaf_b") { old = g_leaf_b; if (value >= 0) g_leaf_b = leaf_depth(value); }
   else if (k == "mini") { old = g_mini; if (value >= 0) g_mini = value ? 1 : 0; }
@@ -1772,6 +1869,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
         h3d_check(cudaFuncSetAttribute(k_fast_tpj<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
+        h3d_check(cudaFuncSetAttribute(k_fast_tpj_ovf, cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
         h3d_check(cudaFuncSetAttribute(k_fast_tpj_r128<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kTpjPool)) ||
         h3d_check(cudaFuncSetAttribute(k_fast_tpj_r128<false>,
@@ -1871,12 +1969,14 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
           void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
           h3d_count_launches(1);
           const dim3 grid = lvl_grid(h3d_grid(j1 - j0, r.jpc), g_interleave != 0);
-          if (r.variant)
+          if (r.variant) {
             launch_tpj<true>(grid, static_cast<int>(r.pool), r.jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err,
                              spec, stp);
-          else
+          } else {
+            TpjSplit sp{w0.ovf, w0.ovf_cap, static_cast<int>(r.pool2), r.ogrid, 0};
             launch_tpj<false>(grid, static_cast<int>(r.pool), r.jpc, r.prefetch, s, P, sorted_pts, n, lv, j0,
-                              j1, err, spec, stp);
+                              j1, err, spec, stp, r.pool2 ? &sp : nullptr);
+          }
           h3d_prof_end(ek, tag, 2, s);
         } else {  // REC_WARP: an oversized job runs in HBM mode, always fits
           h3d_count_launches(1);
@@ -1920,12 +2020,12 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     // they fit a shared-memory slice (int16 local ids); one warp per job
     // (1-warp CTAs, pool = the largest job's need, HBM mode above it) for
     // the few-job levels.
-    cudaMemsetAsync(w0.need, 0, 40 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(w0.need, 0, (kNeedHist + kNeedHistBins) * sizeof(unsigned long long), s);
     const long long chunks = (jobs + 31) / 32;
     h3d_count_launches(1);
     k_tpj_need<<<dim3(h3d_grid(chunks, 8) > 2 * 148 ? 2 * 148 : h3d_grid(chunks, 8), 2), 256, 0, s>>>(
         P, n, lv, j0, j1, w0.need, err, h3d_stamp_buf() ? h3d_stamp_buf() + lv : nullptr);
-    unsigned long long need[40];
+    unsigned long long need[kNeedHist + kNeedHistBins];
     if (h3d_check(cudaMemcpyAsync(need, w0.need, sizeof(need), cudaMemcpyDeviceToHost, s)) ||
         h3d_check(h3d_sync(s)))
       return H3D_E_CUDA;
@@ -2075,7 +2175,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         // too few CTAs for shared memory to limit occupancy
         const long long ctas = 2 * ((jobs + jpc - 1) / jpc);
         xyz = 36ll * need[r] + 32 * 16 <= kTpjXyzMax ||
-              (ctas <= 4 * 148 && 36ll * need[r] + 32 * 16 <= kTpjPool);
+              (ctas <= kTpjXyzCtas && 36ll * need[r] + 32 * 16 <= kTpjPool);
         pool = (xyz ? 36ll : 12ll) * need[r] + 32 * 16;
         if (pool < 1024) pool = 1024;
       }
@@ -2096,16 +2196,26 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       tpj = false;
     }
     if (tpj) {
-      if (g_trace) fprintf(stderr, "h3d level %d: tpj xyz %d jpc %d pool %lld\n", lv, xyz ? 1 : 0, jpc, pool);
+      TpjSplit sp{w0.ovf, w0.ovf_cap, 0, 0, 0};
+      const bool split = !xyz && jpc == 32 && tpj_split(need, pool, lv, &sp);
+      if (g_trace)
+        fprintf(stderr, "h3d level %d: tpj xyz %d jpc %d pool %lld split %lld / %d (%d CTAs)\n", lv, xyz ? 1 : 0,
+                jpc, pool, split ? sp.small : 0, split ? sp.pool : 0, split ? sp.grid : 0);
       h3d_count_launches(1);
       void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
       const dim3 grid = lvl_grid(h3d_grid(jobs, jpc), g_interleave != 0);
       if (xyz)
         launch_tpj<true>(grid, static_cast<int>(pool), jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err);
       else
-        launch_tpj<false>(grid, static_cast<int>(pool), jpc, jobs >= kTpjPrefetchJobs ? 1 : 0, s, P,
-                          sorted_pts, n, lv, j0, j1, err);
-      rec.push_back(LevelRec{lv, REC_TPJ, xyz ? 1 : 0, jpc, jobs >= kTpjPrefetchJobs ? 1 : 0, pool, LaneCfg{}});
+        launch_tpj<false>(grid, static_cast<int>(split ? sp.small : pool), jpc, jobs >= kTpjPrefetchJobs ? 1 : 0,
+                          s, P, sorted_pts, n, lv, j0, j1, err, nullptr, nullptr, split ? &sp : nullptr);
+      LevelRec lr{lv, REC_TPJ, xyz ? 1 : 0, jpc, jobs >= kTpjPrefetchJobs ? 1 : 0, split ? sp.small : pool,
+                  LaneCfg{}};
+      if (split) {
+        lr.pool2 = sp.pool;
+        lr.ogrid = sp.grid;
+      }
+      rec.push_back(lr);
       h3d_prof_end(ek, lv + 1000, 2, s);
       h3d_prof_end(e0, lv + 1000, 2, s);
       h3d_stamp_route(lv, lv + 1000);

@@ -198,7 +198,18 @@ struct PassWS {
   GroupBuf A, B;
   Ev *seq;                  // merged child events of HBM-resident warp jobs (2n)
   Rec *rec;                 // records of HBM-resident warp jobs (n)
-  unsigned long long *need; // thread-per-job pool sizing
+  unsigned long long *need; // thread-per-job pool sizing (+ the per-CTA need histogram)
+  int *ovf;                 // CTAs of a split lane-per-job level left to the big-pool launch
+  long long ovf_cap;
+};
+constexpr int kNeedWords = 48, kNeedHist = 64, kNeedHistBins = 128;  // need[64 .. 192): histogram
+// a split lane-per-job level (fast.cu tpj_split): the overflow list, the big
+// pool and its launch's grid, and the small pool
+struct TpjSplit {
+  int *ovf;
+  long long cap;
+  int pool, grid;
+  long long small;
 };
 
 inline bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
@@ -210,7 +221,9 @@ inline bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
   }
   w.seq = ar.take<Ev>(2 * n);
   w.rec = ar.take<Rec>(n);
-  w.need = ar.take<unsigned long long>(48);
+  w.need = ar.take<unsigned long long>(kNeedHist + kNeedHistBins);
+  w.ovf_cap = (n >> 4) + 64;
+  w.ovf = ar.take<int>(w.ovf_cap + 1);
   return ar.base == nullptr || w.need != nullptr;
 }
 

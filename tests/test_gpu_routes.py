@@ -5,7 +5,7 @@ for bit with no exact-engine fallback:
 * leaf kernel depth 0 / 3 / 4 (levels 1..B fused in shared memory);
 * the time-split pipeline (big.cu) on almost every level (big_kin=16);
 * lane-per-job on every level (tpj_min_jobs=1, pipeline off), on k_fast_tpj
-  and on lane.cu (coordinates / merged events staged in shared memory or not);
+  (its default and its 128-register build) and on lane.cu (coordinates / merged events staged in shared memory or not);
 * warp-per-job on every level (tpj_min_jobs huge, pipeline off);
 * each mini variant (one CTA per job in shared memory) wherever its jobs fit
   (tiny, small, medium, large2, large), and the huge one (one CTA per job, its arrays in global memory).
@@ -33,6 +33,12 @@ ROUTES = {
     "big_everywhere": {"big_kin": 16, "mini": 0},
     "big_everywhere_no_leaf": {"big_kin": 2, "leaf_b": 0, "mini": 0},
     "tpj_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0, "lane": 0},
+    "tpj_r128_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0, "lane": 0,
+                            "tpj_cap_level": 40},
+    # every lane-per-job level split at its median CTA: half the CTAs on the
+    # small-pool launch, the rest through the overflow list
+    "tpj_split_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0, "lane": 0,
+                             "tpj_split": 2, "tpj_xyz_kb": 0, "tpj_xyz_ctas": 0},
     "lane_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
                         "lane_max_level": 40},
     "lane_staged_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
