@@ -641,8 +641,12 @@ __device__ __forceinline__ void tpj_body(Pass2 P, const double *__restrict__ pts
     if (ovf) {  // a split level: the big-pool launch takes this CTA
       if (lane == 0) {
         const int i = atomicAdd(ovf, 1);
-        if (i < ovf_cap) ovf[1 + i] = static_cast<int>(2 * blk + pass);
-        else raise_err(err, E_FASTPATH);
+        if (i < ovf_cap)
+          ovf[1 + i] = static_cast<int>(2 * blk + pass);
+        else if (spec)  // a replayed plan's list launch is too small: measured again
+          atomicCAS(reinterpret_cast<unsigned long long *>(spec), 0ull, static_cast<unsigned long long>(level));
+        else
+          raise_err(err, E_FASTPATH);
       }
       return;
     }
@@ -1665,7 +1669,8 @@ struct LevelRec {
   long long pool;
   LaneCfg lane;
   long long pool2 = 0;  // a split lane-per-job level: the big pool (0: not split)
-  int ogrid = 0;        // ... and the big-pool launch's grid
+  int ogrid = 0;        // ... and the big-pool (or mini list) launch's grid
+  int mini = -1;        // a hybrid level: the mini variant of the large CTAs' jobs
 };
 struct PlanKey {
   int dev;
@@ -1726,25 +1731,74 @@ void load_env_once() {
 }
 
 template <bool XYZ>
-void launch_tpj(dim3 grid, int pool, int jpc, int prefetch, cudaStream_t s, Pass2 P,
+long long launch_tpj(dim3 grid, int pool, int jpc, int prefetch, cudaStream_t s, Pass2 P,
                 const double *pts,
                 long long n, int lv, long long j0, long long j1, long long *err,
                 long long *spec = nullptr, long long *stamp = nullptr, const TpjSplit *sp = nullptr) {
   // a split level: the CTAs that do not fit the small pool go to the list,
   // then to the big-pool launch
   int *ovf = sp ? sp->ovf : nullptr;
-  const long long cap = sp ? sp->cap : 0;
+  // the mini's list launch has a fixed grid: more large CTAs than it covers
+  // fail the level (a replayed plan: measured again)
+  const long long cap = sp ? (sp->mini >= 0 && sp->grid < sp->cap ? sp->grid : sp->cap) : 0;
   if (ovf) cudaMemsetAsync(ovf, 0, sizeof(int), s);
   if (lv <= g_tpj_cap_level)
     k_fast_tpj_r128<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp, ovf,
                                                 cap);
   else
     k_fast_tpj<XYZ><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, prefetch, spec, stamp, ovf, cap);
-  if (ovf) {
+  if (ovf && sp->mini >= 0) {  // hybrid: the large CTAs' jobs one CTA each on a mini variant
+    h3d_count_launches(1);
+    const long long rm = mini_level(P, pts, n, lv, j0, j1, err, s, sp->mini, spec, nullptr, sp->scratch,
+                                    sp->scratch_bytes, ovf, sp->grid);
+    if (rm < 0) return rm;
+  } else if (ovf) {
     h3d_count_launches(1);
     k_fast_tpj_ovf<<<sp->grid, 32, sp->pool, s>>>(P, pts, n, lv, j0, j1, err, sp->pool, jpc, prefetch, spec,
                                                   ovf);
   }
+  return 0;
+}
+
+// The hybrid route for a level the time-split pipeline would take because
+// of a few large jobs (C5's shell runs): lane per job on a small pool for
+// all CTAs but at most an eighth, the large CTAs' jobs one CTA each on the
+// smallest mini variant that fits the level's largest job.
+// The huge variant (global-memory slots, one per list CTA) when the level's
+// largest job needs it and the slots of the large CTAs fit the scratch.
+bool tpj_hybrid(const unsigned long long *need, long long maxkin, size_t gbytes, TpjSplit *sp) {
+  if (!g_tpj_split) return false;
+  const long long np = static_cast<long long>(need[6]);
+  int var = -1;
+  if (np <= kMiniSmallPoints && maxkin <= kMiniSmallEvents) var = 0;
+  else if (np <= kMiniMedPoints && maxkin <= kMiniMedEvents) var = 4;
+  else if (np <= kMiniL2Points && maxkin <= kMiniL2Events) var = 5;
+  else if (np <= kMiniMaxPoints && maxkin <= kMiniMaxEvents) var = 1;
+  else if (np <= kMiniXlPoints && maxkin <= kMiniXlEvents) var = 6;
+  else if (np <= kMiniHugePoints && maxkin <= kMiniHugeEvents) var = 3;
+  if (var < 0) return false;
+  long long C = 0;
+  for (int b = 0; b < kNeedHistBins; ++b) C += static_cast<long long>(need[kNeedHist + b]);
+  long long cap = C / 8;
+  if (var == 3) {
+    const long long slots = static_cast<long long>(gbytes / mini_huge_stride()) / 32;
+    if (slots < 1) return false;  // not even one list entry's slots
+    if (slots < cap) cap = slots;
+  }
+  long long above = C;
+  for (int b = 0; b < kNeedHistBins; ++b) {
+    above -= static_cast<long long>(need[kNeedHist + b]);
+    if (above > cap) continue;
+    long long small = 12 * need_bin_max(b) + 32 * 16;
+    if (small < 1024) small = 1024;
+    if (small > kTpjPool) return false;
+    sp->small = small;
+    sp->pool = 0;
+    sp->grid = static_cast<int>(above < 1 ? 1 : above);
+    sp->mini = var;
+    return true;
+  }
+  return false;
 }
 
 // Split a lane-per-job level whose largest CTA needs far more shared memory
@@ -1973,9 +2027,9 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
             launch_tpj<true>(grid, static_cast<int>(r.pool), r.jpc, 0, s, P, sorted_pts, n, lv, j0, j1, err,
                              spec, stp);
           } else {
-            TpjSplit sp{w0.ovf, w0.ovf_cap, static_cast<int>(r.pool2), r.ogrid, 0};
-            launch_tpj<false>(grid, static_cast<int>(r.pool), r.jpc, r.prefetch, s, P, sorted_pts, n, lv, j0,
-                              j1, err, spec, stp, r.pool2 ? &sp : nullptr);
+            TpjSplit sp{w0.ovf, w0.ovf_cap, static_cast<int>(r.pool2), r.ogrid, 0, r.mini, big_ws, big_bytes};
+            rc = launch_tpj<false>(grid, static_cast<int>(r.pool), r.jpc, r.prefetch, s, P, sorted_pts, n, lv,
+                                   j0, j1, err, spec, stp, (r.pool2 || r.mini >= 0) ? &sp : nullptr);
           }
           h3d_prof_end(ek, tag, 2, s);
         } else {  // REC_WARP: an oversized job runs in HBM mode, always fits
@@ -2140,6 +2194,33 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         rec.push_back(LevelRec{lv, REC_MINI, 3, 0, 0, 0, LaneCfg{}});
         h3d_prof_end(e0, lv + 5000, 2, s);
         h3d_stamp_route(lv, lv + 5000);
+        P = Pass2{P.out0, P.out1, P.in0, P.in1};
+        continue;
+      }
+    }
+    // a few large jobs among many small ones: lane per job + mini (hybrid)
+    {
+      TpjSplit sp{w0.ovf, w0.ovf_cap, 0, 0, 0, -1, big_ws, big_bytes};
+      const bool big_wants = big_ws && (maxkin >= kBigKin || (2 * maxkin >= kBigKin && sumkin >= kBigTotal &&
+                                                              2 * jobs < kBigMaxJobs));
+      if (big_wants && lv <= kTpjMaxLevel && 2 * jobs >= kTpjMinTotalJobs && tpj_hybrid(need, maxkin, big_bytes, &sp)) {
+        if (g_trace)
+          fprintf(stderr, "h3d level %d: hybrid pool %lld, <= %d large CTAs on mini variant %d\n", lv, sp.small,
+                  sp.grid, sp.mini);
+        h3d_count_launches(1);
+        void *ek = h3d_prof_kernels() ? h3d_prof_begin(s) : nullptr;
+        const dim3 grid = lvl_grid(h3d_grid(jobs, 32), g_interleave != 0);
+        const int pf = jobs >= kTpjPrefetchJobs ? 1 : 0;
+        const long long rt = launch_tpj<false>(grid, static_cast<int>(sp.small), 32, pf, s, P, sorted_pts, n, lv,
+                                               j0, j1, err, nullptr, nullptr, &sp);
+        if (rt < 0) return rt;
+        LevelRec lr{lv, REC_TPJ, 0, 32, pf, sp.small, LaneCfg{}};
+        lr.ogrid = sp.grid;
+        lr.mini = sp.mini;
+        rec.push_back(lr);
+        h3d_prof_end(ek, lv + 1000, 2, s);
+        h3d_prof_end(e0, lv + 1000, 2, s);
+        h3d_stamp_route(lv, lv + 1000);
         P = Pass2{P.out0, P.out1, P.in0, P.in1};
         continue;
       }

@@ -210,6 +210,9 @@ struct TpjSplit {
   long long cap;
   int pool, grid;
   long long small;
+  int mini = -1;  // >= 0: the list goes to this mini variant (one CTA per job) instead
+  void *scratch = nullptr;  // the huge variant's global-memory slots
+  size_t scratch_bytes = 0;
 };
 
 inline bool carve_pass(h3d_arena &ar, long long n, PassWS &w) {
@@ -261,10 +264,12 @@ extern int g_lane_stage;
 
 // variant 3 (huge): <= kMiniHugePoints / kMiniHugeEvents per job, the job's
 // arrays in global-memory slots of gscratch (returns 1 when they do not fit)
+size_t mini_huge_stride();  // bytes of one huge-variant global-memory slot
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant,
                      long long *spec = nullptr, long long *stamp = nullptr,
-                     void *gscratch = nullptr, size_t gbytes = 0);
+                     void *gscratch = nullptr, size_t gbytes = 0, const int *list = nullptr,
+                     int list_grid = 0);
 constexpr int kMiniMaxPoints = 1024, kMiniMaxEvents = 2048;
 constexpr int kMiniHugePoints = 8192, kMiniHugeEvents = 16384;
 constexpr int kMiniSmallPoints = 256, kMiniSmallEvents = 512;

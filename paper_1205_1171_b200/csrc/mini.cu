@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
                                                  long long n, int lv, long long j0, long long j1,
                                                  long long *err, int seglen, long long *spec,
                                                  long long *stamp, unsigned char *gmem,
-                                                 size_t gstride) {
+                                                 size_t gstride, const int *list) {
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -314,7 +314,20 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
   int *const curp = gmem ? reinterpret_cast<int *>(smem_raw) : m.cur();
   __shared__ int s_scan[MINI_T / 32];  // mini_excl_sum's warp totals
   const int tid = threadIdx.x, T = MINI_T;
-  const long long j = j0 + lvl_blk();
+  // list mode (a split lane-per-job level's large CTAs): 32 CTAs per list
+  // entry (2 * chunk + pass), one per job of the 32-job chunk
+  long long j;
+  int pass;
+  if (list) {
+    const int e = static_cast<int>(blockIdx.x >> 5);
+    if (e >= *reinterpret_cast<const volatile int *>(list)) return;
+    const int v = list[1 + e];
+    pass = v & 1;
+    j = j0 + static_cast<long long>(v >> 1) * 32 + (blockIdx.x & 31);
+  } else {
+    j = j0 + lvl_blk();
+    pass = lvl_pass();
+  }
   if (j >= j1) return;
   // Stop when an earlier launch failed, or (speculative top levels) when a
   // job of an earlier level did not fit, so this level's input is not valid:
@@ -327,7 +340,6 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
              (spec && *reinterpret_cast<volatile long long *>(spec) != 0);
   __syncthreads();
   if (s_stop) return;
-  const int pass = lvl_pass();
   const GroupBuf in = pass ? P.in1 : P.in0;
   const GroupBuf out = pass ? P.out1 : P.out0;
   const double zs = pass ? -1.0 : 1.0;
@@ -749,7 +761,8 @@ __global__ void __launch_bounds__(MINI_T) k_mini(Pass2 P, const double *__restri
 template <int T, int K, int N>
 static long long launch_mini(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                              long long j1, long long *err, cudaStream_t s, long long *spec,
-                             long long *stamp, void *gscratch = nullptr, size_t gbytes = 0) {
+                             long long *stamp, void *gscratch = nullptr, size_t gbytes = 0,
+                             const int *list = nullptr, int list_grid = 0) {
   static bool attr[64] = {};  // the attribute is per device
   int dev_id = 0;
   cudaGetDevice(&dev_id);
@@ -757,7 +770,8 @@ static long long launch_mini(const Pass2 &P, const double *pts, long long n, int
   const size_t bytes = sizeof(MiniSmem<T, K, N>);
   const size_t stride = (bytes + 255) & ~size_t(255);
   if (gscratch) {  // global-memory slots, one per CTA
-    if (2 * static_cast<size_t>(j1 - j0) * stride > gbytes) return 1;
+    const size_t ctas = list ? 32 * static_cast<size_t>(list_grid) : 2 * static_cast<size_t>(j1 - j0);
+    if (ctas * stride > gbytes) return list ? H3D_E_ARG : 1;  // a list launch was sized to fit
   } else if (!attr[dev_id]) {
     if (h3d_check(cudaFuncSetAttribute(k_mini<T, K, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(bytes))))
@@ -765,18 +779,43 @@ static long long launch_mini(const Pass2 &P, const double *pts, long long n, int
     attr[dev_id] = true;
   }
   h3d_count_launches(1);
-  k_mini<T, K, N><<<lvl_grid(static_cast<unsigned>(j1 - j0), g_interleave != 0), T,
-                    gscratch ? N * sizeof(int) : bytes, s>>>(
+  const dim3 grid = list ? dim3(32u * static_cast<unsigned>(list_grid), 1)
+                         : lvl_grid(static_cast<unsigned>(j1 - j0), g_interleave != 0);
+  k_mini<T, K, N><<<grid, T, gscratch ? N * sizeof(int) : bytes, s>>>(
       P, pts, n, lv, j0, j1, err, g_mini_seglen, spec, stamp, static_cast<unsigned char *>(gscratch),
-      stride);
+      stride, list);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
 
 int g_mini_seglen = 3;  // child events per time segment (H3D_MINI_SEG / h3d_tune)
 
+size_t mini_huge_stride() {
+  return (sizeof(MiniSmem<1024, kMiniHugeEvents, kMiniHugePoints>) + 255) & ~size_t(255);
+}
+
+// list mode (list != nullptr): the jobs of the 32-job chunks in the list
+// (count at list[0]; at most list_grid entries) -- shared-memory variants
 long long mini_level(const Pass2 &P, const double *pts, long long n, int lv, long long j0,
                      long long j1, long long *err, cudaStream_t s, int variant, long long *spec,
-                     long long *stamp, void *gscratch, size_t gbytes) {
+                     long long *stamp, void *gscratch, size_t gbytes, const int *list, int list_grid) {
+  if (list) {
+    if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s, spec, stamp, nullptr, 0, list, list_grid);
+    if (variant == 4)
+      return launch_mini<256, kMiniMedEvents, kMiniMedPoints>(P, pts, n, lv, j0, j1, err, s, spec, stamp, nullptr,
+                                                              0, list, list_grid);
+    if (variant == 5)
+      return launch_mini<512, kMiniL2Events, kMiniL2Points>(P, pts, n, lv, j0, j1, err, s, spec, stamp, nullptr, 0,
+                                                            list, list_grid);
+    if (variant == 1)
+      return launch_mini<1024, 2048, 1024>(P, pts, n, lv, j0, j1, err, s, spec, stamp, nullptr, 0, list, list_grid);
+    if (variant == 6)
+      return launch_mini<1024, kMiniXlEvents, kMiniXlPoints>(P, pts, n, lv, j0, j1, err, s, spec, stamp, nullptr, 0,
+                                                             list, list_grid);
+    if (variant == 3)
+      return launch_mini<1024, kMiniHugeEvents, kMiniHugePoints>(P, pts, n, lv, j0, j1, err, s, spec, stamp,
+                                                                 gscratch, gbytes, list, list_grid);
+    return H3D_E_ARG;
+  }
   if (variant == 2) return launch_mini<128, 320, 192>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
   if (variant == 0) return launch_mini<256, 512, 256>(P, pts, n, lv, j0, j1, err, s, spec, stamp);
   // medium (50 KB: 4 CTAs per SM) and large2 (100 KB: 2 per SM) for levels of

@@ -39,6 +39,9 @@ ROUTES = {
     # small-pool launch, the rest through the overflow list
     "tpj_split_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0, "lane": 0,
                              "tpj_split": 2, "tpj_xyz_kb": 0, "tpj_xyz_ctas": 0},
+    # lane per job + the large CTAs' jobs on a mini variant, wherever the
+    # time-split pipeline would run (big_kin small)
+    "hybrid_everywhere": {"big_kin": 16, "tpj_min_jobs": 1, "mini_tiny_ctas": 0, "mini_ctas": 0, "lane": 0},
     "lane_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
                         "lane_max_level": 40},
     "lane_staged_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
