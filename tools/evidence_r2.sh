@@ -10,6 +10,9 @@ for c in C4 C2 C3; do
     python tools/one_hull.py $c 3 > $out/ncu_list_${c}.log 2>&1
   echo "list $c rc=$?" | tee -a $out/status.txt
 done
+timeout 1500 ncu --metrics $M --clock-control none --csv --log-file $out/launches_C5.csv \
+  python tools/one_hull.py C5 2 > $out/ncu_list_C5.log 2>&1
+echo "list C5 rc=$?" | tee -a $out/status.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/bench_launches_c4.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
   > $out/bench_under_ncu.log 2>&1
