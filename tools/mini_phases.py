@@ -29,9 +29,9 @@ torch.cuda.synchronize()
 L = _lib.load()
 arr = (ctypes.c_longlong * (64 * 16))()
 L.h3d_mini_prof_read(arr)
-names = {1: "points", 2: "mergeS", 3: "scatter", 4: "lists+links", 11: "walk0", 5: "walks", 10: "sweeps",
+names = {1: "points", 2: "mergeS", 3: "scatter", 4: "lists+links", 5: "walks", 10: "sweeps",
          6: "slabs", 7: "classify", 8: "output", 9: "rebuild"}
-order = [1, 2, 3, 4, 11, 5, 10, 6, 7, 8, 9]
+order = [1, 2, 3, 4, 5, 10, 6, 7, 8, 9]
 for lv in range(64):
     v = arr[lv * 16:(lv + 1) * 16]
     if not v[0] or not v[9]:
@@ -40,5 +40,6 @@ for lv in range(64):
     for i in order:
         parts.append(f"{names[i]} {v[i] - prev}")
         prev = v[i]
-    print(f"level {lv}: total {v[9] - v[0]} cycles | " + ", ".join(parts)
-          + f" | walk moves: max {v[12]}, segment 0 {v[13]}, mean {v[14] / max(v[15], 1):.1f} over {v[15]}")
+    walks = (f" | walk moves: max {v[12]}, segment 0 {v[13]}, mean {v[14] / v[15]:.1f} over {v[15]}"
+             if v[15] else "")
+    print(f"level {lv}: total {v[9] - v[0]} cycles | " + ", ".join(parts) + walks)
