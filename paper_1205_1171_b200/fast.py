@@ -132,6 +132,7 @@ STAMP_END = 40
 # the level rows (tag, pass, ms) of the last run_both(stamps=True) of this
 # thread's caller: device time stamps, no event records (csrc/common.cu)
 LAST_LEVEL_ROWS: list = []
+LAST_SORT_MS: list = [None]  # the last stamped hull's presort (device ms)
 
 
 def stamp_rows(stamps, routes) -> list:
@@ -277,6 +278,7 @@ def hull(pts: torch.Tensor, stamps: bool = True) -> HullOut:
         LAST_LEVEL_ROWS[:] = out.level_rows
         if st[0] > 0 and st[1] > 0:
             out.sort_ms = (int(st[1]) - int(st[0])) / 1e6
+            LAST_SORT_MS[0] = out.sort_ms
         if st[1] > 0 and st[STAMP_END] > 0:
             out.passes_ms = (int(st[STAMP_END]) - int(st[1])) / 1e6
     return out
