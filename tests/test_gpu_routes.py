@@ -130,6 +130,14 @@ KNOB_CHOICES = {
     "mini_tiny_kin": [0, 160, BIG_OFF],
     "mini_seg": [1, 3, 16],
     "mini_spec": [0, 1],
+    "mini_one_wave": [0, 296, BIG_OFF],
+    "mini_huge_ctas": [0, 296, 4736],
+    "mini_huge_kin": [0, 1000, BIG_OFF],
+    "tpj_split": [0, 1, 2],
+    "tpj_xyz_ctas": [0, 592],
+    "tpj_cap_level": [0, 6, 40],
+    "lane": [0, 1],
+    "interleave": [0, 1],
 }
 
 
@@ -140,7 +148,7 @@ def test_random_knob_combinations(oracle_mod):
     rng = np.random.default_rng(2024)
     clouds = [generate(20000, "cube", 4), generate(6000, "ball", 5), generate(3000, "sphere", 6)]
     exp = [oracle_mod.convex_hull_3d(p) for p in clouds]
-    for trial in range(16):
+    for trial in range(24):
         kv = {k: int(rng.choice(v)) for k, v in KNOB_CHOICES.items()}
         with fast.tuned(**kv):
             for p, e in zip(clouds, exp):
@@ -149,8 +157,20 @@ def test_random_knob_combinations(oracle_mod):
                 assert np.array_equal(r.vertices, e.vertices), (trial, kv, len(p))
 
 
+REPLAY_KNOBS = {
+    "default": {},
+    # every lane-per-job level split (small pool + overflow list), and the
+    # hybrid route (lane per job + mini list launches) wherever the
+    # pipeline would run: a replayed plan's pools and list grids must take
+    # the next cloud's CTAs or resume measured
+    "split": {"tpj_split": 2, "tpj_xyz_ctas": 0, "tpj_min_jobs": 1, "mini_tiny_ctas": 0, "lane": 0},
+    "hybrid": {"big_kin": 16, "tpj_min_jobs": 1, "mini_tiny_ctas": 0, "mini_ctas": 0, "lane": 0},
+}
+
+
+@pytest.mark.parametrize("knobs", sorted(REPLAY_KNOBS))
 @pytest.mark.parametrize("order", ["cube_then_sphere", "sphere_then_cube", "ball_then_int"])
-def test_plan_replay_across_clouds(order, oracle_mod):
+def test_plan_replay_across_clouds(order, knobs, oracle_mod):
     """A call replays the level plan the previous call with the same n
     recorded (no per-level measurement); a cloud whose jobs do not fit the
     recorded launches makes the replay resume, measured, from that level --
@@ -162,7 +182,7 @@ def test_plan_replay_across_clouds(order, oracle_mod):
         return integer_cloud(n, seed) if kind == "int" else generate(n, kind, seed)
 
     clouds = [make(first, 1), make(first, 2), make(second, 3), make(second, 4), make(first, 5)]
-    with fast.tuned(plan=1):
+    with fast.tuned(plan=1, **REPLAY_KNOBS[knobs]):
         for pts in clouds:
             before = fast.FALLBACKS[0]
             r = H.convex_hull_3d(pts)
