@@ -10,9 +10,12 @@
 // input stops every later launch at once.  After the single read-back an
 // input with ties is redone through the exact tie path (h3d_presort, api.py
 // :90-110), an error is returned, and a fast-path decline is reported in
-// info[0] for the caller's exact engine.  Host synchronisations per hull:
+// info[0] for the caller's exact engine; the next call of the same size
+// then starts on the exact tie path.  Host synchronisations per hull:
 // one for a replayed level plan (fast.cu), one per measured level otherwise,
 // plus this final one -- counted by h3d_sync_count().
+#include <unordered_map>
+
 #include "../../include/hull3d_b200.h"
 #include "fast.cuh"
 #include "h3d_host.h"
@@ -73,20 +76,32 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
     h3d_stamp_now(s, 0);  // slot 0: the presort's start
   }
   int64_t fin = 0;
-  int64_t rc = presort_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr, s);
-  if (rc == 0)
-    rc = passes_and_epilogue(sorted_pts, n, order, presort_ws, presort_ws_bytes, ws_lower, ws_upper,
-                             pass_ws_bytes, faces_raw, cap, faces, vertices, vertex_mark, state_dev, verify,
-                             &fin, s);
+  // a call whose previous same-size call had x ties (integer clouds) goes
+  // straight to the exact tie path: the optimistic attempt would only be
+  // redone
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const long long key = (static_cast<long long>(dev) << 40) ^ n;
+  thread_local std::unordered_map<long long, bool> ties_last;
+  const bool direct = ties_last.count(key) && ties_last[key];
+  int64_t rc = 0;
+  if (!direct) {
+    rc = presort_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr, s);
+    if (rc == 0)
+      rc = passes_and_epilogue(sorted_pts, n, order, presort_ws, presort_ws_bytes, ws_lower, ws_upper,
+                               pass_ws_bytes, faces_raw, cap, faces, vertices, vertex_mark, state_dev, verify,
+                               &fin, s);
+  }
   // the one read-back (+ the level stamps)
   const int words = stamps ? H3D_HULL_STATE : kStStamps;
-  if (rc == 0 && (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev,
-                                            words * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) ||
-                  h3d_check(h3d_sync(s))))
+  if (rc == 0 && !direct &&
+      (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev, words * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s)) ||
+       h3d_check(h3d_sync(s))))
     rc = H3D_E_CUDA;
   const int64_t *hs = info + H3D_HULL_INFO - H3D_HULL_STATE;
   int32_t perturbed = 0;
-  if (rc == 0 && hs[kStErr] == H3D_E_REDO) {
+  if (rc == 0 && (direct || hs[kStErr] == H3D_E_REDO)) {
     // x ties or a long run of equal keys: the exact presort (tie path,
     // perturbation, its own checks), then the rest again
     rc = h3d_presort(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, &perturbed, stream);
@@ -100,6 +115,7 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
                     h3d_check(h3d_sync(s))))
       rc = H3D_E_CUDA;
   }
+  if (rc == 0) ties_last[key] = perturbed != 0;
   if (stamps) h3d_profile_stamps(nullptr);
   if (rc < 0) return rc;
   const long long err = hs[kStErr];
