@@ -325,7 +325,7 @@ def measured_inst(cfg: str, name: str):
 def measured_traffic(cfg: str, name: str):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
     of the kernel, from the committed ncu launch list of this config
-    (profiles/r<round>_ncu_launches_<cfg>.json, the latest round's, made by tools/profile_round.sh +
+    (profiles/r<round>_ncu_launches_<cfg>.json, the latest round's, made by tools/evidence_r2.sh +
     tools/ncu_summary.py).  A big-level "launch" is the pipeline's kernels of
     one level; it is counted per level."""
     import glob
