@@ -1,9 +1,18 @@
 // fast.cu -- the fused fast path: all merge levels of a pass over compact groups.
 //
 // Level scheduler (parallel.py:68-112 on the device); a device error word is
-// read once per hull:
+// read once per hull.  Each level is routed from one small measurement (or
+// replayed from the previous same-size call's plan) to one of:
 //
-//  * k_fast_init1  level 1 (pairs of one-point groups) written directly.
+//  * k_fast_init1  level 1 (pairs of one-point groups) written directly;
+//    k_fast_leaf   levels 1..3 fused, one lane per 8-point block.
+//  * k_lane (lane.cu, levels <= 5) / k_fast_tpj: one LANE per merge job;
+//    a level whose few largest CTAs need far more shared memory than the
+//    rest is split (a small pool + an overflow list for a full-pool launch,
+//    k_fast_tpj_ovf), and a level of a few large jobs among many small ones
+//    runs hybrid (the overflow CTAs' jobs one CTA each on a mini variant).
+//  * k_mini (mini.cu): one CTA per job, the time axis split into segments.
+//  * big.cu: the time-split pipeline over global memory for huge jobs.
 //  * k_fast_tpj    one launch per level while jobs are plentiful: one LANE per
 //                  merge job (merge_tpj2, the reference's sequential sweep with
 //                  stored child event times and the bridge neighbourhood in
