@@ -23,6 +23,8 @@
 namespace h3d {
 int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *workspace,
                       size_t workspace_bytes, long long *err, cudaStream_t s);
+int64_t presort_ties_async(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *workspace,
+                           size_t workspace_bytes, long long *err, long long *perturbed, cudaStream_t s);
 int64_t orient_async(const double *sorted_pts, int64_t n, const int64_t *order, const int32_t *faces_raw,
                      const long long *counts, int64_t cap, int64_t *faces, int32_t *vertex_mark,
                      int64_t *vertices, long long *vcount, void *workspace, size_t workspace_bytes,
@@ -35,7 +37,7 @@ namespace {
 
 // device state words (int64): err, k_lo, k_up, verify diagnostics, vertex
 // count, 3 spare, then the level stamps
-constexpr int kStErr = 0, kStCounts = 1, kStVcount = 4, kStStamps = 8;
+constexpr int kStErr = 0, kStCounts = 1, kStVcount = 4, kStPerturbed = 5, kStStamps = 8;
 
 int64_t passes_and_epilogue(const double *sorted_pts, int64_t n, const int64_t *order, void *presort_ws,
                             size_t presort_ws_bytes, void *ws_lower, void *ws_upper, size_t pass_ws_bytes,
@@ -76,32 +78,30 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
     h3d_stamp_now(s, 0);  // slot 0: the presort's start
   }
   int64_t fin = 0;
-  // a call whose previous same-size call had x ties (integer clouds) goes
-  // straight to the exact tie path: the optimistic attempt would only be
-  // redone
+  // a call whose previous same-size call had x ties (integer clouds) starts
+  // on the tie path (presort_ties_async, also free of host synchronisation):
+  // the optimistic attempt would only be redone
   int dev = 0;
   cudaGetDevice(&dev);
   const long long key = (static_cast<long long>(dev) << 40) ^ n;
   thread_local std::unordered_map<long long, bool> ties_last;
   const bool direct = ties_last.count(key) && ties_last[key];
-  int64_t rc = 0;
-  if (!direct) {
-    rc = presort_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr, s);
-    if (rc == 0)
-      rc = passes_and_epilogue(sorted_pts, n, order, presort_ws, presort_ws_bytes, ws_lower, ws_upper,
-                               pass_ws_bytes, faces_raw, cap, faces, vertices, vertex_mark, state_dev, verify,
-                               &fin, s);
-  }
+  int64_t rc = direct ? presort_ties_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr,
+                                          st + kStPerturbed, s)
+                       : presort_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr, s);
+  if (rc == 0)
+    rc = passes_and_epilogue(sorted_pts, n, order, presort_ws, presort_ws_bytes, ws_lower, ws_upper,
+                             pass_ws_bytes, faces_raw, cap, faces, vertices, vertex_mark, state_dev, verify,
+                             &fin, s);
   // the one read-back (+ the level stamps)
   const int words = stamps ? H3D_HULL_STATE : kStStamps;
-  if (rc == 0 && !direct &&
-      (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev, words * sizeof(int64_t),
-                                 cudaMemcpyDeviceToHost, s)) ||
-       h3d_check(h3d_sync(s))))
+  if (rc == 0 && (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev,
+                                            words * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) ||
+                  h3d_check(h3d_sync(s))))
     rc = H3D_E_CUDA;
   const int64_t *hs = info + H3D_HULL_INFO - H3D_HULL_STATE;
-  int32_t perturbed = 0;
-  if (rc == 0 && (direct || hs[kStErr] == H3D_E_REDO)) {
+  int32_t perturbed = direct && rc == 0 ? static_cast<int32_t>(hs[kStPerturbed]) : 0;
+  if (rc == 0 && hs[kStErr] == H3D_E_REDO) {
     // x ties or a long run of equal keys: the exact presort (tie path,
     // perturbation, its own checks), then the rest again
     rc = h3d_presort(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, &perturbed, stream);
@@ -120,7 +120,8 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
   if (rc < 0) return rc;
   const long long err = hs[kStErr];
   // the gate's verdicts are the presort's errors (api.py:106-108, :131-147)
-  if (err == H3D_E_NONFINITE || err == H3D_E_COINCIDENT || err == H3D_E_COLLINEAR || err == H3D_E_COPLANAR)
+  if (err == H3D_E_NONFINITE || err == H3D_E_TIES || err == H3D_E_COINCIDENT || err == H3D_E_COLLINEAR ||
+      err == H3D_E_COPLANAR)
     return err;
   info[0] = err;  // 0, or the fast path's decline: the caller's exact engine takes over
   info[1] = hs[kStCounts];

@@ -441,6 +441,7 @@ __global__ void k_lexruns(const double *__restrict__ pts, int *perm, long long n
        i += (long long)gridDim.x * blockDim.x) {
     const double x = pts[3ll * perm[i]];
     if (pts[3ll * perm[i + 1]] != x || (i > 0 && pts[3ll * perm[i - 1]] == x)) continue;  // i: run head
+    flag[1] = 1;  // an x tie
     long long e = i + 1;
     while (e < n && pts[3ll * perm[e]] == x && e - i <= RUN_MAX) ++e;
     if (e - i > RUN_MAX) {
@@ -756,7 +757,7 @@ bool carve(h3d_arena &ar, long long n, PresortWS &w) {
   w.head = ar.take<long long>(n);
   w.prim_bytes = prim_bytes_for(n);
   w.prim_tmp = ar.take<char>(w.prim_bytes);
-  w.flag = ar.take<int>(4);
+  w.flag = ar.take<int>(16);
   w.scan = ar.take<ScanState>(1);
   w.partial = ar.take<double>(3 * kColsumBlocks);
   w.centroid = ar.take<double>(4);
@@ -904,6 +905,80 @@ int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t 
   k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, n, w.scan, 16384);
   for (int stage = 0; stage < 3; ++stage) k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
   k_presort_gate<<<1, 1, 0, s>>>(w.flag, w.scan, err);
+  return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
+}
+
+// The exact tie path with no host synchronisation, for a size whose
+// previous call had x ties (h3d_hull): the common tie case -- short runs of
+// equal x, a perturbation that keeps x non-decreasing (the reference's
+// re-sort is then the identity) -- runs through on the device; its gate
+// hands anything else (long runs, a re-sort) back to h3d_presort (E_REDO),
+// and raises the presort's errors in the reference's order.  flag words:
+// [1] non-finite, [2] long run of equal 32-bit keys, [8] long run of equal
+// x, [9] an x tie, [12] a tie that survived the perturbation, [15] x
+// descended after it.
+__global__ void k_ties_gate(const int *flag, const ScanState *st, long long *err, long long *perturbed) {
+  const long long none = 0x7fffffffffffffffll;
+  const int tie = flag[9];
+  long long e = 0;
+  if (flag[1]) e = H3D_E_NONFINITE;
+  else if (flag[2] || flag[8] || flag[15]) e = H3D_E_REDO;
+  else if (tie && flag[12]) e = H3D_E_TIES;
+  else if (st->i == none) e = H3D_E_COINCIDENT;
+  else if (st->j == none) e = H3D_E_COLLINEAR;
+  else if (st->k == none) e = H3D_E_COPLANAR;
+  *perturbed = tie;
+  if (e) raise_err(err, e);
+}
+
+int64_t presort_ties_async(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *workspace,
+                           size_t workspace_bytes, long long *err, long long *perturbed, cudaStream_t s) {
+  if (n < 1 || n > (1ll << 30)) return H3D_E_ARG;
+  h3d_arena ar(workspace, workspace_bytes);
+  PresortWS w;
+  if (!carve(ar, n, w)) return H3D_E_ARG;
+  const unsigned G = h3d_grid(n, 256) > 4096 ? 4096 : h3d_grid(n, 256);
+  long long *ord = reinterpret_cast<long long *>(order);
+  cudaMemsetAsync(w.flag, 0, sizeof(int) * 16, s);
+  h3d_count_launches(1);
+  k_scan_init<<<1, 1, 0, s>>>(w.scan);
+  const unsigned long long mm_init[2] = {~0ull, 0ull};
+  cudaMemcpyAsync(w.mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, s);
+  h3d_count_launches(2);
+  k_scan_input<<<G > 1184 ? 1184 : G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
+  unsigned *k32a = reinterpret_cast<unsigned *>(w.k0), *k32b = reinterpret_cast<unsigned *>(w.k1);
+  k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, nullptr);
+  bool alt = false;
+  h3d_count_launches(5);
+  if (h3d_check(prim::rs_sort_pairs<unsigned>(w.prim_tmp, w.prim_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32, &alt,
+                                              s, true)))
+    return H3D_E_CUDA;
+  int *vs = alt ? w.v1 : w.v0;
+  h3d_count_launches(1);
+  k_tiefix<<<G, 256, 0, s>>>(pts, alt ? k32b : k32a, vs, n, w.flag + 2);
+  // lexsort (x, y, z): the runs of equal x re-ordered by (y, z, index)
+  cudaMemcpyAsync(w.v2, vs, sizeof(int) * n, cudaMemcpyDeviceToDevice, s);
+  h3d_count_launches(4);
+  k_lexruns<<<G, 256, 0, s>>>(pts, w.v2, n, w.flag + 8);
+  k_gather_rows<<<G, 256, 0, s>>>(pts, w.v2, n, w.work, nullptr, nullptr);
+  // perturb_ties (api.py:99-101): run heads by max-scan, then base + rank * step
+  k_run_heads<<<G, 256, 0, s>>>(w.work, n, w.head);
+  if (h3d_check(prim::scan<false, long long>(w.prim_tmp, w.prim_bytes, w.head, w.head, n, prim::OpMax(), -1ll,
+                                             -1ll, s)))
+    return H3D_E_CUDA;
+  h3d_count_launches(5);
+  k_perturb<<<G, 256, 0, s>>>(w.work, w.head, n);
+  k_perturbed_order<<<G, 256, 0, s>>>(w.work, n, w.flag + 12);
+  cudaMemcpyAsync(sorted_pts, w.work, 3 * sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+  k_perm_to_order<<<G, 256, 0, s>>>(w.v2, n, ord);
+  // the scale on the (perturbed) sorted rows, then the degeneracy scan
+  k_scan_init<<<1, 1, 0, s>>>(w.scan);
+  k_absmax<<<G, 256, 0, s>>>(sorted_pts, 3 * n, &w.scan->scale_bits);
+  h3d_count_launches(5);
+  k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, n, w.scan, 16384);
+  for (int stage = 0; stage < 3; ++stage)
+    k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
+  k_ties_gate<<<1, 1, 0, s>>>(w.flag, w.scan, err, perturbed);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
 

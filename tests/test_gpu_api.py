@@ -204,3 +204,43 @@ def test_tie_path_variants(case, oracle_mod):
     assert r.stats.perturbed and exp.perturbed
     assert np.array_equal(r.faces, exp.faces)
     assert np.array_equal(r.vertices, exp.vertices)
+
+
+def test_tie_path_repeated_size(oracle_mod):
+    """Same-size calls after a call with x ties start on the device tie path
+    (hull.cu: presort_ties_async, no host synchronisation); its gate hands
+    long runs and a descending perturbed x back to the exact presort and
+    raises the degeneracy errors -- every call still equals the oracle,
+    including a tie-free cloud on that path (perturbed stays False)."""
+    rng = np.random.default_rng(5)
+
+    def cloud(kind):
+        pts = rng.uniform(-1, 1, (3000, 3))
+        if kind == "short_runs":
+            pts[:600, 0] = np.repeat(rng.uniform(-1, 1, 200), 3)
+        elif kind == "long_run":
+            pts[:100, 0] = 0.25
+        elif kind == "perturbed_descends":
+            pts[:5, 0] = 1.0
+            pts[5, 0] = np.nextafter(np.nextafter(1.0, 2.0), 2.0)
+        elif kind == "coplanar_ties":
+            pts[:, 2] = 0.0
+            pts[:4, 0] = 0.5
+        rng.shuffle(pts)
+        return pts
+
+    seq = ["short_runs", "short_runs", "none", "short_runs", "long_run", "perturbed_descends",
+           "coplanar_ties", "short_runs", "short_runs"]
+    for kind in seq:
+        pts = cloud(kind)
+        try:
+            exp = oracle_mod.convex_hull_3d(pts)
+        except ValueError as e:  # the oracle's DegenerateInputError: the package's own class
+            assert type(e).__name__ == "DegenerateInputError", kind
+            with pytest.raises(H.DegenerateInputError):
+                H.convex_hull_3d(pts)
+            continue
+        r = H.convex_hull_3d(pts)
+        assert r.stats.perturbed == exp.perturbed, kind
+        assert np.array_equal(r.faces, exp.faces), kind
+        assert np.array_equal(r.vertices, exp.vertices), kind
