@@ -202,14 +202,19 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n,
                             size_t workspace_bytes, void *stream);
 
 /* Routing knobs of the fast path (not a reference interface; used by the
- * tests to drive every kernel route and by tuning sweeps): "big_kin"
- * (time-split pipeline from this merged child log size), "big_total" (or
- * half that log size with this many child events in the level), "leaf_b" (levels
- * 1..B fused: 3 or 4; 0-2 = off), "tpj_min_jobs", "tpj_xyz_kb", "tpj_max_level", "mini"
- * (0/1: the one-CTA-per-job shared-memory merges), "mini_ctas" (their CTA
- * cap), "mini_tiny_ctas" / "mini_tiny_kin" (the 6-CTA-per-SM variant: CTA
- * cap, and the merged child log size from which it replaces the lane-per-job
- * kernel).  value < 0 only queries.  Returns the previous value, or -1 for an unknown name.
+ * tests to drive every kernel route and by tuning sweeps; DESIGN.md §3.2b
+ * lists them with their defaults): "big_kin" (time-split pipeline from this
+ * merged child log size), "big_total" (or half that log size with this many
+ * child events in the level), "big_max_jobs", "leaf_b" (levels 1..B fused: 3
+ * or 4; 0-2 = off), "lane" / "lane_max_level" / "lane_xyz_kb" / "lane_stage"
+ * (the lane.cu kernel), "tpj_min_jobs", "tpj_xyz_kb", "tpj_xyz_ctas",
+ * "tpj_max_level", "tpj_cap_level" (the 128-register build up to this
+ * level), "tpj_split" (split / hybrid lane-per-job levels; 2 = split every
+ * level, tests), "mini" (0/1: the one-CTA-per-job merges), "mini_ctas",
+ * "mini_one_wave", "mini_tiny_ctas" / "mini_tiny_kin", "mini_huge_ctas" /
+ * "mini_huge_kin", "mini_seg", "mini_spec", "plan" (record & replay level
+ * plans), "interleave" (the two passes' CTAs adjacent).  value < 0 only
+ * queries.  Returns the previous value, or -1 for an unknown name.
  * Environment variables H3D_BIG_KIN, H3D_LEAF_B, ... set the defaults. */
 int64_t h3d_tune(const char *name, int64_t value);
 
