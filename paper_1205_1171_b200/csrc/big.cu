@@ -928,9 +928,13 @@ static unsigned grid_of(long long work) {
   return static_cast<unsigned>(g);
 }
 
+// kin_total / pts_total: the level's merged child events and points (both
+// passes) from the caller's measurement -- then the level reads nothing back:
+// the segment kernels size their grids from an upper bound of the segment
+// count and take the exact count from the device scan
 long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double *pts,
                     long long n, int lv, long long j0, long long j1, long long *err,
-                    cudaStream_t s) {
+                    cudaStream_t s, long long kin_total, long long pts_total) {
   h3d_arena ar(big_ws, big_bytes);
   BigWS W;
   if (!big_ws || !carve_big(ar, big_capacity(n), W)) return 1;
@@ -945,12 +949,14 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   k_big_jobs<<<grid_of(J2), 256, 0, s>>>(P, n, lv, j0, J, W, err);
   if (scan(W.jkin, W.jkinoff, J2 + 1) || scan(W.jns, W.jnsoff, J2 + 1)) return H3D_E_CUDA;
   // totals: the level must fit the scratch
-  int tot[3];
-  if (h3d_check(cudaMemcpyAsync(&tot[0], W.jkinoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(cudaMemcpyAsync(&tot[1], W.jnsoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(h3d_sync(s)))
+  int tot[3] = {0, 0, 0};
+  const bool known = kin_total >= 0 && pts_total >= 0;
+  if (!known &&
+      (h3d_check(cudaMemcpyAsync(&tot[0], W.jkinoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+       h3d_check(cudaMemcpyAsync(&tot[1], W.jnsoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+       h3d_check(h3d_sync(s))))
     return H3D_E_CUDA;
-  const long long kin = tot[0], pts_n = tot[1];
+  const long long kin = known ? kin_total : tot[0], pts_n = known ? pts_total : tot[1];
   // segment length: enough segments to give every SM a few warps
   static long long segs_per_sm = -1;
   if (segs_per_sm < 0) {
@@ -962,10 +968,16 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
   h3d_count_launches(1);
   k_big_segs<<<grid_of(J2 + 1), 256, 0, s>>>(J, W, static_cast<int>(SEG));
   if (scan(W.jseg, W.jsegoff, J2 + 1)) return H3D_E_CUDA;
-  if (h3d_check(cudaMemcpyAsync(&tot[2], W.jsegoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
-      h3d_check(h3d_sync(s)))
-    return H3D_E_CUDA;
-  const long long nseg = tot[2];
+  // segments: sum over jobs of ceil(kin_j / SEG) (at least one per merge)
+  // <= kin / SEG + J2; with the totals known that bound sizes the grids
+  // (every segment kernel reads the exact count, jsegoff[J2], on the device)
+  long long nseg = kin / SEG + J2;
+  if (!known) {
+    if (h3d_check(cudaMemcpyAsync(&tot[2], W.jsegoff + J2, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+        h3d_check(h3d_sync(s)))
+      return H3D_E_CUDA;
+    nseg = tot[2];
+  }
   if (kin > 4 * W.m || pts_n > 2 * W.m || nseg > 4 * W.m / SEG_MIN + W.m) {
     // carries were already copied; the caller reruns the level elsewhere
     return 1;

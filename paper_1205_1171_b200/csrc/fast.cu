@@ -493,7 +493,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
   unsigned long long lb[24];
 #pragma unroll
   for (int q = 0; q < 24; ++q) lb[q] = 0;
-  unsigned long long ksum = 0;
+  unsigned long long ksum = 0, nssum = 0;  // out[9] merged child events, out[11] points of the merges
   // out[kNeedHist + b]: CTAs (32 jobs) whose point sum falls in bin b
   // (b = floor(6 log2 sum): six bins per octave) -- the host sizes a split
   // level's small pool from it
@@ -537,6 +537,7 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
     mx[7] = wb > mx[7] ? wb : mx[7];
     mx[8] = kin > mx[8] ? kin : mx[8];
     ksum += kin;
+    nssum += nS;
     unsigned long long t = nS;
     mx[5] = t > mx[5] ? t : mx[5];  // 1 job per CTA
 #pragma unroll
@@ -550,6 +551,8 @@ __global__ void k_tpj_need(Pass2 P, long long n, int level, long long j0, long l
   __shared__ unsigned long long red[32][34];
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int o = 16; o; o >>= 1) ksum += __shfl_xor_sync(FULL, ksum, o);
+  for (int o = 16; o; o >>= 1) nssum += __shfl_xor_sync(FULL, nssum, o);
+  if (lane == 0 && nssum) atomicAdd(out + 11, nssum);
 #pragma unroll
   for (int r = 0; r < 9; ++r) {
     unsigned long long m = mx[r];
@@ -2240,7 +2243,8 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
     // for levels of fewer jobs)
     if (big_ws && (maxkin >= kBigKin ||
                    (2 * maxkin >= kBigKin && sumkin >= kBigTotal && 2 * jobs < kBigMaxJobs))) {
-      const long long rb = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s);
+      const long long rb = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s, sumkin,
+                                     static_cast<long long>(need[11]));
       if (rb < 0) return rb;
       if (rb == 0) {
         rec.push_back(LevelRec{lv, REC_BIG, 0, 0, 0, 0, LaneCfg{}});
