@@ -1013,6 +1013,10 @@ long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double
     long long cap = (8 * W.m + 128) / (nseg > 0 ? nseg : 1);
     if (cap > 1024) cap = 1024;
     if (cap < 1) cap = 1;
+    // the segment count is an upper bound when the totals came from the
+    // measurement: counts past the real segments must read as zero in the
+    // scan of the slab sizes
+    if (known) cudaMemsetAsync(W.bcnt, 0, sizeof(int) * (nseg + 1), s);
     h3d_count_launches(3);
     const unsigned gsw = static_cast<unsigned>((nseg + 127) / 128 > 0 ? (nseg + 127) / 128 : 1);
     k_big_sweep<0><<<gsw, 128, 0, s>>>(P, pts, n, lv, j0, J, W, static_cast<int>(SEG), static_cast<int>(cap), err);
