@@ -22,13 +22,13 @@
 
 namespace h3d {
 int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *workspace,
-                      size_t workspace_bytes, long long *err, cudaStream_t s);
+                      size_t workspace_bytes, long long *err, cudaStream_t s, int *sums_ready);
 int64_t presort_ties_async(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *workspace,
                            size_t workspace_bytes, long long *err, long long *perturbed, cudaStream_t s);
 int64_t orient_async(const double *sorted_pts, int64_t n, const int64_t *order, const int32_t *faces_raw,
                      const long long *counts, int64_t cap, int64_t *faces, int32_t *vertex_mark,
                      int64_t *vertices, long long *vcount, void *workspace, size_t workspace_bytes,
-                     cudaStream_t s);
+                     cudaStream_t s, int sums_ready);
 }  // namespace h3d
 
 using namespace h3d;
@@ -43,7 +43,7 @@ int64_t passes_and_epilogue(const double *sorted_pts, int64_t n, const int64_t *
                             size_t presort_ws_bytes, void *ws_lower, void *ws_upper, size_t pass_ws_bytes,
                             int32_t *faces_raw, int64_t cap, int64_t *faces, int64_t *vertices,
                             int32_t *vertex_mark, int64_t *state_dev, int32_t verify, int64_t *fin,
-                            cudaStream_t s) {
+                            cudaStream_t s, int sums_ready) {
   long long *st = reinterpret_cast<long long *>(state_dev);
   int levels = 0;
   while ((1ll << levels) < n) ++levels;
@@ -55,7 +55,7 @@ int64_t passes_and_epilogue(const double *sorted_pts, int64_t n, const int64_t *
                                      state_dev + kStErr, s);
   if (e < 0) return e;
   return orient_async(sorted_pts, n, order, faces_raw, st + kStCounts, cap, faces, vertex_mark, vertices,
-                      st + kStVcount, presort_ws, presort_ws_bytes, s);
+                      st + kStVcount, presort_ws, presort_ws_bytes, s, sums_ready);
 }
 
 }  // namespace
@@ -86,13 +86,15 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
   const long long key = (static_cast<long long>(dev) << 40) ^ n;
   thread_local std::unordered_map<long long, bool> ties_last;
   const bool direct = ties_last.count(key) && ties_last[key];
+  int sums_ready = 0;  // the optimistic gather made the epilogue's centroid sums
   int64_t rc = direct ? presort_ties_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr,
                                           st + kStPerturbed, s)
-                       : presort_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr, s);
+                       : presort_async(pts, n, sorted_pts, order, presort_ws, presort_ws_bytes, st + kStErr, s,
+                                       &sums_ready);
   if (rc == 0)
     rc = passes_and_epilogue(sorted_pts, n, order, presort_ws, presort_ws_bytes, ws_lower, ws_upper,
                              pass_ws_bytes, faces_raw, cap, faces, vertices, vertex_mark, state_dev, verify,
-                             &fin, s);
+                             &fin, s, sums_ready);
   // the one read-back (+ the level stamps)
   const int words = stamps ? H3D_HULL_STATE : kStStamps;
   if (rc == 0 && (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev,
@@ -109,7 +111,7 @@ int64_t h3d_hull(const double *pts, int64_t n, double *sorted_pts, int64_t *orde
     if (rc == 0)
       rc = passes_and_epilogue(sorted_pts, n, order, presort_ws, presort_ws_bytes, ws_lower, ws_upper,
                                pass_ws_bytes, faces_raw, cap, faces, vertices, vertex_mark, state_dev, verify,
-                               &fin, s);
+                               &fin, s, 0);
     if (rc == 0 && (h3d_check(cudaMemcpyAsync(info + H3D_HULL_INFO - H3D_HULL_STATE, state_dev,
                                               words * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) ||
                     h3d_check(h3d_sync(s))))

@@ -236,6 +236,56 @@ __global__ void k_gather_rows(const double *__restrict__ pts, const int *__restr
   }
 }
 
+// The optimistic presort's gather with the epilogue's centroid column sums
+// folded in: the grid and the per-thread row order of k_colsum (kColsumBlocks
+// x 256 threads, grid-stride over the sorted rows) and the same block
+// reduction, so the partial sums -- and the centroid -- are bit for bit
+// k_colsum's; four rows in flight per thread, added in row order.
+__global__ void __launch_bounds__(256) k_gather_rows_colsum(const double *__restrict__ pts,
+                                                           const int *__restrict__ perm, long long n,
+                                                           double *out, long long *order, int *tie,
+                                                           double *partial) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double s0 = 0, s1 = 0, s2 = 0;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i < n; i += 4 * stride) {
+    long long r[4];
+    double x[4], y[4], z[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r[q] = i + q * stride < n ? perm[i + q * stride] : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i + q * stride < n) {
+        x[q] = pts[3 * r[q]];
+        y[q] = pts[3 * r[q] + 1];
+        z[q] = pts[3 * r[q] + 2];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long k = i + q * stride;
+      if (k >= n) break;
+      // adjacent equal x in the sorted order (the reference's tie test)
+      if (k > 0 && x[q] == pts[3ll * perm[k - 1]]) *tie = 1;
+      out[3 * k] = x[q];
+      out[3 * k + 1] = y[q];
+      out[3 * k + 2] = z[q];
+      order[k] = r[q];
+      s0 += x[q];
+      s1 += y[q];
+      s2 += z[q];
+    }
+  }
+  __shared__ double s_warp[8];
+  const prim::OpSum add;
+  double t = prim::block_reduce256(s0, s_warp, add);
+  if (threadIdx.x == 0) partial[3 * blockIdx.x] = t;
+  t = prim::block_reduce256(s1, s_warp, add);
+  if (threadIdx.x == 0) partial[3 * blockIdx.x + 1] = t;
+  t = prim::block_reduce256(s2, s_warp, add);
+  if (threadIdx.x == 0) partial[3 * blockIdx.x + 2] = t;
+}
+
 // ---- sharded presort (multi-GPU): one rank's window [q0, p1) of the global
 // stable x order without sorting the other ranks' points.  The 32-bit keys of
 // every point are computed; a 3-pass radix select (11+11+10 bits) finds the
@@ -876,7 +926,7 @@ __global__ void k_presort_gate(const int *flag, const ScanState *st, long long *
 // (head, then each full stage only if the head left it undecided: the
 // stage kernels return at once otherwise), gate.  Returns 0 or a code.
 int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t *order, void *workspace,
-                      size_t workspace_bytes, long long *err, cudaStream_t s) {
+                      size_t workspace_bytes, long long *err, cudaStream_t s, int *sums_ready) {
   if (n < 1 || n > (1ll << 30)) return H3D_E_ARG;
   h3d_arena ar(workspace, workspace_bytes);
   PresortWS w;
@@ -900,7 +950,18 @@ int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t 
   int *vs = alt ? w.v1 : w.v0;
   h3d_count_launches(2);
   k_tiefix<<<G, 256, 0, s>>>(pts, alt ? k32b : k32a, vs, n, w.flag + 2);
-  k_gather_rows<<<G, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, nullptr, w.flag);
+  // the epilogue's centroid partial sums land where orient_async carves
+  // them: the front of this workspace, inside the keys (dead after the tie
+  // fix) when they hold them -- else the epilogue sums the rows itself
+  h3d_arena ea(workspace, workspace_bytes);
+  EpiWS ew;
+  carve_epi(ea, n, ew);
+  const bool fuse = reinterpret_cast<char *>(ew.count) <= reinterpret_cast<char *>(w.k1);
+  if (fuse)
+    k_gather_rows_colsum<<<kColsumBlocks, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, w.flag, ew.partial);
+  else
+    k_gather_rows<<<G, 256, 0, s>>>(pts, vs, n, sorted_pts, ord, nullptr, w.flag);
+  *sums_ready = fuse ? 1 : 0;
   h3d_count_launches(5);
   k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, n, w.scan, 16384);
   for (int stage = 0; stage < 3; ++stage) k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
@@ -988,12 +1049,13 @@ int64_t presort_ties_async(const double *pts, int64_t n, double *sorted_pts, int
 int64_t orient_async(const double *sorted_pts, int64_t n, const int64_t *order, const int32_t *faces_raw,
                      const long long *counts, int64_t cap, int64_t *faces, int32_t *vertex_mark,
                      int64_t *vertices, long long *vcount, void *workspace, size_t workspace_bytes,
-                     cudaStream_t s) {
+                     cudaStream_t s, int sums_ready) {
   h3d_arena ar(workspace, workspace_bytes);
   EpiWS w;
   if (!carve_epi(ar, n, w)) return H3D_E_ARG;
-  h3d_count_launches(3);
-  k_colsum<<<kColsumBlocks, 256, 0, s>>>(sorted_pts, n, w.partial);
+  h3d_count_launches(sums_ready ? 2 : 3);
+  // sums_ready: the optimistic presort's gather made the partial sums
+  if (!sums_ready) k_colsum<<<kColsumBlocks, 256, 0, s>>>(sorted_pts, n, w.partial);
   k_centroid<<<1, 32, 0, s>>>(w.partial, kColsumBlocks, n, w.centroid);
   cudaMemsetAsync(vertex_mark, 0, sizeof(int) * n, s);
   const unsigned G = h3d_grid(cap, 256) > 1184 ? 1184 : h3d_grid(cap, 256);
