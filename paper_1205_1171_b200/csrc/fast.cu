@@ -1734,6 +1734,7 @@ void load_env_once() {
   if (const char *e = getenv("H3D_LANE_MAX_LEVEL")) g_lane_max_level = atoi(e);
   if (const char *e = getenv("H3D_LANE_XYZ_KB")) g_lane_xyz_max = atoll(e) * 1024;
   if (const char *e = getenv("H3D_LANE_STAGE")) g_lane_stage = atoi(e);
+  if (const char *e = getenv("H3D_LANE_OWN")) g_lane_own = atoi(e);
   if (const char *e = getenv("H3D_TPJ_PREFETCH")) kTpjPrefetchJobs = atoll(e);
   if (const char *e = getenv("H3D_PLAN")) g_plan = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_INTERLEAVE")) g_interleave = atoi(e) ? 1 : 0;
@@ -1880,6 +1881,7 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "lane_max_level") { old = g_lane_max_level; if (value >= 0) g_lane_max_level = static_cast<int>(value); }
   else if (k == "lane_xyz_kb") { old = g_lane_xyz_max / 1024; if (value >= 0) g_lane_xyz_max = value * 1024; }
   else if (k == "lane_stage") { old = g_lane_stage; if (value >= 0) g_lane_stage = value ? 1 : 0; }
+  else if (k == "lane_own") { old = g_lane_own; if (value >= 0) g_lane_own = static_cast<int>(value); }
   else if (k == "tpj_max_level") { old = kTpjMaxLevel; if (value >= 0) kTpjMaxLevel = static_cast<int>(value); }
   return old;
 }

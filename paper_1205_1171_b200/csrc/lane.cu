@@ -334,8 +334,10 @@ __global__ void __launch_bounds__(32) k_lane(
 #endif
 Pass2 P, const double *__restrict__ pts, long long n,
                                              int level, long long j0, long long j1,
-                                             long long *err, int pool, int jpc, int stage,
+                                             long long *err, int pool, int jpc, int stage_own,
                                              long long *spec, long long *stamp) {
+  // stage_own: bit 0 stage the merged events, bit 1 each lane stages its own job's rows
+  const int stage = stage_own & 1, own = (stage_own >> 1) & 1;
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // level start (ns)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -423,10 +425,41 @@ Pass2 P, const double *__restrict__ pts, long long n,
   __syncwarp();
   const int tot_pts = s_pre[32];
   // ---- stage links, gids (+ coordinates): flattened over the 32 jobs'
-  // points, coalesced, U elements per lane in flight
+  // points, coalesced, U elements per lane in flight -- or (own, small jobs
+  // without coordinates) every lane its own job's rows, no job-index walk
   constexpr int U = 4;
   int js = 0;
-  for (int x0 = 0; x0 < tot_pts; x0 += 32 * U) {
+  if (own && !XYZ) {
+    if (merge) {
+      const LSlice<XYZ> T(smem + off, nS);
+      for (int p0 = 0; p0 < nS; p0 += U) {
+        int2 l[U];
+        int g[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int p = p0 + q;
+          if (p < nS) {
+            const long long src = p < nSL ? L + p : M + (p - nSL);
+            l[q] = in.lnk[src];
+            g[q] = in.gid[src];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int p = p0 + q;
+          if (p >= nS) break;
+          int2 lq = l[q];
+          if (p >= nSL) {
+            if (lq.x != NIL) lq.x += nSL;
+            if (lq.y != NIL) lq.y += nSL;
+          }
+          T.lk[p] = make_short2(static_cast<short>(lq.x), static_cast<short>(lq.y));
+          T.gd[p] = g[q];
+        }
+      }
+    }
+  }
+  for (int x0 = 0; x0 < (own && !XYZ ? 0 : tot_pts); x0 += 32 * U) {
     int jj[U], p[U];
     long long src[U];
     int2 l[U];
@@ -531,8 +564,42 @@ Pass2 P, const double *__restrict__ pts, long long n,
   }
   __syncwarp();
   // ---- write-out (cooperative, coalesced): links + gids at their new ids
+  // (own: every lane its own job, no job-index walk)
   bool bad = false;
-  const int tot_p2 = s_pre[32], tot_ev = s_epre[32];
+  const int tot_p2 = own ? 0 : s_pre[32], tot_ev = own ? 0 : s_epre[32];
+  if (own && merge) {
+    for (int p = 0; p < nS; ++p) {
+      const unsigned id = S.fi[p];
+      if (id == FULL) continue;
+      const short2 l = S.lk[p];
+      int2 o;
+      o.x = l.x == NIL ? NIL : static_cast<int>(S.fi[l.x]);
+      o.y = l.y == NIL ? NIL : static_cast<int>(S.fi[l.y]);
+      bad |= (o.x == -1 && l.x != NIL) | (o.y == -1 && l.y != NIL);
+      out.lnk[L + id] = o;
+      out.gid[L + id] = S.gd[p];
+    }
+    for (int e = 0; e < static_cast<int>(k); ++e) {
+      EvP *dst = out.ev + 2 * L + e;
+      Ev o;
+      if (e < ocap) {
+        const unsigned long long w = S.ow[e];
+        o.t = S.ot[e];
+        o.a = static_cast<int>(w & 0x7fff);
+        o.b = static_cast<int>((w >> 15) & 0x7fff);
+        o.c = static_cast<int>((w >> 30) & 0x7fff);
+        o.kind = static_cast<int>(w >> 45);
+      } else {
+        o = *dst;
+      }
+      const unsigned na = S.fi[o.a], nb = S.fi[o.b], nc = S.fi[o.c];
+      bad |= (na == FULL) | (nb == FULL) | (nc == FULL);
+      o.a = static_cast<int>(na);
+      o.b = static_cast<int>(nb);
+      o.c = static_cast<int>(nc);
+      *dst = EvP(o);
+    }
+  }
   int jw = 0;
   for (int x = lane; x < tot_p2; x += 32) {
     while (s_pre[jw + 1] <= x) ++jw;  // the job index only advances
@@ -590,6 +657,7 @@ bool g_lane_attr[64] = {};
 // it saves, profiles/r2_levels_c4.jsonl)
 long long g_lane_xyz_max = 0;  // H3D_LANE_XYZ_KB: stage coordinates up to this pool
 int g_lane_stage = 0;          // H3D_LANE_STAGE: stage merged events (0 = never)
+int g_lane_own = 4;            // H3D_LANE_OWN: up to this level each lane stages and writes its own job (C4 level 4 -3 %)
 
 // Host side: choose the variant (coordinates / merged events staged in
 // shared memory) and jobs per CTA from the level's measured shared-memory
@@ -616,9 +684,11 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
     const dim3 grid = lvl_grid(h3d_grid(jobs, jpc), g_interleave != 0);
     const int pool = static_cast<int>(cfg->pool);
     if (cfg->v >= 2)
-      k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec, stamp);
+      k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, (cfg->v & 1) | ((lv <= g_lane_own ? 1 : 0) << 1),
+                                          spec, stamp);
     else
-      k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, cfg->v & 1, spec, stamp);
+      k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, pool, jpc, (cfg->v & 1) | ((lv <= g_lane_own ? 1 : 0) << 1),
+                                           spec, stamp);
     return 0;
   }
   auto pick = [&](int v, int *jr) {  // fewest-lanes-idle jobs per CTA that fits
@@ -651,11 +721,11 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
   h3d_count_launches(1);
   const dim3 grid = lvl_grid(h3d_grid(jobs, jpc), g_interleave != 0);
   if (v >= 2)
-    k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1,
-                                       spec, stamp);
+    k_lane<true><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc,
+                                       (v & 1) | ((lv <= g_lane_own ? 1 : 0) << 1), spec, stamp);
   else
-    k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc, v & 1,
-                                        spec, stamp);
+    k_lane<false><<<grid, 32, pool, s>>>(P, pts, n, lv, j0, j1, err, static_cast<int>(pool), jpc,
+                                        (v & 1) | ((lv <= g_lane_own ? 1 : 0) << 1), spec, stamp);
   if (cfg) *cfg = LaneCfg{v, r, pool};
   return 0;
 }

@@ -46,6 +46,8 @@ ROUTES = {
                         "lane_max_level": 40},
     "lane_staged_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
                                "lane_max_level": 40, "lane_xyz_kb": 200, "lane_stage": 1},
+    "lane_own_everywhere": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
+                            "lane_max_level": 40, "lane_own": 40},
     "lane_events_staged": {"tpj_min_jobs": 1, "big_kin": BIG_OFF, "mini_tiny_ctas": 0,
                            "lane_max_level": 40, "lane_stage": 1},
     "warp_everywhere": {"tpj_min_jobs": BIG_OFF, "big_kin": BIG_OFF, "leaf_b": 0, "mini": 0},
@@ -136,6 +138,7 @@ KNOB_CHOICES = {
     "tpj_split": [0, 1, 2],
     "tpj_xyz_ctas": [0, 592],
     "tpj_cap_level": [0, 6, 40],
+    "lane_own": [0, 4, 40],
     "lane": [0, 1],
     "interleave": [0, 1],
 }
