@@ -11,5 +11,8 @@ cap() {  # name config skip (k_mini launches of one hull x 2 hulls)
 }
 cap mini_c4_l20 C4 23
 cap mini_c4_l24 C4 27
-cap mini_c2_l20 C2 23
+# C2's top level runs on the huge variant: pick it by its demangled name
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k "regex:16384" -s 3 -c 1 -o $out/mini_c2_l20 python tools/one_hull.py C2 2 > $out/mini_c2_l20.log 2>&1
+echo "mini_c2_l20 rc=$?" | tee -a $out/status.txt
 cap mini_c3_l9 C3 10
