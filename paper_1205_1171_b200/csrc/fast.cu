@@ -1683,6 +1683,7 @@ struct LevelRec {
   long long pool2 = 0;  // a split lane-per-job level: the big pool (0: not split)
   int ogrid = 0;        // ... and the big-pool (or mini list) launch's grid
   int mini = -1;        // a hybrid level: the mini variant of the large CTAs' jobs
+  long long big_kin = -1, big_pts = -1;  // a pipeline level: its measured totals (checked on replay)
 };
 struct PlanKey {
   int dev;
@@ -2014,7 +2015,7 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
       cudaMemsetAsync(spec, 0, sizeof(long long), s);
       const int lv_start = lv;
       for (const LevelRec &r : plan) {
-        if (r.lv != lv || lv > lv_hi || r.kind == REC_BIG) break;
+        if (r.lv != lv || lv > lv_hi) break;
         if (lv > lv_lo) check(P, lv - 1, spec);
         const long long j0 = p0 >> lv, j1 = (p1 + (1ll << lv) - 1) >> lv;
         // the level's first kernel writes its start stamp (no extra launch)
@@ -2023,7 +2024,17 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
         void *e0 = h3d_profiling() ? h3d_prof_begin(s) : nullptr;
         int tag = lv;
         long long rc = 0;
-        if (r.kind == REC_MINI) {
+        if (r.kind == REC_BIG) {
+          // the pipeline with the recorded totals (checked on the device);
+          // a level that no longer fits the scratch resumes measured
+          tag = lv + 4000;
+          if (stp) h3d_stamp_now(s, lv);
+          rc = big_level(P, big_ws, big_bytes, sorted_pts, n, lv, j0, j1, err, s, r.big_kin, r.big_pts, spec);
+          if (rc == 1) {
+            h3d_prof_drop(e0);
+            break;
+          }
+        } else if (r.kind == REC_MINI) {
           tag = lv + 5000;
           rc = mini_level(P, sorted_pts, n, lv, j0, j1, err, s, r.variant, spec, stp, big_ws, big_bytes);
         } else if (r.kind == REC_LANE) {
@@ -2249,7 +2260,10 @@ int64_t h3d_fast_passes_range(const double *sorted_pts, int64_t n, int64_t p0, i
                                      static_cast<long long>(need[11]));
       if (rb < 0) return rb;
       if (rb == 0) {
-        rec.push_back(LevelRec{lv, REC_BIG, 0, 0, 0, 0, LaneCfg{}});
+        LevelRec lr{lv, REC_BIG, 0, 0, 0, 0, LaneCfg{}};
+        lr.big_kin = sumkin;
+        lr.big_pts = static_cast<long long>(need[11]);
+        rec.push_back(lr);
         h3d_prof_end(e0, lv + 4000, 2, s);
       h3d_stamp_route(lv, lv + 4000);
         P = Pass2{P.out0, P.out1, P.in0, P.in1};

@@ -241,7 +241,8 @@ long long big_capacity(long long n);
 // the level does not fit the scratch (caller falls back), or a negative code
 long long big_level(const Pass2 &P, void *big_ws, size_t big_bytes, const double *pts,
                     long long n, int lv, long long j0, long long j1, long long *err,
-                    cudaStream_t s, long long kin_total = -1, long long pts_total = -1);
+                    cudaStream_t s, long long kin_total = -1, long long pts_total = -1,
+                    long long *spec = nullptr);
 
 // one merge level of both passes, one CTA per job, all in shared memory
 // (mini.cu): jobs of at most MINI_N points and MINI_K merged child events
