@@ -964,7 +964,9 @@ int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t 
   *sums_ready = fuse ? 1 : 0;
   h3d_count_launches(5);
   k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, n, w.scan, 16384);
-  for (int stage = 0; stage < 3; ++stage) k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
+  // (grid-stride: 4 CTAs per SM suffice; a stage the head decided returns at once)
+  const unsigned GD = G < 4 * 148 ? G : 4 * 148;
+  for (int stage = 0; stage < 3; ++stage) k_degenerate<<<GD, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
   k_presort_gate<<<1, 1, 0, s>>>(w.flag, w.scan, err);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
@@ -1038,7 +1040,7 @@ int64_t presort_ties_async(const double *pts, int64_t n, double *sorted_pts, int
   h3d_count_launches(5);
   k_degenerate_head<<<1, 1024, 0, s>>>(sorted_pts, n, w.scan, 16384);
   for (int stage = 0; stage < 3; ++stage)
-    k_degenerate<<<G, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
+    k_degenerate<<<G < 4 * 148 ? G : 4 * 148, 256, 0, s>>>(sorted_pts, n, w.scan, stage, 1, n);
   k_ties_gate<<<1, 1, 0, s>>>(w.flag, w.scan, err, perturbed);
   return h3d_check(cudaGetLastError()) ? H3D_E_CUDA : 0;
 }
