@@ -89,6 +89,45 @@ __global__ void k_keys32(const double *__restrict__ pts, long long n,
   }
 }
 
+// k_keys32 with the radix sort's four 8-bit digit histograms accumulated on
+// the way (block histograms in shared memory, one atomic per bin and block):
+// the sort then skips its histogram pass over the keys
+__global__ void __launch_bounds__(256) k_keys32_rshist(const double *__restrict__ pts, long long n,
+                                                      const unsigned long long *__restrict__ mm, unsigned *keys,
+                                                      unsigned *hist) {
+  __shared__ unsigned sh[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  const double lo = key_to_double(mm[0]), hi = key_to_double(mm[1]);
+  const double span = __dsub_rn(hi, lo);
+  const double sc = span > 0.0 ? __ddiv_rn(4294967295.0, span) : 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {  // four loads in flight
+    double x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = pts[3 * (i + q * stride)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned k = fixed_key(x[q], lo, sc);
+      keys[i + q * stride] = k;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+    }
+  }
+  for (; i < n; i += stride) {
+    const unsigned k = fixed_key(pts[3 * i], lo, sc);
+    keys[i] = k;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i2 = threadIdx.x; i2 < 4 * 256; i2 += blockDim.x) {
+    const unsigned c = (&sh[0][0])[i2];
+    if (c) atomicAdd(hist + i2, c);
+  }
+}
+
 // runs of equal 32-bit keys: insertion sort by (64-bit order key, index)
 __global__ void k_tiefix(const double *__restrict__ pts, const unsigned *__restrict__ k32,
                          int *vals, long long n, int *flag) {
@@ -941,11 +980,13 @@ int64_t presort_async(const double *pts, int64_t n, double *sorted_pts, int64_t 
   h3d_count_launches(2);
   k_scan_input<<<G > 1184 ? 1184 : G, 256, 0, s>>>(pts, n, w.flag + 1, w.mm, &w.scan->scale_bits);
   unsigned *k32a = reinterpret_cast<unsigned *>(w.k0), *k32b = reinterpret_cast<unsigned *>(w.k1);
-  k_keys32<<<G, 256, 0, s>>>(pts, n, w.mm, k32a, nullptr);
+  // the keys with the sort's digit histograms (zeroed with its tickets)
+  cudaMemsetAsync(w.prim_tmp, 0, 8 * prim::RS_BINS * sizeof(unsigned) + 256, s);
+  k_keys32_rshist<<<G > 1184 ? 1184 : G, 256, 0, s>>>(pts, n, w.mm, k32a, static_cast<unsigned *>(w.prim_tmp));
   bool alt = false;
-  h3d_count_launches(5);
+  h3d_count_launches(4);
   if (h3d_check(prim::rs_sort_pairs<unsigned>(w.prim_tmp, w.prim_bytes, k32a, w.v0, k32b, w.v1, n, 0, 32, &alt,
-                                              s, true)))
+                                              s, true, true)))
     return H3D_E_CUDA;
   int *vs = alt ? w.v1 : w.v0;
   h3d_count_launches(2);

@@ -266,9 +266,12 @@ inline size_t rs_temp_bytes(long long n) {
 // (v0 is not read, only used as the ping-pong buffer).  Returns a CUDA
 // error code.
 template <typename K>
+// hist_ready: the caller zeroed the histogram / ticket words at the front of
+// tmp (rs_hist_bytes) and accumulated the digit histograms of k0 into them
+// (e.g. while writing the keys) -- no histogram pass here
 inline cudaError_t rs_sort_pairs(void *tmp, size_t tmp_bytes, K *k0, int *v0, K *k1, int *v1, long long n,
                                  int begin_bit, int end_bit, bool *in_alt, cudaStream_t s,
-                                 bool iota_vals = false) {
+                                 bool iota_vals = false, bool hist_ready = false) {
   *in_alt = false;
   if (n <= 0 || end_bit <= begin_bit) return cudaSuccess;
   if (tmp_bytes < rs_temp_bytes<K>(n)) return cudaErrorInvalidValue;
@@ -278,11 +281,14 @@ inline cudaError_t rs_sort_pairs(void *tmp, size_t tmp_bytes, K *k0, int *v0, K 
       reinterpret_cast<unsigned long long *>(static_cast<char *>(tmp) + 8 * RS_BINS * sizeof(unsigned) + 256);
   const int passes = (end_bit - begin_bit + 7) / 8;
   const long long tiles = (n + rs_tile<K>() - 1) / rs_tile<K>();
-  cudaError_t e = cudaMemsetAsync(tmp, 0, 8 * RS_BINS * sizeof(unsigned) + 256, s);
-  if (e != cudaSuccess) return e;
-  long long hg = (n + 255) / 256;
-  if (hg > 148 * 8) hg = 148 * 8;
-  k_rs_hist<K><<<static_cast<unsigned>(hg), 256, 0, s>>>(k0, n, begin_bit, end_bit, hist);
+  cudaError_t e = cudaSuccess;
+  if (!hist_ready) {
+    e = cudaMemsetAsync(tmp, 0, 8 * RS_BINS * sizeof(unsigned) + 256, s);
+    if (e != cudaSuccess) return e;
+    long long hg = (n + 255) / 256;
+    if (hg > 148 * 8) hg = 148 * 8;
+    k_rs_hist<K><<<static_cast<unsigned>(hg), 256, 0, s>>>(k0, n, begin_bit, end_bit, hist);
+  }
   K *ka = k0, *kb = k1;
   int *va = v0, *vb = v1;
   bool alt = false;
