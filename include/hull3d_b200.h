@@ -207,7 +207,7 @@ int64_t h3d_orient_remap_ex(const double *sorted_pts, int64_t n,
  * merged child log size), "big_total" (or half that log size with this many
  * child events in the level), "big_max_jobs", "leaf_b" (levels 1..B fused: 3
  * or 4; 0-2 = off), "lane" / "lane_max_level" / "lane_xyz_kb" / "lane_stage"
- * (the lane.cu kernel), "tpj_min_jobs", "tpj_xyz_kb", "tpj_xyz_ctas",
+ * / "lane_own" / "lane_pf1" / "lane_pf2" (the lane.cu kernel), "tpj_min_jobs", "tpj_xyz_kb", "tpj_xyz_ctas",
  * "tpj_max_level", "tpj_cap_level" (the 128-register build up to this
  * level), "tpj_split" (split / hybrid lane-per-job levels; 2 = split every
  * level, tests), "mini" (0/1: the one-CTA-per-job merges), "mini_ctas",

@@ -1741,6 +1741,8 @@ void load_env_once() {
   if (const char *e = getenv("H3D_INTERLEAVE")) g_interleave = atoi(e) ? 1 : 0;
   if (const char *e = getenv("H3D_TPJ_CAP_LEVEL")) g_tpj_cap_level = atoi(e);
   if (const char *e = getenv("H3D_TPJ_SPLIT")) g_tpj_split = atoi(e);
+  if (const char *e = getenv("H3D_LANE_PF1")) g_lane_pf1 = atoi(e);
+  if (const char *e = getenv("H3D_LANE_PF2")) g_lane_pf2 = atoi(e);
   g_leaf_b = leaf_depth(g_leaf_b);
 }
 
@@ -1883,6 +1885,8 @@ int64_t h3d_tune(const char *name, int64_t value) {
   else if (k == "lane_xyz_kb") { old = g_lane_xyz_max / 1024; if (value >= 0) g_lane_xyz_max = value * 1024; }
   else if (k == "lane_stage") { old = g_lane_stage; if (value >= 0) g_lane_stage = value ? 1 : 0; }
   else if (k == "lane_own") { old = g_lane_own; if (value >= 0) g_lane_own = static_cast<int>(value); }
+  else if (k == "lane_pf1") { old = g_lane_pf1; if (value >= 0) g_lane_pf1 = static_cast<int>(value); }
+  else if (k == "lane_pf2") { old = g_lane_pf2; if (value >= 0) g_lane_pf2 = static_cast<int>(value); }
   else if (k == "tpj_max_level") { old = kTpjMaxLevel; if (value >= 0) kTpjMaxLevel = static_cast<int>(value); }
   return old;
 }

@@ -263,6 +263,7 @@ long long lane_level(const Pass2 &P, const double *pts, long long n, int lv, lon
 extern long long g_lane_xyz_max;  // lane.cu knobs
 extern int g_lane_stage;
 extern int g_lane_own;
+extern int g_lane_pf1, g_lane_pf2;
 
 // variant 3 (huge): <= kMiniHugePoints / kMiniHugeEvents per job, the job's
 // arrays in global-memory slots of gscratch (returns 1 when they do not fit)

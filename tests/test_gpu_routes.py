@@ -139,6 +139,8 @@ KNOB_CHOICES = {
     "tpj_xyz_ctas": [0, 592],
     "tpj_cap_level": [0, 6, 40],
     "lane_own": [0, 4, 40],
+    "lane_pf1": [0, 4, 40],
+    "lane_pf2": [0, 5, 40],
     "lane": [0, 1],
     "interleave": [0, 1],
 }
