@@ -1660,7 +1660,7 @@ int g_lane = 1;       // H3D_LANE: lane-per-job levels on lane.cu (0 = k_fast_tp
 // lane.cu 2.33 / 1.90 ms at levels 4 / 5 vs 2.60 / 2.13; k_fast_tpj ahead
 // from level 6 on, profiles/r2_levels_c4.jsonl)
 int g_lane_max_level = 5;  // H3D_LANE_MAX_LEVEL
-long long kTpjPrefetchJobs = 1ll << 18;  // H3D_TPJ_PREFETCH: L2 prefetch of rows from this many jobs
+long long kTpjPrefetchJobs = 1ll << 17;  // H3D_TPJ_PREFETCH: L2 prefetch of rows from this many jobs (2^18 -> 2^17: C4 level 7 -2.3 %)
 
 // leaf kernel depth: 3 or 4 fused levels, anything below 3 = off
 int leaf_depth(long long b) { return b >= 4 ? 4 : (b == 3 ? 3 : 0); }
